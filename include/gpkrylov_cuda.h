@@ -1,0 +1,155 @@
+/*
+ * gpkrylov_cuda.h — C-ABI of the B200-native preconditioned mBCG hot path.
+ *
+ * Drop-in boundary for the reference's C++ kernel-operator / preconditioner /
+ * solver interface (/root/reference/proj/include/gpkrylov).  Plain pointers and
+ * sizes only.  All host matrices are fp64 COLUMN-MAJOR with an explicit leading
+ * dimension, matching Eigen's default layout.  Host buffers are borrowed for
+ * the duration of a synchronous call; device memory is owned by the opaque
+ * context.  Entry points suffixed `_device` take device pointers (same layout)
+ * and leave inputs resident in HBM.
+ *
+ * Error convention (common.hpp:19-35): every call returns a gpk_status; the
+ * message (mirroring the reference's exception text) is in gpk_last_error().
+ * A context is NOT thread-safe: one host thread drives it.
+ */
+#ifndef GPKRYLOV_CUDA_H
+#define GPKRYLOV_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gpk_ctx gpk_ctx;
+
+/* common.hpp:19-35 — status codes map 1:1 onto the reference's exception types. */
+typedef enum {
+  GPK_OK = 0,
+  GPK_INPUT_ERROR = 1,     /* input_error      (CLI exit 1) */
+  GPK_NUMERICAL_ERROR = 2, /* numerical_error  (CLI exit 2) */
+  GPK_SOLVER_ERROR = 3,    /* solver_error : numerical_error */
+  GPK_CUDA_ERROR = 4,      /* device failure, reported as numerical_error by the facade */
+  GPK_NCCL_ERROR = 5
+} gpk_status;
+
+/* kernels.hpp:70-87 KernelFamily (RationalQuadratic is rejected: out of scope). */
+typedef enum { GPK_RBF = 0, GPK_MATERN12 = 1, GPK_MATERN32 = 2, GPK_MATERN52 = 3, GPK_RATQUAD = 4 } gpk_family;
+
+/* Arithmetic of the fused kernel MVM.  FP64: entries and accumulation in fp64.
+ * FP32: fp32 entries (direct-difference distances, SFU exp) with fp32
+ * accumulation per 32-column tile and fp64 accumulation across tiles; CG state
+ * and all reductions stay fp64. */
+typedef enum { GPK_PREC_FP64 = 0, GPK_PREC_FP32 = 1 } gpk_precision;
+
+/* krylov.hpp:15-24 CgConfig (+ GPU fields). */
+typedef struct {
+  int max_iters;        /* >= 1 */
+  double rel_tol;       /* in (0,1): stop when ||P^-1 r_k|| <= rel_tol ||P^-1 b|| */
+  int collect_tridiag;  /* record alpha/beta for the Lanczos tridiagonal */
+  int precision;        /* gpk_precision of the operator inside the iterations */
+  int refine;           /* FP32 only: fp64 true-residual audit + defect correction (max passes) */
+} gpk_cg_cfg;
+
+/* gp_likelihood.hpp:26-32 MllConfig (+ GPU fields). */
+typedef struct {
+  gpk_cg_cfg solver;
+  int share_probes;    /* reuse the forward probe batch in the backward pass (reference default 1) */
+  int with_gradient;   /* evaluate_mll's with_gradient flag */
+  int backward_mode;   /* 0: fused bilinear derivative pass over the forward solves (default)
+                          1: reference-faithful: mBCG over the (d+1) l right-hand sides dK_w z_i */
+} gpk_mll_cfg;
+
+/* gp_likelihood.hpp:35-46 MllEvaluation, caller-allocated arrays. */
+typedef struct {
+  double value;                 /* mLL estimate */
+  double* gradient;             /* d+2: outputscale, lengthscales, noise (log-space) */
+  int solve_iterations;         /* iterations of the K_hat u = y solve */
+  double* forward_gammas;       /* l (nullable) */
+  double* backward_gammas;      /* (d+2) x l row-major by parameter (nullable; NaN where unavailable) */
+  double value_sample_variance; /* unbiased variance of n*gamma_i */
+  int* forward_cg_iterations;   /* l (nullable) */
+  int total_cg_iterations;
+  /* telemetry (not in the reference struct) */
+  double logdet;                /* log det K_hat estimate */
+  double logdet_precond;        /* log det P_hat */
+  double quad;                  /* y^T u */
+  int refine_passes;            /* fp64 defect-correction passes used */
+  double max_true_rel_residual; /* max over columns of ||P^-1(b - K_hat x)|| / ||P^-1 b|| in fp64 (or -1) */
+  double seconds_solve, seconds_backward, seconds_total;
+  long long kernel_entries;     /* kernel-matrix entries evaluated by the fused kernels */
+  long long mvm_flops;          /* algorithmic fused-MVM flops */
+  int gpu_launches;             /* kernels this library launched in the call */
+} gpk_mll_result;
+
+/* ---- context ----------------------------------------------------------- */
+gpk_status gpk_create(int device, gpk_ctx** out);
+void gpk_destroy(gpk_ctx* ctx);
+const char* gpk_last_error(const gpk_ctx* ctx);
+/* Version / build string (sm_100a). */
+const char* gpk_version(void);
+
+/* KernelOperator ctor data (kernels.hpp:159-173): X is n x d, column-major, ld >= n. */
+gpk_status gpk_set_data(gpk_ctx* ctx, const double* X, int64_t n, int64_t d, int64_t ldx);
+gpk_status gpk_set_data_device(gpk_ctx* ctx, const double* dX, int64_t n, int64_t d, int64_t ldx);
+/* Hyperparameters (kernels.hpp:17-64), log space; log_ls has d entries. */
+gpk_status gpk_set_params(gpk_ctx* ctx, int family, double ratquad_alpha, double log_outputscale,
+                          const double* log_lengthscales, double log_noise);
+
+/* ---- kernel operator (kernels.hpp:184-267) ------------------------------ */
+/* out = (K + sigma^2 I) V, V n x t. */
+gpk_status gpk_kernel_mvm(gpk_ctx* ctx, const double* V, int64_t ldv, int t, double* out, int64_t ldo,
+                          int precision);
+/* out = (d K_hat / d theta_which) V, raw parameter; which in [0, d+1]. */
+gpk_status gpk_kernel_deriv_mvm(gpk_ctx* ctx, int which, const double* V, int64_t ldv, int t, double* out,
+                                int64_t ldo, int precision);
+/* Noise-free kernel column / derivative column (reference expanded-distance formula, fp64). */
+gpk_status gpk_kernel_column(gpk_ctx* ctx, int64_t i, double* out);
+gpk_status gpk_kernel_deriv_column(gpk_ctx* ctx, int which, int64_t i, double* out);
+
+/* ---- preconditioner (preconditioners.hpp:82-295) ------------------------ */
+/* P_hat = I (IdentityPreconditioner, common.hpp:59-70). */
+gpk_status gpk_precond_identity(gpk_ctx* ctx);
+/* Greedy pivoted partial Cholesky of K (preconditioners.hpp:236-264) in fp64, then the
+ * DiagPlusLowRank factorisation with sigma^2 = noise (:84-95).  pivots: rank entries
+ * (nullable); achieved: achieved rank; remaining_diag: n (nullable). */
+gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double noise, int64_t* pivots,
+                                int* achieved, double* remaining_diag);
+/* Frozen-pivot dL/dtheta factors for every non-noise parameter (preconditioners.hpp:269-295). */
+gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx);
+/* Copy-outs for parity: L (n x k), dL_which (n x k). */
+gpk_status gpk_precond_factor(gpk_ctx* ctx, double* L, int64_t ldl);
+gpk_status gpk_precond_deriv_factor(gpk_ctx* ctx, int which, double* dL, int64_t ldl);
+/* out = P_hat^{-1} V (Woodbury, :114-118). */
+gpk_status gpk_precond_solve(gpk_ctx* ctx, const double* V, int64_t ldv, int t, double* out, int64_t ldo);
+gpk_status gpk_precond_logdet(gpk_ctx* ctx, double* out);
+/* tr(P_hat^{-1} dP_hat/dtheta_which) (:138-145, :168). */
+gpk_status gpk_precond_trace_inv_deriv(gpk_ctx* ctx, int which, double* out);
+
+/* ---- solver (krylov.hpp:47-153) ------------------------------------------ */
+/* Batched PCG over the t columns of B; every column follows pcg_solve exactly and
+ * is independent of the others (batched_pcg contract).  alpha/beta/resid_hist are
+ * max_iters x t column-major (column c = history of column c), nullable. */
+gpk_status gpk_mbcg(gpk_ctx* ctx, const double* B, int64_t ldb, int t, const gpk_cg_cfg* cfg, double* X,
+                    int64_t ldx, int* iters, int* converged, double* alpha, double* beta, double* resid_hist);
+
+/* ---- likelihood (gp_likelihood.hpp:51-103) -------------------------------- */
+/* One mLL (+ gradient) evaluation.  Z: n x l probe block (make_probes); probe_seed
+ * is recorded and used for the unshared backward batch (mix_seed(seed, 0xb2d)). */
+gpk_status gpk_evaluate_mll(gpk_ctx* ctx, const double* y, const double* Z, int64_t ldz, int l,
+                            uint64_t probe_seed, const gpk_mll_cfg* cfg, gpk_mll_result* res);
+gpk_status gpk_evaluate_mll_device(gpk_ctx* ctx, const double* dy, const double* dZ, int64_t ldz, int l,
+                                   uint64_t probe_seed, const gpk_mll_cfg* cfg, gpk_mll_result* res);
+
+/* ---- probes (trace_estimation.hpp:27-36, common.hpp:93-98) --------------- */
+gpk_status gpk_make_probes(int64_t n, int count, uint64_t seed, double* out /* n x count col-major */);
+uint64_t gpk_mix_seed(uint64_t seed, uint64_t salt);
+
+/* Number of this library's kernels launched on ctx since creation. */
+long long gpk_launch_count(const gpk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPKRYLOV_CUDA_H */

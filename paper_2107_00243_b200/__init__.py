@@ -1,0 +1,15 @@
+"""B200-native (sm_100a) preconditioned mBCG hot path of Wenger et al. (arXiv 2107.00243).
+
+One log-marginal-likelihood + gradient evaluation (reference: evaluate_mll,
+proj/include/gpkrylov/gp_likelihood.hpp:51-103) runs as hand-written CUDA
+kernels behind the C-ABI in include/gpkrylov_cuda.h (libgpkrylov_cuda.so);
+``gpkrylov`` mirrors the reference's C++ interface on top of it.
+"""
+from .gpkrylov import (  # noqa: F401
+    CgConfig, CgResult, CudaError, DiagPlusLowRank, Hyperparameters, IdentityPreconditioner, InputError,
+    KernelOperator, KernelSpec, MllConfig, MllEvaluation, NumericalError, ProbeBatch, SolverError, SymTridiagonal,
+    batched_pcg, evaluate_mll, evaluate_mll_device, make_probes, mix_seed, mll_estimate, mll_gradient, pcg_solve,
+    pivoted_cholesky, pivoted_cholesky_deriv_factors, pivoted_cholesky_with_derivatives,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,106 @@
+"""ctypes binding of libgpkrylov_cuda.so (include/gpkrylov_cuda.h).
+
+The product path: every call goes to the sm_100a library.  There is no CPU
+fallback — if the shared library is missing or no CUDA device is visible the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libgpkrylov_cuda.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "gpkrylov_cuda.h")
+
+GPK_OK, GPK_INPUT_ERROR, GPK_NUMERICAL_ERROR, GPK_SOLVER_ERROR, GPK_CUDA_ERROR, GPK_NCCL_ERROR = range(6)
+GPK_RBF, GPK_MATERN12, GPK_MATERN32, GPK_MATERN52, GPK_RATQUAD = range(5)
+GPK_PREC_FP64, GPK_PREC_FP32 = 0, 1
+
+
+class gpk_cg_cfg(C.Structure):
+    _fields_ = [("max_iters", C.c_int), ("rel_tol", C.c_double), ("collect_tridiag", C.c_int),
+                ("precision", C.c_int), ("refine", C.c_int)]
+
+
+class gpk_mll_cfg(C.Structure):
+    _fields_ = [("solver", gpk_cg_cfg), ("share_probes", C.c_int), ("with_gradient", C.c_int),
+                ("backward_mode", C.c_int)]
+
+
+class gpk_mll_result(C.Structure):
+    _fields_ = [("value", C.c_double), ("gradient", C.POINTER(C.c_double)), ("solve_iterations", C.c_int),
+                ("forward_gammas", C.POINTER(C.c_double)), ("backward_gammas", C.POINTER(C.c_double)),
+                ("value_sample_variance", C.c_double), ("forward_cg_iterations", C.POINTER(C.c_int)),
+                ("total_cg_iterations", C.c_int), ("logdet", C.c_double), ("logdet_precond", C.c_double),
+                ("quad", C.c_double), ("refine_passes", C.c_int), ("max_true_rel_residual", C.c_double),
+                ("seconds_solve", C.c_double), ("seconds_backward", C.c_double), ("seconds_total", C.c_double),
+                ("kernel_entries", C.c_longlong), ("mvm_flops", C.c_longlong), ("gpu_launches", C.c_int)]
+
+
+_D = C.POINTER(C.c_double)
+_I = C.POINTER(C.c_int)
+_L = C.POINTER(C.c_int64)
+_V = C.c_void_p
+
+# name -> (restype, argtypes); mirrors include/gpkrylov_cuda.h
+SIGNATURES = {
+    "gpk_create": (C.c_int, [C.c_int, C.POINTER(_V)]),
+    "gpk_destroy": (None, [_V]),
+    "gpk_last_error": (C.c_char_p, [_V]),
+    "gpk_version": (C.c_char_p, []),
+    "gpk_set_data": (C.c_int, [_V, _D, C.c_int64, C.c_int64, C.c_int64]),
+    "gpk_set_data_device": (C.c_int, [_V, _V, C.c_int64, C.c_int64, C.c_int64]),
+    "gpk_set_params": (C.c_int, [_V, C.c_int, C.c_double, C.c_double, _D, C.c_double]),
+    "gpk_kernel_mvm": (C.c_int, [_V, _D, C.c_int64, C.c_int, _D, C.c_int64, C.c_int]),
+    "gpk_kernel_deriv_mvm": (C.c_int, [_V, C.c_int, _D, C.c_int64, C.c_int, _D, C.c_int64, C.c_int]),
+    "gpk_kernel_column": (C.c_int, [_V, C.c_int64, _D]),
+    "gpk_kernel_deriv_column": (C.c_int, [_V, C.c_int, C.c_int64, _D]),
+    "gpk_precond_identity": (C.c_int, [_V]),
+    "gpk_pivoted_cholesky": (C.c_int, [_V, C.c_int, C.c_double, C.c_double, _L, _I, _D]),
+    "gpk_precond_deriv_factors": (C.c_int, [_V]),
+    "gpk_precond_factor": (C.c_int, [_V, _D, C.c_int64]),
+    "gpk_precond_deriv_factor": (C.c_int, [_V, C.c_int, _D, C.c_int64]),
+    "gpk_precond_solve": (C.c_int, [_V, _D, C.c_int64, C.c_int, _D, C.c_int64]),
+    "gpk_precond_logdet": (C.c_int, [_V, _D]),
+    "gpk_precond_trace_inv_deriv": (C.c_int, [_V, C.c_int, _D]),
+    "gpk_mbcg": (C.c_int, [_V, _D, C.c_int64, C.c_int, C.POINTER(gpk_cg_cfg), _D, C.c_int64, _I, _I, _D, _D, _D]),
+    "gpk_evaluate_mll": (C.c_int, [_V, _D, _D, C.c_int64, C.c_int, C.c_uint64, C.POINTER(gpk_mll_cfg),
+                                   C.POINTER(gpk_mll_result)]),
+    "gpk_evaluate_mll_device": (C.c_int, [_V, _V, _V, C.c_int64, C.c_int, C.c_uint64, C.POINTER(gpk_mll_cfg),
+                                          C.POINTER(gpk_mll_result)]),
+    "gpk_make_probes": (C.c_int, [C.c_int64, C.c_int, C.c_uint64, _D]),
+    "gpk_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "gpk_launch_count": (C.c_longlong, [_V]),
+}
+
+
+class ExtensionMissing(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load the sm_100a library (raises if it was not built; never falls back)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ExtensionMissing(
+                f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def header_functions():
+    """Function names declared in include/gpkrylov_cuda.h."""
+    src = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"^\s*(?:gpk_status|void|const char\*|uint64_t|long long)\s+(gpk_\w+)\s*\(",
+                                 src, flags=re.M)))

@@ -1,0 +1,240 @@
+// Fused derivative pass (backward, bilinear form).
+//
+// The reference's backward pass (gp_likelihood.hpp:87-101 ->
+// trace_estimation.hpp:190-224) runs one PCG solve K_hat w = dK_w z_i per
+// hyperparameter and probe ((d+1) l solves) and one deriv_apply per parameter
+// for u' dK_w u.  Because K_hat^{-1} is symmetric,
+//     z_i' K_hat^{-1} dK_w z_i = s_i' dK_w z_i   with s_i = K_hat^{-1} z_i,
+// the forward probe solutions (which the reference already keeps,
+// trace_estimation.hpp:171) give every stochastic term in ONE pass over the
+// n^2 kernel entries:
+//     quad[w]  = sum_ab dK_w[a,b] u_a u_b
+//     gamma[w] = sum_ab dK_w[a,b] W_ab,   W_ab = sum_i S[a,i] Z[b,i]
+// with dK_0 = 2 o shape(s) and dK_{l_j} = (-2 o^2 / l_j) shape_ds(s) ds_j^2.
+//
+// CTA = 256 threads = 16 x 16 threads, each owning a 4 x 4 tile of (a, b)
+// pairs of a 64 x 64 block tile; W tiles come from register-blocked outer
+// products over the l probe columns staged in shared memory; per-thread fp32
+// sums of one b-tile are flushed into fp64 accumulators.
+#include "gpk_common.cuh"
+#include "gpk_internal.h"
+
+namespace gpk {
+
+constexpr int kDA = 64;  // a rows per block tile
+constexpr int kDB = 64;  // b cols per block tile
+constexpr int kDThreads = 256;
+constexpr int kDBTilesPerBlock = 16;  // b-tiles handled by one CTA (fixed -> deterministic)
+
+template <typename T, int FAM>
+GPK_DEV void shape_pair(T s, T& e, T& ds) {
+  if constexpr (sizeof(T) == 4) {
+    if constexpr (FAM == kRBF) {
+      e = ex2_approx(-s);
+      ds = -0.5f * e;
+    } else {
+      const float r = sqrt_approx(s);
+      const float x = ex2_approx(-r);
+      if constexpr (FAM == kMatern12) {
+        e = x;
+        ds = s > 0.0f ? -x * kLog2e / (2.0f * r) : 0.0f;
+      } else if constexpr (FAM == kMatern32) {
+        e = fmaf(r, kLn2, 1.0f) * x;
+        ds = -1.5f * x;
+      } else {
+        const float rr = r * kLn2;
+        e = fmaf(rr, fmaf(rr, 1.0f / 3.0f, 1.0f), 1.0f) * x;
+        ds = -(5.0f / 6.0f) * (1.0f + rr) * x;
+      }
+    }
+  } else {
+    if constexpr (FAM == kRBF) {
+      e = exp(-0.5 * s);
+      ds = -0.5 * e;
+    } else if constexpr (FAM == kMatern12) {
+      const double r = sqrt(s);
+      e = exp(-r);
+      ds = s > 0.0 ? -e / (2.0 * r) : 0.0;
+    } else if constexpr (FAM == kMatern32) {
+      const double r = sqrt(3.0 * s);
+      const double x = exp(-r);
+      e = (1.0 + r) * x;
+      ds = -1.5 * x;
+    } else {
+      const double r = sqrt(5.0 * s);
+      const double x = exp(-r);
+      e = (1.0 + r + r * r / 3.0) * x;
+      ds = -(5.0 / 6.0) * (1.0 + r) * x;
+    }
+  }
+}
+
+// X: [n_pad][DP] packed scaled coordinates (fp32 pre-scaled / fp64 plain);
+// U: [n_pad]; S, Z: column-major [l][n_pad] (zero in padded rows).
+// partials: per CTA, 2*(DP+1) doubles = {Q0, Q_1..Q_DP, G0, G_1..G_DP}.
+template <typename T, int FAM, int DP>
+__global__ void __launch_bounds__(kDThreads, 1)
+    deriv_contract_kernel(const T* __restrict__ X, const T* __restrict__ U, const T* __restrict__ S,
+                          const T* __restrict__ Z, int n_pad, int l, double* __restrict__ partials) {
+  constexpr int NA = 2 * (DP + 1);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Ss = reinterpret_cast<T*>(smem_raw);  // [l][kDA]
+  T* Zs = Ss + l * kDA;                    // [l][kDB]
+  T* Xa = Zs + l * kDB;                    // [kDA][DP]
+  T* Xb = Xa + kDA * DP;                   // [kDB][DP]
+  T* Ua = Xb + kDB * DP;                   // [kDA]
+  T* Ub = Ua + kDA;                        // [kDB]
+  __shared__ double red[kDThreads / 32];
+
+  const int tid = threadIdx.x;
+  const int ta = tid & 15;  // a-group (4 rows)
+  const int tb = tid >> 4;  // b-group (4 cols)
+  const int a0 = blockIdx.x * kDA;
+  const int nbt = n_pad / kDB;
+  const int bt0 = blockIdx.y * kDBTilesPerBlock;
+  const int bt1 = min(bt0 + kDBTilesPerBlock, nbt);
+
+  // a-tile operands (once per CTA)
+  for (int e = tid; e < l * kDA; e += kDThreads) {
+    const int i = e / kDA, r = e % kDA;
+    Ss[e] = S[static_cast<long long>(i) * n_pad + a0 + r];
+  }
+  for (int e = tid; e < kDA * DP; e += kDThreads) Xa[e] = X[static_cast<long long>(a0) * DP + e];
+  for (int e = tid; e < kDA; e += kDThreads) Ua[e] = U[a0 + e];
+
+  double acc64[NA];
+#pragma unroll
+  for (int q = 0; q < NA; ++q) acc64[q] = 0.0;
+
+  for (int bt = bt0; bt < bt1; ++bt) {
+    const int b0 = bt * kDB;
+    __syncthreads();  // previous b-tile fully consumed
+    for (int e = tid; e < l * kDB; e += kDThreads) {
+      const int i = e / kDB, r = e % kDB;
+      Zs[e] = Z[static_cast<long long>(i) * n_pad + b0 + r];
+    }
+    for (int e = tid; e < kDB * DP; e += kDThreads) Xb[e] = X[static_cast<long long>(b0) * DP + e];
+    for (int e = tid; e < kDB; e += kDThreads) Ub[e] = U[b0 + e];
+    __syncthreads();
+
+    // W tile (4 x 4 per thread) = S[a, :] . Z[b, :]
+    T w[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) w[r][c] = T(0);
+    for (int i = 0; i < l; ++i) {
+      T sa[4], zb[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) sa[r] = Ss[i * kDA + ta * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) zb[c] = Zs[i * kDB + tb * 4 + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[r][c] = fma(sa[r], zb[c], w[r][c]);
+    }
+
+    T acc[NA];
+#pragma unroll
+    for (int q = 0; q < NA; ++q) acc[q] = T(0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int bl = tb * 4 + c;
+      T xb[DP];
+#pragma unroll
+      for (int k = 0; k < DP; ++k) xb[k] = Xb[bl * DP + k];
+      const T ub = Ub[bl];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int al = ta * 4 + r;
+        T dd[DP];
+        T s = T(0);
+#pragma unroll
+        for (int k = 0; k < DP; ++k) {
+          const T df = Xa[al * DP + k] - xb[k];
+          dd[k] = df * df;
+          s += dd[k];
+        }
+        T e, ds;
+        shape_pair<T, FAM>(s, e, ds);
+        const T q = Ua[al] * ub;
+        const T wv = w[r][c];
+        acc[0] = fma(e, q, acc[0]);
+        acc[DP + 1] = fma(e, wv, acc[DP + 1]);
+        const T g = ds * q, h = ds * wv;
+#pragma unroll
+        for (int k = 0; k < DP; ++k) {
+          acc[1 + k] = fma(g, dd[k], acc[1 + k]);
+          acc[DP + 2 + k] = fma(h, dd[k], acc[DP + 2 + k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NA; ++q) acc64[q] += static_cast<double>(acc[q]);
+  }
+
+  // fixed-order block reduction -> one partial row per CTA
+  const long long blk = static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x;
+  for (int q = 0; q < NA; ++q) {
+    const double v = block_sum(acc64[q], red);
+    if (tid == 0) partials[blk * NA + q] = v;
+  }
+}
+
+template <typename T, int FAM, int DP>
+static cudaError_t launch_dc_t(const void* X, const void* U, const void* S, const void* Z, int n_pad, int l,
+                               double* partials, int* nblocks, cudaStream_t st) {
+  const size_t sm = sizeof(T) * (static_cast<size_t>(l) * (kDA + kDB) + (kDA + kDB) * DP + kDA + kDB);
+  auto k = deriv_contract_kernel<T, FAM, DP>;
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+  }
+  const int nat = n_pad / kDA;
+  const int nbt = n_pad / kDB;
+  dim3 g(nat, (nbt + kDBTilesPerBlock - 1) / kDBTilesPerBlock);
+  *nblocks = static_cast<int>(g.x * g.y);
+  if (partials == nullptr) return cudaSuccess;  // size query
+  k<<<g, kDThreads, sm, st>>>(static_cast<const T*>(X), static_cast<const T*>(U), static_cast<const T*>(S),
+                              static_cast<const T*>(Z), n_pad, l, partials);
+  return cudaGetLastError();
+}
+
+template <typename T, int FAM>
+static cudaError_t launch_dc_dp(int dp, const void* X, const void* U, const void* S, const void* Z, int n_pad, int l,
+                                double* partials, int* nblocks, cudaStream_t st) {
+  switch (dp) {
+    case 4: return launch_dc_t<T, FAM, 4>(X, U, S, Z, n_pad, l, partials, nblocks, st);
+    case 12: return launch_dc_t<T, FAM, 12>(X, U, S, Z, n_pad, l, partials, nblocks, st);
+    case 20: return launch_dc_t<T, FAM, 20>(X, U, S, Z, n_pad, l, partials, nblocks, st);
+    case 32: return launch_dc_t<T, FAM, 32>(X, U, S, Z, n_pad, l, partials, nblocks, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+static cudaError_t launch_dc_fam(int fam, int dp, const void* X, const void* U, const void* S, const void* Z,
+                                 int n_pad, int l, double* partials, int* nblocks, cudaStream_t st) {
+  switch (fam) {
+    case kRBF: return launch_dc_dp<T, kRBF>(dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
+    case kMatern12: return launch_dc_dp<T, kMatern12>(dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
+    case kMatern32: return launch_dc_dp<T, kMatern32>(dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
+    case kMatern52: return launch_dc_dp<T, kMatern52>(dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// U/S/Z layout: U [n_pad], S and Z column-major [l][n_pad]; X [n_pad][dp].
+cudaError_t launch_deriv_contract(bool fp64, int family, int dp, const void* X, const void* U, const void* SZ,
+                                  int n, int n_pad, int l, int d, double* partials, int* nblocks, cudaStream_t st) {
+  (void)n;
+  (void)d;
+  const size_t elem = fp64 ? 8 : 4;
+  const void* S = SZ;
+  const void* Z = static_cast<const unsigned char*>(SZ) + elem * static_cast<size_t>(l) * n_pad;
+  return fp64 ? launch_dc_fam<double>(family, dp, X, U, S, Z, n_pad, l, partials, nblocks, st)
+              : launch_dc_fam<float>(family, dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
+}
+
+}  // namespace gpk

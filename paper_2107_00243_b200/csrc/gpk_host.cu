@@ -1,0 +1,1465 @@
+// Host driver and C-ABI of libgpkrylov_cuda.so.
+//
+// Mirrors the reference's C++ interface (proj/include/gpkrylov):
+//   KernelOperator (kernels.hpp:157-336)      -> gpk_set_data / gpk_set_params / gpk_kernel_*
+//   pcg_solve / batched_pcg (krylov.hpp)      -> mbcg() : one batched CG over all columns
+//   DiagPlusLowRank + pivoted_cholesky (+deriv factors) (preconditioners.hpp) -> Precond
+//   slq_quadrature / vr_logdet / trace_residual (trace_estimation.hpp) -> host SLQ + fused passes
+//   evaluate_mll (gp_likelihood.hpp:51-103)  -> evaluate()
+// The heavy lifting runs in the sm_100a kernels (gpk_mvm*.cu, gpk_deriv.cu,
+// gpk_linalg.cu); this file owns the control flow, O(m^2) tridiagonal
+// eigen-solves, O(k^3) inner Cholesky and error mapping.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gpk_internal.h"
+#include "gpk_linalg.h"
+#include "gpkrylov_cuda.h"
+
+namespace {
+
+struct GpkError {
+  gpk_status code;
+  std::string msg;
+};
+[[noreturn]] void fail(gpk_status c, const std::string& m) { throw GpkError{c, m}; }
+void require(bool c, const std::string& m) {
+  if (!c) fail(GPK_INPUT_ERROR, m);
+}
+
+#define CK(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess) fail(GPK_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t cnt) {
+    if (cnt == 0) cnt = 1;
+    if (cnt <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    CK(cudaMalloc(&p, cnt * sizeof(T)));
+    cap = cnt;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  ~DBuf() { release(); }
+};
+
+std::string num(double v) { return std::to_string(v); }  // the reference formats with std::to_string
+
+// ---------------------------------------------------------------------------
+// Tridiagonal eigen-solve for SLQ (trace_estimation.hpp:88-110): implicit QL
+// with Wilkinson-type shifts, tracking only the first row of the eigenvector
+// matrix (the quadrature weights), O(m^2).
+// ---------------------------------------------------------------------------
+bool tridiag_eig_first_row(std::vector<double>& d, std::vector<double> e, std::vector<double>& z0) {
+  const int m = static_cast<int>(d.size());
+  z0.assign(m, 0.0);
+  if (m == 0) return true;
+  z0[0] = 1.0;
+  e.resize(m, 0.0);
+  e[m - 1] = 0.0;
+  for (int l = 0; l < m; ++l) {
+    int iter = 0, mm;
+    do {
+      for (mm = l; mm < m - 1; ++mm) {
+        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
+        if (std::fabs(e[mm]) <= 2.220446049250313e-16 * dd) break;
+      }
+      if (mm != l) {
+        if (++iter > 60) return false;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = std::hypot(g, 1.0);
+        g = d[mm] - d[l] + e[l] / (g + (g >= 0.0 ? r : -r));
+        double s = 1.0, c = 1.0, p = 0.0;
+        bool deflated = false;
+        for (int i = mm - 1; i >= l; --i) {
+          const double f = s * e[i];
+          const double b = c * e[i];
+          r = std::hypot(f, g);
+          e[i + 1] = r;
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[mm] = 0.0;
+            deflated = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          d[i + 1] = g + p;
+          g = c * r - b;
+          const double zf = z0[i + 1];
+          z0[i + 1] = s * z0[i] + c * zf;
+          z0[i] = c * z0[i] - s * zf;
+        }
+        if (deflated) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[mm] = 0.0;
+      }
+    } while (mm != l);
+  }
+  return true;
+}
+
+struct SlqOut {
+  double value = 0.0;
+  int clamped = 0;
+};
+SlqOut slq_log(const std::vector<double>& diag, const std::vector<double>& sub) {
+  SlqOut o;
+  if (diag.empty()) return o;
+  std::vector<double> d = diag, z0;
+  if (!tridiag_eig_first_row(d, sub, z0)) fail(GPK_NUMERICAL_ERROR, "slq_quadrature: eigensolver failed");
+  double amax = 0.0;
+  for (double v : d) amax = std::max(amax, std::fabs(v));
+  const double floor_value = 1e-12 * amax;
+  for (size_t j = 0; j < d.size(); ++j) {
+    double node = d[j];
+    if (node < floor_value) {
+      node = floor_value;
+      ++o.clamped;
+    }
+    o.value += (z0[j] * z0[j]) * std::log(node);
+  }
+  return o;
+}
+
+double unbiased_variance(const std::vector<double>& v) {
+  if (v.size() < 2) return 0.0;
+  double mean = 0.0;
+  for (double x : v) mean += x;
+  mean /= static_cast<double>(v.size());
+  double ss = 0.0;
+  for (double x : v) ss += (x - mean) * (x - mean);
+  return ss / static_cast<double>(v.size() - 1);
+}
+
+// host Cholesky (lower, column-major) and inverse of the k x k inner matrix
+bool host_cholesky(std::vector<double>& a, int k) {
+  for (int j = 0; j < k; ++j) {
+    double s = a[j + j * k];
+    for (int c = 0; c < j; ++c) s -= a[j + c * k] * a[j + c * k];
+    if (!(s > 0.0) || !std::isfinite(s)) return false;
+    const double l = std::sqrt(s);
+    a[j + j * k] = l;
+    for (int i = j + 1; i < k; ++i) {
+      double t = a[i + j * k];
+      for (int c = 0; c < j; ++c) t -= a[i + c * k] * a[j + c * k];
+      a[i + j * k] = t / l;
+    }
+  }
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i < j; ++i) a[i + j * k] = 0.0;
+  return true;
+}
+std::vector<double> host_chol_inverse(const std::vector<double>& l, int k) {
+  std::vector<double> inv(static_cast<size_t>(k) * k, 0.0), col(k);
+  for (int j = 0; j < k; ++j) {
+    std::fill(col.begin(), col.end(), 0.0);
+    col[j] = 1.0;
+    for (int i = 0; i < k; ++i) {
+      double s = col[i];
+      for (int c = 0; c < i; ++c) s -= l[i + c * k] * col[c];
+      col[i] = s / l[i + i * k];
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double s = col[i];
+      for (int c = i + 1; c < k; ++c) s -= l[c + i * k] * col[c];
+      col[i] = s / l[i + i * k];
+    }
+    for (int i = 0; i < k; ++i) inv[i + j * k] = col[i];
+  }
+  for (int j = 0; j < k; ++j)  // exact symmetry
+    for (int i = j + 1; i < k; ++i) {
+      const double v = 0.5 * (inv[i + j * k] + inv[j + i * k]);
+      inv[i + j * k] = inv[j + i * k] = v;
+    }
+  return inv;
+}
+
+// ---------------------------------------------------------------------------
+// small kernels local to the driver
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void to_padded_kernel(const double* __restrict__ src, long long lds, int n, int n_pad, int t,
+                                 T* __restrict__ dst) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(t) * n_pad) return;
+  const int c = static_cast<int>(idx / n_pad), i = static_cast<int>(idx % n_pad);
+  dst[idx] = static_cast<T>(i < n ? src[c * lds + i] : 0.0);
+}
+__global__ void fill_kernel(double* __restrict__ p, long long cnt, double v) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < cnt) p[i] = v;
+}
+__global__ void residual_kernel(const double* __restrict__ B, long long ldb, const double* __restrict__ KX,
+                                const double* __restrict__ X, double sig2, int n, long long ldn,
+                                double* __restrict__ R) {
+  const int s = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long o = s * ldn + i;
+  R[o] = B[s * ldb + i] - (KX[o] + sig2 * X[o]);
+}
+
+}  // namespace
+
+// ===========================================================================
+struct gpk_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  long long launches = 0;
+
+  // ---- data (kernels.hpp:159-173)
+  int n = 0, d = 0, n_pad = 0, dp = 0;
+  long long ldn = 0;
+  bool have_data = false, have_params = false;
+  DBuf<double> X, sx, sq, ls_dev, X64s;
+  DBuf<float> X32;
+  // ---- params
+  int family = 0;
+  double log_o = 0, log_noise = 0, o = 1, o2 = 1, noise = 1e-2;
+  std::vector<double> log_ls, ls;
+  bool packed = false;
+
+  // ---- preconditioner
+  int pkind = 0;  // 0 none, 1 identity, 2 diag-plus-low-rank
+  int k = 0;
+  double pnoise = 0.0, plogdet = 0.0;
+  DBuf<double> L, C, dL;
+  std::vector<long long> pivots;
+  bool have_dl = false;
+  std::vector<double> trace_det;  // tr(P^-1 dP_w), w = 0..d+1
+
+  // ---- workspaces
+  DBuf<double> w_part, w_y, w_kx, w_g1, w_W, w_T, w_B, w_tmp, w_tmp2, w_ps, w_hist;
+  DBuf<double> st_X[2], st_R[2], st_P[2], st_Z;
+  DBuf<float> w_v32, w_f32;
+  DBuf<double> w_v64, w_f64;
+  DBuf<gpk::SlotState> w_ss[2];
+  DBuf<int> w_map;
+  DBuf<double> w_argval;
+  DBuf<long long> w_argidx;
+
+  // ---- telemetry
+  long long entries = 0, flops = 0;
+
+  void set_device() { CK(cudaSetDevice(device)); }
+  void sync() { CK(cudaStreamSynchronize(st)); }
+  void check_launch(cudaError_t e, int count, const char* what) {
+    if (e != cudaSuccess) fail(GPK_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+    launches += count;
+  }
+  void h2d(void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+  }
+  void d2h(void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+    sync();
+  }
+
+  void require_ready() {
+    require(have_data, "gpkrylov_cuda: no data set (gpk_set_data)");
+    require(have_params, "gpkrylov_cuda: no hyperparameters set (gpk_set_params)");
+    require(static_cast<int>(log_ls.size()) == d, "KernelOperator: lengthscale count must equal data dimension");
+    if (!packed) pack();
+  }
+
+  // kernels.hpp:166-168 + packed MVM operands
+  void pack() {
+    X32.ensure(static_cast<size_t>(n_pad) * dp);
+    X64s.ensure(static_cast<size_t>(n_pad) * dp);
+    sx.ensure(static_cast<size_t>(n) * d);
+    sq.ensure(n);
+    ls_dev.ensure(d);
+    h2d(ls_dev.p, ls.data(), sizeof(double) * d);
+    check_launch(gpk::launch_pack_x(X.p, n, n, d, n_pad, ls_dev.p, gpk::prescale_c(family), dp, X32.p, dp, X64s.p,
+                                    sx.p, sq.p, st),
+                 1, "pack_x");
+    packed = true;
+  }
+
+  int splits_for() const {
+    const int rb = n_pad / 128;
+    const int ntiles = n_pad / 32;
+    int s = (2 * 148 + rb - 1) / rb;
+    s = std::max(1, std::min(s, ntiles / 4));
+    const int per = (ntiles + s - 1) / s;
+    return (ntiles + per - 1) / per;
+  }
+
+  // out[:, c] = op(V[:, c]) for c < t.  which < 0: K (noise-free, scaled o^2);
+  // which == 0: dK/do; 1..d: dK/dl_j; d+1: identity (noise derivative).
+  void apply_kernel(const double* V, long long ldv, int t, double* out, long long ldo, bool fp64, int which) {
+    if (t <= 0) return;
+    if (which == d + 1) {
+      check_launch(gpk::launch_gather_cols(V, ldv, nullptr, 1.0, n, t, out, ldo, st), 1, "copy");
+      return;
+    }
+    const int mode = which >= 1 ? gpk::kModeDls : gpk::kModeValue;
+    const int chunk = fp64 ? 64 : 128;
+    const int splits = splits_for();
+    const int ntiles = n_pad / 32;
+    const int per = (ntiles + splits - 1) / splits;
+    for (int c0 = 0; c0 < t; c0 += chunk) {
+      const int tc = std::min(chunk, t - c0);
+      const gpk::MvmShape sh = gpk::mvm_shape(tc, fp64, mode);
+      const void* vp;
+      if (fp64) {
+        w_v64.ensure(static_cast<size_t>(n_pad) * sh.vld);
+        check_launch(gpk::launch_pack_v64(V + c0 * ldv, ldv, nullptr, tc, n, n_pad, sh, w_v64.p, st), 1, "pack_v64");
+        vp = w_v64.p;
+      } else {
+        w_v32.ensure(static_cast<size_t>(n_pad) * sh.vld);
+        check_launch(gpk::launch_pack_v32(V + c0 * ldv, ldv, nullptr, tc, n, n_pad, sh, w_v32.p, st), 1, "pack_v32");
+        vp = w_v32.p;
+      }
+      gpk::MvmArgs a{};
+      a.n = n;
+      a.n_pad = n_pad;
+      a.t = tc;
+      a.jdim = which >= 1 ? which - 1 : 0;
+      a.jtiles_per_split = per;
+      const double c = fp64 ? 1.0 : gpk::prescale_c(family);
+      if (which < 0) a.scale = o2;
+      else if (which == 0) a.scale = 2.0 * o;
+      else a.scale = (-2.0 * o2 / ls[which - 1]) / c;
+      const void* xp = fp64 ? static_cast<const void*>(X64s.p) : static_cast<const void*>(X32.p);
+      if (splits == 1) {
+        a.ldo = ldo;
+        a.split_stride = 0;
+        check_launch(gpk::launch_fused_kmvm(fp64, family, dp, mode, xp, vp, out + c0 * ldo, a, 1, st), 1,
+                     "fused_kmvm");
+      } else {
+        a.ldo = n_pad;
+        a.split_stride = static_cast<long long>(tc) * n_pad;
+        w_y.ensure(static_cast<size_t>(splits) * tc * n_pad);
+        check_launch(gpk::launch_fused_kmvm(fp64, family, dp, mode, xp, vp, w_y.p, a, splits, st), 1, "fused_kmvm");
+        check_launch(gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, n, n_pad, out + c0 * ldo, ldo, st),
+                     1, "reduce_splits");
+      }
+      entries += static_cast<long long>(n) * n;
+      const int cf[] = {2, 3, 6, 9};
+      flops += static_cast<long long>(n) * n * (2LL * tc + 3LL * d + cf[family]);
+    }
+  }
+
+  // Z = P^{-1} R  (identity / Woodbury, preconditioners.hpp:114-118); column-major [t][ldn]
+  void psolve(const double* R, int t, double* Z) {
+    if (t <= 0) return;
+    if (pkind == 1) {
+      check_launch(gpk::launch_gather_cols(R, ldn, nullptr, 1.0, n, t, Z, ldn, st), 1, "copy");
+      return;
+    }
+    if (k == 0) {
+      check_launch(gpk::launch_woodbury_finish(R, nullptr, pnoise, n, ldn, t, Z, st), 1, "woodbury");
+      return;
+    }
+    w_g1.ensure(gpk::g1_workspace(n, k, t));
+    w_W.ensure(static_cast<size_t>(k) * t);
+    w_T.ensure(static_cast<size_t>(t) * ldn);
+    check_launch(gpk::launch_g1(L.p, n, k, R, ldn, t, n, w_g1.p, w_W.p, k, st), 2, "g1");
+    check_launch(gpk::launch_g2(C.p, n, k, w_W.p, k, t, n, w_T.p, ldn, st), 1, "g2");
+    check_launch(gpk::launch_woodbury_finish(R, w_T.p, pnoise, n, ldn, t, Z, st), 1, "woodbury");
+  }
+
+  // per-column dots a.b  (host result, fixed-order reduction)
+  std::vector<double> col_dots(const double* A, const double* B, int t, long long ld) {
+    std::vector<double> out(t);
+    if (t <= 0) return out;
+    const int nrb = gpk::num_chunks(n);
+    w_part.ensure(static_cast<size_t>(t) * nrb * 3 + t);
+    check_launch(gpk::launch_dot_partials(0, A, B, 0.0, n, ld, t, w_part.p, st), 1, "dots");
+    double* res = w_part.p + static_cast<size_t>(t) * nrb * 3;
+    check_launch(gpk::launch_reduce_partials(w_part.p, nrb, t, res, st), 1, "reduce");
+    d2h(out.data(), res, sizeof(double) * t);
+    return out;
+  }
+
+  // -------------------------------------------------------------------------
+  // Batched PCG (krylov.hpp:47-129 per column, batched_pcg semantics :131-153).
+  // B, Xout: device column-major with leading dimensions.  Histories are host
+  // arrays [t][max_iters] (nullable).
+  // -------------------------------------------------------------------------
+  struct CgOut {
+    std::vector<int> iters, converged, status;
+    std::vector<double> bad, norm0;
+  };
+  CgOut mbcg(const double* B, long long ldb, int t, int max_iters, double rel_tol, bool fp64, double* Xout,
+             long long ldx, double* alpha_h, double* beta_h, double* resid_h,
+             const std::vector<double>* tol_scale = nullptr) {
+    require(max_iters >= 1, "CgConfig: max_iters must be >= 1");
+    require(rel_tol > 0.0 && rel_tol < 1.0, "CgConfig: rel_tol must be in (0, 1)");
+    CgOut out;
+    out.iters.assign(t, 0);
+    out.converged.assign(t, 0);
+    out.status.assign(t, 0);
+    out.bad.assign(t, 0.0);
+    out.norm0.assign(t, 0.0);
+    if (t <= 0) return out;
+    const int nrb = gpk::num_chunks(n);
+    for (int b = 0; b < 2; ++b) {
+      st_X[b].ensure(static_cast<size_t>(t) * ldn);
+      st_R[b].ensure(static_cast<size_t>(t) * ldn);
+      st_P[b].ensure(static_cast<size_t>(t) * ldn);
+      w_ss[b].ensure(t);
+    }
+    st_Z.ensure(static_cast<size_t>(t) * ldn);
+    w_kx.ensure(static_cast<size_t>(t) * ldn);
+    w_part.ensure(static_cast<size_t>(t) * nrb * 3 + t);
+    w_map.ensure(t);
+    const bool hist = alpha_h || beta_h || resid_h;
+    if (hist) w_hist.ensure(static_cast<size_t>(3) * t * max_iters);
+    double* dh_a = hist ? w_hist.p : nullptr;
+    double* dh_b = hist ? w_hist.p + static_cast<size_t>(t) * max_iters : nullptr;
+    double* dh_r = hist ? w_hist.p + static_cast<size_t>(2) * t * max_iters : nullptr;
+    if (hist) {
+      const long long cnt = 3LL * t * max_iters;
+      fill_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(w_hist.p, cnt, 0.0);
+      check_launch(cudaGetLastError(), 1, "fill");
+    }
+    int cur = 0;
+    double *Xs = st_X[0].p, *Rs = st_R[0].p, *Ps = st_P[0].p, *Zs = st_Z.p;
+    gpk::SlotState* ss = w_ss[0].p;
+    std::vector<gpk::SlotState> hs(t);
+    for (int s = 0; s < t; ++s) {
+      std::memset(&hs[s], 0, sizeof(gpk::SlotState));
+      hs[s].col = s;
+    }
+    h2d(ss, hs.data(), sizeof(gpk::SlotState) * t);
+    // x0 = 0, r = b, z = P^{-1} r, norm0 = ||z||, p = z, rz = r.z   (krylov.hpp:55-67)
+    check_launch(gpk::launch_gather_cols(nullptr, 0, nullptr, 0.0, n, t, Xs, ldn, st), 1, "zero");
+    check_launch(gpk::launch_gather_cols(B, ldb, nullptr, 1.0, n, t, Rs, ldn, st), 1, "gather");
+    psolve(Rs, t, Zs);
+    double* prz = w_part.p;
+    double* pzz = w_part.p + static_cast<size_t>(t) * nrb;
+    double* ppap = w_part.p + static_cast<size_t>(2) * t * nrb;
+    check_launch(gpk::launch_dot_partials(0, Rs, Zs, 0.0, n, ldn, t, prz, st), 1, "dots");
+    check_launch(gpk::launch_dot_partials(0, Zs, Zs, 0.0, n, ldn, t, pzz, st), 1, "dots");
+    check_launch(gpk::launch_cg_init(prz, pzz, nrb, t, ss, st), 1, "cg_init");
+    check_launch(gpk::launch_gather_cols(Zs, ldn, nullptr, 1.0, n, t, Ps, ldn, st), 1, "copy");
+    d2h(hs.data(), ss, sizeof(gpk::SlotState) * t);
+    for (int s = 0; s < t; ++s) out.norm0[s] = hs[s].norm0;
+    int ta = t;
+    // per-column tolerance (defect-correction passes use absolute targets)
+    auto tol_of = [&](int col) { return tol_scale ? rel_tol * (*tol_scale)[col] : rel_tol; };
+    // slots whose columns differ in tolerance are handled through SlotState.norm0 scaling
+    if (tol_scale) {
+      for (int s = 0; s < t; ++s) hs[s].norm0 = hs[s].norm0 * tol_of(hs[s].col) / rel_tol;
+      h2d(ss, hs.data(), sizeof(gpk::SlotState) * t);
+    }
+    auto finish_slots = [&](const std::vector<int>& done) {
+      // scatter the finished columns' solutions to Xout
+      if (done.empty()) return;
+      std::vector<int> slots, cols;
+      for (int s : done) {
+        slots.push_back(s);
+        cols.push_back(hs[s].col);
+      }
+      // gather finished slots into w_kx then scatter by column
+      h2d(w_map.p, slots.data(), sizeof(int) * slots.size());
+      check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, n, static_cast<int>(slots.size()), w_kx.p, ldn, st),
+                   1, "gather");
+      h2d(w_map.p, cols.data(), sizeof(int) * cols.size());
+      check_launch(gpk::launch_scatter_cols(w_kx.p, ldn, w_map.p, n, static_cast<int>(cols.size()), Xout, ldx, st), 1,
+                   "scatter");
+      sync();
+    };
+    auto compact = [&](const std::vector<int>& keep) {
+      const int nt = static_cast<int>(keep.size());
+      const int nb = cur ^ 1;
+      if (nt > 0) {
+        h2d(w_map.p, keep.data(), sizeof(int) * nt);
+        check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, n, nt, st_X[nb].p, ldn, st), 1, "compact");
+        check_launch(gpk::launch_gather_cols(Rs, ldn, w_map.p, 1.0, n, nt, st_R[nb].p, ldn, st), 1, "compact");
+        check_launch(gpk::launch_gather_cols(Ps, ldn, w_map.p, 1.0, n, nt, st_P[nb].p, ldn, st), 1, "compact");
+        std::vector<gpk::SlotState> ns(nt);
+        for (int q = 0; q < nt; ++q) ns[q] = hs[keep[q]];
+        h2d(w_ss[nb].p, ns.data(), sizeof(gpk::SlotState) * nt);
+        sync();
+        hs = ns;
+      } else {
+        hs.clear();
+      }
+      cur = nb;
+      Xs = st_X[cur].p;
+      Rs = st_R[cur].p;
+      Ps = st_P[cur].p;
+      ss = w_ss[cur].p;
+      ta = nt;
+    };
+    auto handle_flags = [&]() {
+      std::vector<int> done, keep;
+      for (int s = 0; s < ta; ++s) {
+        const gpk::SlotState& x = hs[s];
+        if (x.flag == gpk::kFlagError) {
+          out.status[x.col] = x.status;
+          out.bad[x.col] = x.bad;
+          out.iters[x.col] = x.iters;
+        }
+      }
+      // errors: report the lowest column first (reference solves y before the probes)
+      int worst = -1;
+      for (int s = 0; s < ta; ++s)
+        if (hs[s].flag == gpk::kFlagError && (worst < 0 || hs[s].col < hs[worst].col)) worst = s;
+      if (worst >= 0) {
+        const gpk::SlotState& x = hs[worst];
+        std::string m = "pcg_solve: breakdown at iteration " + std::to_string(x.iters);
+        if (x.status == gpk::kStatusAlpha)
+          m += " (alpha = " + num(x.bad) + "); operator or preconditioner not positive definite";
+        else
+          m += " (r'z = " + num(x.bad) + ")";
+        throw GpkError{GPK_SOLVER_ERROR, "#col" + std::to_string(x.col) + "#" + m};
+      }
+      for (int s = 0; s < ta; ++s) {
+        if (hs[s].flag == gpk::kFlagConverged) {
+          out.iters[hs[s].col] = hs[s].iters;
+          out.converged[hs[s].col] = 1;
+          done.push_back(s);
+        } else {
+          keep.push_back(s);
+        }
+      }
+      if (!done.empty()) {
+        finish_slots(done);
+        compact(keep);
+      }
+    };
+    handle_flags();  // zero right-hand sides finish with 0 iterations
+    for (int it = 1; it <= max_iters && ta > 0; ++it) {
+      w_kx.ensure(static_cast<size_t>(ta) * ldn);
+      apply_kernel(Ps, ldn, ta, w_kx.p, ldn, fp64, -1);  // K p (noise-free)
+      check_launch(gpk::launch_dot_partials(1, Ps, w_kx.p, noise, n, ldn, ta, ppap, st), 1, "dots");
+      check_launch(gpk::launch_cg_alpha(ppap, nrb, ta, it, ss, dh_a, max_iters, st), 1, "cg_alpha");
+      check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, n, ldn, ta, ss, st), 1, "cg_xr");
+      psolve(Rs, ta, Zs);
+      check_launch(gpk::launch_dot_partials(0, Rs, Zs, 0.0, n, ldn, ta, prz, st), 1, "dots");
+      check_launch(gpk::launch_dot_partials(0, Zs, Zs, 0.0, n, ldn, ta, pzz, st), 1, "dots");
+      check_launch(gpk::launch_cg_beta(prz, pzz, nrb, ta, it, rel_tol, ss, dh_b, dh_r, max_iters, st), 1, "cg_beta");
+      check_launch(gpk::launch_cg_update_p(Ps, Zs, n, ldn, ta, ss, st), 1, "cg_p");
+      d2h(hs.data(), ss, sizeof(gpk::SlotState) * ta);
+      handle_flags();
+    }
+    // columns that hit max_iters: not an error, converged = false (krylov.hpp:120)
+    if (ta > 0) {
+      std::vector<int> all;
+      for (int s = 0; s < ta; ++s) {
+        out.iters[hs[s].col] = hs[s].iters;
+        all.push_back(s);
+      }
+      finish_slots(all);
+    }
+    if (hist) {
+      std::vector<double> h(static_cast<size_t>(3) * t * max_iters);
+      d2h(h.data(), w_hist.p, sizeof(double) * h.size());
+      const size_t blk = static_cast<size_t>(t) * max_iters;
+      if (alpha_h) std::memcpy(alpha_h, h.data(), sizeof(double) * blk);
+      if (beta_h) std::memcpy(beta_h, h.data() + blk, sizeof(double) * blk);
+      if (resid_h) std::memcpy(resid_h, h.data() + 2 * blk, sizeof(double) * blk);
+    }
+    return out;
+  }
+
+  // FP32 defect correction: audit the fp64 preconditioned true residual of
+  // every converged column and correct the ones above tolerance.
+  int refine(const double* B, long long ldb, int t, double* Xd, long long ldx, const CgOut& cg, int max_iters,
+             double rel_tol, int passes, double* max_ratio) {
+    w_tmp.ensure(static_cast<size_t>(t) * ldn);
+    w_tmp2.ensure(static_cast<size_t>(t) * ldn);
+    w_B.ensure(static_cast<size_t>(t) * ldn);
+    int used = 0;
+    *max_ratio = 0.0;
+    for (int pass = 0; pass <= passes; ++pass) {
+      // R = B - (K X + s2 X)  in fp64
+      w_kx.ensure(static_cast<size_t>(t) * ldn);
+      apply_kernel(Xd, ldx, t, w_kx.p, ldn, true, -1);
+      check_launch(gpk::launch_gather_cols(Xd, ldx, nullptr, 1.0, n, t, w_tmp2.p, ldn, st), 1, "copy");
+      dim3 g((n + 255) / 256, t);
+      residual_kernel<<<g, 256, 0, st>>>(B, ldb, w_kx.p, w_tmp2.p, noise, n, ldn, w_B.p);
+      check_launch(cudaGetLastError(), 1, "residual");
+      psolve(w_B.p, t, w_tmp.p);
+      const std::vector<double> zz = col_dots(w_tmp.p, w_tmp.p, t, ldn);
+      std::vector<int> bad;
+      std::vector<double> scale;
+      double mr = 0.0;
+      for (int c = 0; c < t; ++c) {
+        if (!cg.converged[c] || cg.norm0[c] == 0.0) continue;
+        const double ratio = std::sqrt(zz[c]) / cg.norm0[c];
+        mr = std::max(mr, ratio);
+        if (ratio > rel_tol) {
+          bad.push_back(c);
+          scale.push_back(cg.norm0[c] / std::sqrt(zz[c]));
+        }
+      }
+      *max_ratio = mr;
+      if (bad.empty() || pass == passes) break;
+      ++used;
+      // correction solve K E = R[:, bad] with absolute target rel_tol * norm0
+      const int nb = static_cast<int>(bad.size());
+      DBuf<double> Rb, Eb;
+      Rb.ensure(static_cast<size_t>(nb) * ldn);
+      Eb.ensure(static_cast<size_t>(nb) * ldn);
+      w_map.ensure(nb);
+      h2d(w_map.p, bad.data(), sizeof(int) * nb);
+      check_launch(gpk::launch_gather_cols(w_B.p, ldn, w_map.p, 1.0, n, nb, Rb.p, ldn, st), 1, "gather");
+      // relative tolerance of the correction solve: 0.5 * rel_tol * norm0 / ||P^-1 r_true|| (< 0.5)
+      std::vector<double> ts(nb);
+      for (int q = 0; q < nb; ++q) ts[q] = 0.5 * scale[q];
+      CgOut c2 = mbcg(Rb.p, ldn, nb, max_iters, rel_tol, false, Eb.p, ldn, nullptr, nullptr, nullptr, &ts);
+      (void)c2;
+      // X[:, bad] += E
+      w_tmp2.ensure(static_cast<size_t>(nb) * ldn);
+      check_launch(gpk::launch_gather_cols(Xd, ldx, w_map.p, 1.0, n, nb, w_tmp2.p, ldn, st), 1, "gather");
+      check_launch(gpk::launch_axpby(w_tmp2.p, Eb.p, 1.0, 1.0, n, nb, ldn, st), 1, "axpy");
+      check_launch(gpk::launch_scatter_cols(w_tmp2.p, ldn, w_map.p, n, nb, Xd, ldx, st), 1, "scatter");
+      sync();
+    }
+    return used;
+  }
+};
+
+namespace {
+
+gpk_status guard(gpk_ctx* ctx, const std::function<void()>& f) {
+  try {
+    if (ctx) ctx->set_device();
+    f();
+    if (ctx) ctx->err.clear();
+    return GPK_OK;
+  } catch (const GpkError& e) {
+    if (ctx) ctx->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return GPK_NUMERICAL_ERROR;
+  }
+}
+
+// Strip the internal "#colN#" prefix of an mBCG breakdown message.
+std::string strip_col(const std::string& m, int* col) {
+  *col = -1;
+  if (m.size() > 4 && m.compare(0, 4, "#col") == 0) {
+    const size_t e = m.find('#', 4);
+    *col = std::stoi(m.substr(4, e - 4));
+    return m.substr(e + 1);
+  }
+  return m;
+}
+
+uint64_t mix_seed_impl(uint64_t seed, uint64_t salt) {  // common.hpp:93-98
+  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+void make_probes_impl(int64_t n, int count, uint64_t seed, double* out) {  // trace_estimation.hpp:27-36
+  require(n >= 1, "make_probes: n must be >= 1");
+  require(count >= 1, "make_probes: need at least one probe");
+  std::mt19937_64 rng(seed);
+  const double inv = 1.0 / std::sqrt(static_cast<double>(n));
+  for (int c = 0; c < count; ++c)
+    for (int64_t i = 0; i < n; ++i) out[c * n + i] = (rng() & 1ULL) ? inv : -inv;
+}
+
+// ---------------------------------------------------------------------------
+// evaluate_mll (gp_likelihood.hpp:51-103) on device-resident y (n) and Z (n x l)
+// ---------------------------------------------------------------------------
+void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, int l, uint64_t seed,
+                   const gpk_mll_cfg* cfg, gpk_mll_result* res) {
+  c->require_ready();
+  require(cfg != nullptr && res != nullptr, "evaluate_mll: null config or result");
+  require(l >= 1, "make_probes: need at least one probe");
+  require(c->pkind != 0, "evaluate_mll: no preconditioner (gpk_pivoted_cholesky or gpk_precond_identity)");
+  const int n = c->n, d = c->d, np = d + 2;
+  const long long ldn = c->ldn;
+  const bool fp64 = cfg->solver.precision == GPK_PREC_FP64;
+  const int mi = cfg->solver.max_iters;
+  const double tol = cfg->solver.rel_tol;
+  require(mi >= 1, "CgConfig: max_iters must be >= 1");
+  require(tol > 0.0 && tol < 1.0, "CgConfig: rel_tol must be in (0, 1)");
+  const long long launches0 = c->launches;
+  c->entries = 0;
+  c->flops = 0;
+  cudaEvent_t e0, e1, e2;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&e2));
+  CK(cudaEventRecord(e0, c->st));
+
+  // ---- forward: one mBCG over [y, z_1..z_l] (pcg_solve(y) + vr_logdet's probe solves)
+  const int t = 1 + l;
+  DBuf<double> B, Xs;
+  B.ensure(static_cast<size_t>(t) * ldn);
+  Xs.ensure(static_cast<size_t>(t) * ldn);
+  c->check_launch(gpk::launch_gather_cols(dy, n, nullptr, 1.0, n, 1, B.p, ldn, c->st), 1, "gather");
+  c->check_launch(gpk::launch_gather_cols(dZ, ldz, nullptr, 1.0, n, l, B.p + ldn, ldn, c->st), 1, "gather");
+  std::vector<double> ah(static_cast<size_t>(t) * mi), bh(static_cast<size_t>(t) * mi);
+  gpk_ctx::CgOut cg;
+  try {
+    cg = c->mbcg(B.p, ldn, t, mi, tol, fp64, Xs.p, ldn, ah.data(), bh.data(), nullptr);
+  } catch (const GpkError& e) {
+    if (e.code != GPK_SOLVER_ERROR) throw;
+    int col;
+    const std::string m = strip_col(e.msg, &col);
+    if (col <= 0) fail(GPK_SOLVER_ERROR, m);  // the y solve (gp_likelihood.hpp:61)
+    fail(GPK_NUMERICAL_ERROR, "vr_logdet: probe " + std::to_string(col - 1) + ": " + m);  // :177-179
+  }
+  res->refine_passes = 0;
+  res->max_true_rel_residual = -1.0;
+  if (!fp64 && cfg->solver.refine > 0) {
+    double mr = 0.0;
+    res->refine_passes = c->refine(B.p, ldn, t, Xs.p, ldn, cg, mi, tol, cfg->solver.refine, &mr);
+    res->max_true_rel_residual = mr;
+  }
+  const double* U = Xs.p;
+  const double* S = Xs.p + ldn;
+
+  // ---- SLQ per probe (trace_estimation.hpp:163-176) on the host
+  std::vector<double> gam(l);
+  for (int i = 0; i < l; ++i) {
+    const int col = 1 + i;
+    const int m = cg.iters[col];
+    std::vector<double> dg, sb;
+    for (int kk = 1; kk <= m; ++kk) {  // krylov.hpp:85-92
+      const double a = ah[static_cast<size_t>(col) * mi + kk - 1];
+      double dv = 1.0 / a;
+      if (kk > 1) {
+        const double ap = ah[static_cast<size_t>(col) * mi + kk - 2];
+        const double bp = bh[static_cast<size_t>(col) * mi + kk - 2];
+        dv += bp / ap;
+        sb.push_back(std::sqrt(bp) / ap);
+      }
+      dg.push_back(dv);
+    }
+    try {
+      gam[i] = slq_log(dg, sb).value;
+    } catch (const GpkError& e) {
+      fail(GPK_NUMERICAL_ERROR, "vr_logdet: probe " + std::to_string(i) + ": " + e.msg);
+    }
+    if (res->forward_cg_iterations) res->forward_cg_iterations[i] = m;
+    if (res->forward_gammas) res->forward_gammas[i] = gam[i];
+  }
+  const double plogdet = c->pkind == 1 ? 0.0 : c->plogdet;
+  double stoch = 0.0;  // finish_estimate (trace_estimation.hpp:132-141)
+  for (double g : gam) stoch += g;
+  stoch *= static_cast<double>(n) / static_cast<double>(l);
+  std::vector<double> scaled(l);
+  for (int i = 0; i < l; ++i) scaled[i] = static_cast<double>(n) * gam[i];
+  res->value_sample_variance = unbiased_variance(scaled);
+  res->logdet = plogdet + stoch;
+  res->logdet_precond = plogdet;
+  const double quad = c->col_dots(dy, U, 1, n)[0];  // y.u
+  res->quad = quad;
+  const double kPi = 3.14159265358979323846;
+  res->value = -0.5 * (quad + res->logdet + static_cast<double>(n) * std::log(2.0 * kPi));
+  res->solve_iterations = cg.iters[0];
+  res->total_cg_iterations = 0;
+  for (int col = 0; col < t; ++col) res->total_cg_iterations += cg.iters[col];
+  CK(cudaEventRecord(e1, c->st));
+
+  if (cfg->with_gradient) {
+    require(res->gradient != nullptr, "evaluate_mll: null gradient buffer");
+    // backward probe batch (gp_likelihood.hpp:79-84)
+    const double* Zb = dZ;
+    long long ldzb = ldz;
+    DBuf<double> Zu, Su;
+    const double* Sb = S;
+    long long ldsb = ldn;
+    if (!cfg->share_probes) {
+      std::vector<double> hz(static_cast<size_t>(n) * l);
+      make_probes_impl(n, l, mix_seed_impl(seed, 0xb2dULL), hz.data());
+      Zu.ensure(static_cast<size_t>(l) * ldn);
+      CK(cudaMemcpy2DAsync(Zu.p, ldn * sizeof(double), hz.data(), n * sizeof(double), n * sizeof(double), l,
+                           cudaMemcpyHostToDevice, c->st));
+      Zb = Zu.p;
+      ldzb = ldn;
+    }
+    // ---- preconditioner terms: Q = P^{-1} Zb, t_{w,i} = z_i' P^{-1} dP_w z_i
+    DBuf<double> Zc, Q;
+    Zc.ensure(static_cast<size_t>(l) * ldn);
+    Q.ensure(static_cast<size_t>(l) * ldn);
+    c->check_launch(gpk::launch_gather_cols(Zb, ldzb, nullptr, 1.0, n, l, Zc.p, ldn, c->st), 1, "gather");
+    c->psolve(Zc.p, l, Q.p);
+    std::vector<std::vector<double>> tw(np, std::vector<double>(l, 0.0));
+    std::vector<double> tdet(np, 0.0);
+    const bool dplr = c->pkind == 2;
+    if (dplr) {
+      tdet[d + 1] = c->trace_det[d + 1];
+      const std::vector<double> zq = c->col_dots(Zc.p, Q.p, l, ldn);
+      for (int i = 0; i < l; ++i) tw[d + 1][i] = zq[i];  // dP/dsigma^2 = I
+      if (c->k > 0) {
+        require(c->have_dl, "DiagPlusLowRank: derivative factors not attached");
+        const int k = c->k;
+        // [Q Zc] is contiguous: columns 0..l-1 of Q then Zc (separate buffers -> two G1s)
+        DBuf<double> A, Bw, part;
+        A.ensure(static_cast<size_t>(2) * l * k);
+        Bw.ensure(static_cast<size_t>(2) * l * k);
+        part.ensure(gpk::g1_workspace(n, k, l));
+        c->check_launch(gpk::launch_g1(c->L.p, n, k, Q.p, ldn, l, n, part.p, A.p, k, c->st), 2, "g1");
+        c->check_launch(gpk::launch_g1(c->L.p, n, k, Zc.p, ldn, l, n, part.p, A.p + static_cast<size_t>(l) * k, k,
+                                       c->st),
+                        2, "g1");
+        std::vector<double> hA(static_cast<size_t>(2) * l * k), hB(static_cast<size_t>(2) * l * k);
+        c->d2h(hA.data(), A.p, sizeof(double) * hA.size());
+        for (int w = 0; w <= d; ++w) {
+          tdet[w] = c->trace_det[w];
+          const double* dLw = c->dL.p + static_cast<size_t>(w) * n * k;
+          c->check_launch(gpk::launch_g1(dLw, n, k, Q.p, ldn, l, n, part.p, Bw.p, k, c->st), 2, "g1");
+          c->check_launch(
+              gpk::launch_g1(dLw, n, k, Zc.p, ldn, l, n, part.p, Bw.p + static_cast<size_t>(l) * k, k, c->st), 2,
+              "g1");
+          c->d2h(hB.data(), Bw.p, sizeof(double) * hB.size());
+          for (int i = 0; i < l; ++i) {
+            // (dL' q_i).(L' z_i) + (L' q_i).(dL' z_i)   (LowRankDerivOp::apply, preconditioners.hpp:62-69)
+            double acc = 0.0;
+            const double* bq = hB.data() + static_cast<size_t>(i) * k;
+            const double* bz = hB.data() + static_cast<size_t>(l + i) * k;
+            const double* aq = hA.data() + static_cast<size_t>(i) * k;
+            const double* az = hA.data() + static_cast<size_t>(l + i) * k;
+            for (int q = 0; q < k; ++q) acc += bq[q] * az[q] + aq[q] * bz[q];
+            tw[w][i] = acc;
+          }
+        }
+      }
+    }
+    // ---- K_hat terms: quad_w = u' dK_w u and z_i' K_hat^{-1} dK_w z_i
+    std::vector<double> quadw(np, 0.0);
+    std::vector<std::vector<double>> zw(np, std::vector<double>(l, 0.0));  // z_i' w_i
+    std::vector<bool> per_probe(np, true);
+    // unshared batch needs its own solves s_i = K_hat^{-1} zb_i
+    DBuf<double> Sx;
+    if (!cfg->share_probes) {
+      Sx.ensure(static_cast<size_t>(l) * ldn);
+      gpk_ctx::CgOut cgb;
+      try {
+        cgb = c->mbcg(Zc.p, ldn, l, mi, tol, fp64, Sx.p, ldn, nullptr, nullptr, nullptr);
+      } catch (const GpkError& e) {
+        int col;
+        const std::string m = strip_col(e.msg, &col);
+        fail(GPK_NUMERICAL_ERROR, "trace residual: probe " + std::to_string(std::max(col, 0)) + ": " + m);
+      }
+      for (int i = 0; i < l; ++i) res->total_cg_iterations += cgb.iters[i];
+      if (!fp64 && cfg->solver.refine > 0) {
+        double mr;
+        c->refine(Zc.p, ldn, l, Sx.p, ldn, cgb, mi, tol, cfg->solver.refine, &mr);
+      }
+      Sb = Sx.p;
+      ldsb = ldn;
+    }
+    // noise: w_i = s_i (cached forward solves when shared, gp_likelihood.hpp:90)
+    {
+      const double uu = c->col_dots(U, U, 1, n)[0];
+      quadw[d + 1] = uu;
+      const std::vector<double> zs = c->col_dots(Zc.p, Sb, l, ldn);
+      for (int i = 0; i < l; ++i) zw[d + 1][i] = zs[i];
+    }
+    if (cfg->backward_mode == 0) {
+      // fused bilinear derivative pass over all n^2 pairs
+      const int n_pad = c->n_pad;
+      const size_t elem = fp64 ? 8 : 4;
+      DBuf<unsigned char> ops;
+      ops.ensure(elem * static_cast<size_t>(n_pad) * (1 + 2 * l));
+      unsigned char* Up = ops.p;
+      unsigned char* SZp = ops.p + elem * n_pad;
+      auto conv = [&](const double* src, long long lds, int tt, unsigned char* dst) {
+        const long long tot = static_cast<long long>(tt) * n_pad;
+        if (fp64)
+          to_padded_kernel<double><<<static_cast<unsigned>((tot + 255) / 256), 256, 0, c->st>>>(
+              src, lds, n, n_pad, tt, reinterpret_cast<double*>(dst));
+        else
+          to_padded_kernel<float><<<static_cast<unsigned>((tot + 255) / 256), 256, 0, c->st>>>(
+              src, lds, n, n_pad, tt, reinterpret_cast<float*>(dst));
+        c->check_launch(cudaGetLastError(), 1, "to_padded");
+      };
+      conv(U, n, 1, Up);
+      conv(Sb, ldsb, l, SZp);
+      conv(Zc.p, ldn, l, SZp + elem * static_cast<size_t>(l) * n_pad);
+      const void* Xp = fp64 ? static_cast<const void*>(c->X64s.p) : static_cast<const void*>(c->X32.p);
+      int nblk = 0;
+      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, n, n_pad, l, d, nullptr, &nblk,
+                                                 c->st),
+                      0, "deriv_contract");
+      const int na = 2 * (c->dp + 1);
+      DBuf<double> part;
+      part.ensure(static_cast<size_t>(nblk) * na);
+      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, n, n_pad, l, d, part.p, &nblk,
+                                                 c->st),
+                      1, "deriv_contract");
+      std::vector<double> hp(static_cast<size_t>(nblk) * na);
+      c->d2h(hp.data(), part.p, sizeof(double) * hp.size());
+      std::vector<double> tot(na, 0.0);
+      for (int b = 0; b < nblk; ++b)
+        for (int q = 0; q < na; ++q) tot[q] += hp[static_cast<size_t>(b) * na + q];
+      const double cpre = fp64 ? 1.0 : gpk::prescale_c(c->family);
+      const int DP = c->dp;
+      // outputscale: dK = 2 o shape ; lengthscale j: dK = (-2 o^2 / l_j) shape_ds ds_j^2
+      quadw[0] = 2.0 * c->o * tot[0];
+      const double g0 = 2.0 * c->o * tot[DP + 1];
+      for (int i = 0; i < l; ++i) zw[0][i] = std::nan("");
+      per_probe[0] = false;
+      double gsum[64];
+      gsum[0] = g0;
+      for (int j = 0; j < d; ++j) {
+        const double fac = (-2.0 * c->o2 / c->ls[j]) / cpre;
+        quadw[1 + j] = fac * tot[1 + j];
+        gsum[1 + j] = fac * tot[DP + 2 + j];
+        per_probe[1 + j] = false;
+      }
+      c->entries += static_cast<long long>(n) * n;
+      // gradient for the non-noise parameters from the summed stochastic term
+      for (int w = 0; w <= d; ++w) {
+        double tsum = 0.0;
+        for (int i = 0; i < l; ++i) tsum += tw[w][i];
+        const double stoch_w = static_cast<double>(n) / static_cast<double>(l) * (gsum[w] - tsum);
+        const double tau = tdet[w] + stoch_w;
+        res->gradient[w] = 0.5 * (quadw[w] - tau) * (w == 0 ? c->o : c->ls[w - 1]);
+        if (res->backward_gammas)
+          for (int i = 0; i < l; ++i) res->backward_gammas[static_cast<size_t>(w) * l + i] = std::nan("");
+      }
+    } else {
+      // reference-faithful: mBCG over the (d+1) l right-hand sides dK_w z_i (trace_estimation.hpp:209)
+      const int tb = (d + 1) * l;
+      DBuf<double> RH, Wsol;
+      RH.ensure(static_cast<size_t>(tb) * ldn);
+      Wsol.ensure(static_cast<size_t>(tb) * ldn);
+      for (int w = 0; w <= d; ++w)
+        c->apply_kernel(Zc.p, ldn, l, RH.p + static_cast<size_t>(w) * l * ldn, ldn, fp64, w);
+      gpk_ctx::CgOut cgw;
+      try {
+        cgw = c->mbcg(RH.p, ldn, tb, mi, tol, fp64, Wsol.p, ldn, nullptr, nullptr, nullptr);
+      } catch (const GpkError& e) {
+        int col;
+        const std::string m = strip_col(e.msg, &col);
+        fail(GPK_NUMERICAL_ERROR, "trace residual: probe " + std::to_string(std::max(col, 0) % l) + ": " + m);
+      }
+      if (!fp64 && cfg->solver.refine > 0) {
+        double mr;
+        c->refine(RH.p, ldn, tb, Wsol.p, ldn, cgw, mi, tol, cfg->solver.refine, &mr);
+      }
+      for (int q = 0; q < tb; ++q) res->total_cg_iterations += cgw.iters[q];
+      DBuf<double> du;
+      du.ensure(static_cast<size_t>(ldn));
+      for (int w = 0; w <= d; ++w) {
+        const std::vector<double> zs = c->col_dots(Zc.p, Wsol.p + static_cast<size_t>(w) * l * ldn, l, ldn);
+        for (int i = 0; i < l; ++i) zw[w][i] = zs[i];
+        c->apply_kernel(U, n, 1, du.p, ldn, fp64, w);
+        quadw[w] = c->col_dots(U, du.p, 1, n)[0];
+      }
+      for (int w = 0; w <= d; ++w) {
+        std::vector<double> gm(l);
+        double st = 0.0;
+        for (int i = 0; i < l; ++i) {
+          gm[i] = zw[w][i] - tw[w][i];  // gamma_i = z.(w - wt)
+          st += gm[i];
+        }
+        st *= static_cast<double>(n) / static_cast<double>(l);
+        const double tau = tdet[w] + st;
+        res->gradient[w] = 0.5 * (quadw[w] - tau) * (w == 0 ? c->o : c->ls[w - 1]);
+        if (res->backward_gammas)
+          for (int i = 0; i < l; ++i) res->backward_gammas[static_cast<size_t>(w) * l + i] = gm[i];
+      }
+    }
+    // noise component (gp_likelihood.hpp:87-101 with w = d+1)
+    {
+      const int w = d + 1;
+      double st = 0.0;
+      std::vector<double> gm(l);
+      for (int i = 0; i < l; ++i) {
+        gm[i] = zw[w][i] - tw[w][i];
+        st += gm[i];
+      }
+      st *= static_cast<double>(n) / static_cast<double>(l);
+      const double tau = tdet[w] + st;
+      res->gradient[w] = 0.5 * (quadw[w] - tau) * c->noise;
+      if (res->backward_gammas)
+        for (int i = 0; i < l; ++i) res->backward_gammas[static_cast<size_t>(w) * l + i] = gm[i];
+    }
+  }
+  CK(cudaEventRecord(e2, c->st));
+  c->sync();
+  float ms1 = 0, ms2 = 0;
+  CK(cudaEventElapsedTime(&ms1, e0, e1));
+  CK(cudaEventElapsedTime(&ms2, e1, e2));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  res->seconds_solve = ms1 * 1e-3;
+  res->seconds_backward = ms2 * 1e-3;
+  res->seconds_total = (ms1 + ms2) * 1e-3;
+  res->kernel_entries = c->entries;
+  res->mvm_flops = c->flops;
+  res->gpu_launches = static_cast<int>(c->launches - launches0);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* gpk_version(void) { return "gpkrylov_cuda 0.1 (sm_100a)"; }
+
+gpk_status gpk_create(int device, gpk_ctx** out) {
+  if (!out) return GPK_INPUT_ERROR;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return GPK_CUDA_ERROR;
+  if (device < 0 || device >= ndev) return GPK_INPUT_ERROR;
+  auto* c = new gpk_ctx();
+  c->device = device;
+  const gpk_status s = guard(c, [&] { CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking)); });
+  if (s != GPK_OK) {
+    delete c;
+    return s;
+  }
+  *out = c;
+  return GPK_OK;
+}
+
+void gpk_destroy(gpk_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->st);
+  cudaStreamDestroy(ctx->st);
+  delete ctx;
+}
+
+const char* gpk_last_error(const gpk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+long long gpk_launch_count(const gpk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+static void set_data_common(gpk_ctx* c, const double* X, int64_t n, int64_t d, int64_t ldx, bool device) {
+  require(n >= 1, "KernelOperator: empty dataset");
+  require(d >= 1, "Hyperparameters: need at least one lengthscale");
+  require(ldx >= n, "gpk_set_data: ldx < n");
+  require(gpk::dpad_for(static_cast<int>(d)) > 0, "gpkrylov_cuda: input dimension above 32 is not supported");
+  require(n < (1LL << 30), "gpkrylov_cuda: n too large for one device");
+  c->n = static_cast<int>(n);
+  c->d = static_cast<int>(d);
+  c->n_pad = static_cast<int>((n + 127) / 128 * 128);
+  c->ldn = (n + 31) / 32 * 32;
+  c->dp = gpk::dpad_for(c->d);
+  c->X.ensure(static_cast<size_t>(n) * d);
+  CK(cudaMemcpy2DAsync(c->X.p, n * sizeof(double), X, ldx * sizeof(double), n * sizeof(double), d,
+                       device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+  c->have_data = true;
+  c->packed = false;
+  c->pkind = 0;
+  c->have_dl = false;
+}
+
+gpk_status gpk_set_data(gpk_ctx* ctx, const double* X, int64_t n, int64_t d, int64_t ldx) {
+  return guard(ctx, [&] { set_data_common(ctx, X, n, d, ldx, false); ctx->sync(); });
+}
+gpk_status gpk_set_data_device(gpk_ctx* ctx, const double* dX, int64_t n, int64_t d, int64_t ldx) {
+  return guard(ctx, [&] { set_data_common(ctx, dX, n, d, ldx, true); });
+}
+
+gpk_status gpk_set_params(gpk_ctx* ctx, int family, double alpha, double log_o, const double* log_ls,
+                          double log_noise) {
+  return guard(ctx, [&] {
+    (void)alpha;
+    require(family >= 0 && family <= 4, "KernelSpec: unknown kernel family");
+    require(family != GPK_RATQUAD, "gpkrylov_cuda: rational quadratic kernel is not supported on the GPU path");
+    require(ctx->have_data, "gpkrylov_cuda: set data before hyperparameters");
+    auto ok = [](double lv) { return std::isfinite(lv) && std::isfinite(std::exp(lv)) && std::exp(lv) > 0.0; };
+    require(ok(log_o), "Hyperparameters: output scale not positive finite");  // kernels.hpp:55-63
+    require(ok(log_noise), "Hyperparameters: noise variance not positive finite");
+    for (int j = 0; j < ctx->d; ++j)
+      require(ok(log_ls[j]), "Hyperparameters: lengthscale " + std::to_string(j) + " not positive finite");
+    ctx->family = family;
+    ctx->log_o = log_o;
+    ctx->log_noise = log_noise;
+    ctx->log_ls.assign(log_ls, log_ls + ctx->d);
+    ctx->o = std::exp(log_o);
+    ctx->o2 = std::pow(ctx->o, 2);
+    ctx->noise = std::exp(log_noise);
+    ctx->ls.resize(ctx->d);
+    for (int j = 0; j < ctx->d; ++j) ctx->ls[j] = std::exp(log_ls[j]);
+    ctx->have_params = true;
+    ctx->packed = false;
+    ctx->pack();
+  });
+}
+
+static void mvm_common(gpk_ctx* c, int which, const double* V, int64_t ldv, int t, double* out, int64_t ldo,
+                       int precision) {
+  c->require_ready();
+  require(t >= 1, "KernelOperator: vector length does not match n");
+  require(which >= -1 && which <= c->d + 1, "KernelOperator: hyperparameter index out of range");
+  const int n = c->n;
+  for (int q = 0; q < t; ++q)
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(V[q * ldv + i])) fail(GPK_INPUT_ERROR, "KernelOperator: non-finite entries in input vector");
+  DBuf<double> dv, dout;
+  dv.ensure(static_cast<size_t>(t) * c->ldn);
+  dout.ensure(static_cast<size_t>(t) * c->ldn);
+  CK(cudaMemcpy2DAsync(dv.p, c->ldn * sizeof(double), V, ldv * sizeof(double), n * sizeof(double), t,
+                       cudaMemcpyHostToDevice, c->st));
+  c->apply_kernel(dv.p, c->ldn, t, dout.p, c->ldn, precision == GPK_PREC_FP64, which);
+  if (which < 0) c->check_launch(gpk::launch_axpby(dout.p, dv.p, 1.0, c->noise, n, t, c->ldn, c->st), 1, "axpy");
+  CK(cudaMemcpy2DAsync(out, ldo * sizeof(double), dout.p, c->ldn * sizeof(double), n * sizeof(double), t,
+                       cudaMemcpyDeviceToHost, c->st));
+  c->sync();
+}
+
+gpk_status gpk_kernel_mvm(gpk_ctx* ctx, const double* V, int64_t ldv, int t, double* out, int64_t ldo, int precision) {
+  return guard(ctx, [&] { mvm_common(ctx, -1, V, ldv, t, out, ldo, precision); });
+}
+gpk_status gpk_kernel_deriv_mvm(gpk_ctx* ctx, int which, const double* V, int64_t ldv, int t, double* out,
+                                int64_t ldo, int precision) {
+  return guard(ctx, [&] {
+    if (which < 0 || which > ctx->d + 1) fail(GPK_INPUT_ERROR, "KernelOperator: hyperparameter index out of range");
+    mvm_common(ctx, which, V, ldv, t, out, ldo, precision);
+  });
+}
+
+static void column_common(gpk_ctx* c, int which, int64_t i, double* out) {
+  c->require_ready();
+  require(i >= 0 && i < c->n, which < 0 ? "kernel_column: index out of range" : "kernel_deriv_column: index out of range");
+  require(which >= -1 && which <= c->d + 1, "KernelOperator: hyperparameter index out of range");
+  DBuf<double> col;
+  col.ensure(c->n);
+  if (which == c->d + 1) {
+    std::fill(out, out + c->n, 0.0);
+    return;
+  }
+  double fac = 1.0;
+  if (which == 0) fac = 2.0 / c->o;
+  if (which >= 1) {
+    const double lj = c->ls[which - 1];
+    fac = -2.0 * c->o2 / (lj * lj * lj);
+  }
+  c->check_launch(gpk::launch_kernel_column(c->family, c->sx.p, c->X.p, c->sq.p, c->n, c->d, i, which, c->o2, fac,
+                                            col.p, c->st),
+                  1, "kernel_column");
+  c->d2h(out, col.p, sizeof(double) * c->n);
+}
+
+gpk_status gpk_kernel_column(gpk_ctx* ctx, int64_t i, double* out) {
+  return guard(ctx, [&] { column_common(ctx, -1, i, out); });
+}
+gpk_status gpk_kernel_deriv_column(gpk_ctx* ctx, int which, int64_t i, double* out) {
+  return guard(ctx, [&] {
+    if (which < 0 || which > ctx->d + 1) fail(GPK_INPUT_ERROR, "KernelOperator: hyperparameter index out of range");
+    column_common(ctx, which, i, out);
+  });
+}
+
+gpk_status gpk_precond_identity(gpk_ctx* ctx) {
+  return guard(ctx, [&] {
+    require(ctx->have_data, "gpkrylov_cuda: no data set (gpk_set_data)");
+    ctx->pkind = 1;
+    ctx->k = 0;
+    ctx->plogdet = 0.0;
+    ctx->have_dl = true;
+    ctx->trace_det.assign(ctx->d + 2, 0.0);
+  });
+}
+
+// preconditioners.hpp:236-264 + DiagPlusLowRank ctor (:84-95)
+gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double noise, int64_t* pivots_out,
+                                int* achieved, double* remaining_diag) {
+  return guard(ctx, [&] {
+    gpk_ctx* c = ctx;
+    c->require_ready();
+    const int n = c->n;
+    require(rank >= 0 && rank <= n, "pivoted_cholesky: rank must be in [0, n]");
+    require(noise > 0.0 && std::isfinite(noise), "DiagPlusLowRank: noise variance must be positive");
+    c->pkind = 0;
+    c->have_dl = false;
+    c->pivots.clear();
+    DBuf<double> dg, col;
+    dg.ensure(n);
+    col.ensure(n);
+    c->L.ensure(static_cast<size_t>(n) * std::max(rank, 1));
+    const long long cnt = n;
+    fill_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, c->st>>>(dg.p, cnt, c->o * c->o);  // :230-233
+    c->check_launch(cudaGetLastError(), 1, "fill");
+    const double kmax = c->o * c->o;
+    const int nb = gpk::pchol_blocks(n);
+    c->w_argval.ensure(nb + 1);
+    c->w_argidx.ensure(nb + 1);
+    long long p = 0;  // argmax of the constant diagonal: lowest index
+    double dp = kmax;
+    int step = 0;
+    for (; step < rank; ++step) {
+      if (dp < -1e-10 * kmax)
+        fail(GPK_NUMERICAL_ERROR, "pivoted_cholesky: negative pivot " + num(dp) + " at step " + std::to_string(step) +
+                                      "; matrix not PSD");
+      if (dp <= diag_tol) break;
+      c->check_launch(gpk::launch_kernel_column(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, p, -1, c->o2, 1.0, col.p,
+                                                c->st),
+                      1, "kernel_column");
+      const double root = std::sqrt(dp);
+      c->check_launch(gpk::launch_pchol_step(c->L.p, n, step, p, root, col.p, dg.p, n, c->w_argval.p, c->w_argidx.p,
+                                             c->w_argval.p + nb, c->w_argidx.p + nb, c->st),
+                      2, "pchol_step");
+      c->pivots.push_back(p);
+      double hv;
+      long long hi;
+      CK(cudaMemcpyAsync(&hv, c->w_argval.p + nb, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(&hi, c->w_argidx.p + nb, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+      c->sync();
+      dp = hv;
+      p = hi;
+    }
+    c->k = step;
+    if (achieved) *achieved = step;
+    if (pivots_out)
+      for (int s = 0; s < step; ++s) pivots_out[s] = c->pivots[s];
+    if (remaining_diag) c->d2h(remaining_diag, dg.p, sizeof(double) * n);
+    // DiagPlusLowRank: inner = L'L + s2 I, Cholesky, C = L inner^{-1}, logdet
+    c->pnoise = noise;
+    const int k = c->k;
+    double ld = static_cast<double>(n) * std::log(noise);  // :127-133
+    if (k > 0) {
+      DBuf<double> G, part;
+      G.ensure(static_cast<size_t>(k) * k);
+      part.ensure(gpk::g1_workspace(n, k, k));
+      c->check_launch(gpk::launch_g1(c->L.p, n, k, c->L.p, n, k, n, part.p, G.p, k, c->st), 2, "gram");
+      std::vector<double> inner(static_cast<size_t>(k) * k);
+      c->d2h(inner.data(), G.p, sizeof(double) * inner.size());
+      for (int a = 0; a < k; ++a) inner[a + a * k] += noise;
+      if (!host_cholesky(inner, k))
+        fail(GPK_NUMERICAL_ERROR, "DiagPlusLowRank: inner Cholesky failed (cannot happen for sigma^2 > 0)");
+      double sl = 0.0;
+      for (int a = 0; a < k; ++a) sl += std::log(inner[a + a * k]);
+      ld += 2.0 * sl - static_cast<double>(k) * std::log(noise);
+      const std::vector<double> inv = host_chol_inverse(inner, k);
+      DBuf<double> Inv;
+      Inv.ensure(static_cast<size_t>(k) * k);
+      c->h2d(Inv.p, inv.data(), sizeof(double) * inv.size());
+      c->C.ensure(static_cast<size_t>(n) * k);
+      c->check_launch(gpk::launch_g2(c->L.p, n, k, Inv.p, k, k, n, c->C.p, n, c->st), 1, "cache");
+      c->sync();
+    }
+    c->plogdet = ld;
+    c->pkind = 2;
+    // trace of P^{-1} for the noise derivative: (n - sum C o L) / s2  (:138-145 with dP = I)
+    c->trace_det.assign(c->d + 2, 0.0);
+    double cl = 0.0;
+    if (k > 0) {
+      const int nrb = gpk::num_chunks(n * k);
+      DBuf<double> part, outv;
+      part.ensure(nrb);
+      outv.ensure(1);
+      // flat dot over n*k entries
+      c->check_launch(gpk::launch_dot_partials(0, c->C.p, c->L.p, 0.0, n * k, 0, 1, part.p, c->st), 1, "dot");
+      c->check_launch(gpk::launch_reduce_partials(part.p, nrb, 1, outv.p, c->st), 1, "reduce");
+      c->d2h(&cl, outv.p, sizeof(double));
+    }
+    c->trace_det[c->d + 1] = static_cast<double>(n) / noise - cl / noise;
+  });
+}
+
+// preconditioners.hpp:269-295
+gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
+  return guard(ctx, [&] {
+    gpk_ctx* c = ctx;
+    c->require_ready();
+    if (c->pkind == 1) return;
+    require(c->pkind == 2, "DiagPlusLowRank: derivative factors not attached");
+    const int n = c->n, k = c->k, nw = c->d + 1;
+    require(static_cast<int>(c->pivots.size()) == k,
+            "pivoted_cholesky_deriv_factors: preconditioner has no pivot record");
+    c->have_dl = false;
+    if (k > 0) {
+      c->dL.ensure(static_cast<size_t>(nw) * n * k);
+      DBuf<double> dcol;
+      dcol.ensure(static_cast<size_t>(nw) * n);
+      for (int s = 0; s < k; ++s) {
+        const long long p = c->pivots[s];
+        for (int w = 0; w < nw; ++w) {
+          double fac = 2.0 / c->o;
+          if (w >= 1) {
+            const double lj = c->ls[w - 1];
+            fac = -2.0 * c->o2 / (lj * lj * lj);
+          }
+          c->check_launch(gpk::launch_kernel_column(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, p, w, c->o2, fac,
+                                                    dcol.p + static_cast<size_t>(w) * n, c->st),
+                          1, "kernel_deriv_column");
+        }
+        c->check_launch(gpk::launch_dl_step(c->L.p, n, c->dL.p, static_cast<long long>(n) * k, nw, s, p, dcol.p, n, n,
+                                            c->st),
+                        1, "dl_step");
+      }
+      // tr(P^{-1} dP_w) = 2 sum(C o dL_w)  (algebraically equal to preconditioners.hpp:138-145)
+      const int nrb = gpk::num_chunks(n * k);
+      DBuf<double> part, outv;
+      part.ensure(static_cast<size_t>(nrb));
+      outv.ensure(1);
+      for (int w = 0; w < nw; ++w) {
+        c->check_launch(gpk::launch_dot_partials(0, c->C.p, c->dL.p + static_cast<size_t>(w) * n * k, 0.0, n * k, 0, 1,
+                                                 part.p, c->st),
+                        1, "dot");
+        c->check_launch(gpk::launch_reduce_partials(part.p, nrb, 1, outv.p, c->st), 1, "reduce");
+        double v;
+        c->d2h(&v, outv.p, sizeof(double));
+        c->trace_det[w] = 2.0 * v;
+      }
+    }
+    c->have_dl = true;
+  });
+}
+
+gpk_status gpk_precond_factor(gpk_ctx* ctx, double* L, int64_t ldl) {
+  return guard(ctx, [&] {
+    require(ctx->pkind == 2, "gpkrylov_cuda: no pivoted-Cholesky preconditioner");
+    if (ctx->k == 0) return;
+    CK(cudaMemcpy2DAsync(L, ldl * sizeof(double), ctx->L.p, ctx->n * sizeof(double), ctx->n * sizeof(double), ctx->k,
+                         cudaMemcpyDeviceToHost, ctx->st));
+    ctx->sync();
+  });
+}
+
+gpk_status gpk_precond_deriv_factor(gpk_ctx* ctx, int which, double* dL, int64_t ldl) {
+  return guard(ctx, [&] {
+    require(ctx->pkind == 2 && ctx->have_dl, "DiagPlusLowRank: derivative factors not attached");
+    require(which >= 0 && which <= ctx->d + 1, "DiagPlusLowRank: hyperparameter index out of range");
+    const int n = ctx->n, k = ctx->k;
+    if (k == 0) return;
+    if (which == ctx->d + 1) {
+      for (int c = 0; c < k; ++c) std::fill(dL + c * ldl, dL + c * ldl + n, 0.0);
+      return;
+    }
+    CK(cudaMemcpy2DAsync(dL, ldl * sizeof(double), ctx->dL.p + static_cast<size_t>(which) * n * k, n * sizeof(double),
+                         n * sizeof(double), k, cudaMemcpyDeviceToHost, ctx->st));
+    ctx->sync();
+  });
+}
+
+gpk_status gpk_precond_solve(gpk_ctx* ctx, const double* V, int64_t ldv, int t, double* out, int64_t ldo) {
+  return guard(ctx, [&] {
+    require(ctx->pkind != 0, "gpkrylov_cuda: no preconditioner");
+    const int n = ctx->n;
+    DBuf<double> dv, dz;
+    dv.ensure(static_cast<size_t>(t) * ctx->ldn);
+    dz.ensure(static_cast<size_t>(t) * ctx->ldn);
+    CK(cudaMemcpy2DAsync(dv.p, ctx->ldn * sizeof(double), V, ldv * sizeof(double), n * sizeof(double), t,
+                         cudaMemcpyHostToDevice, ctx->st));
+    ctx->psolve(dv.p, t, dz.p);
+    CK(cudaMemcpy2DAsync(out, ldo * sizeof(double), dz.p, ctx->ldn * sizeof(double), n * sizeof(double), t,
+                         cudaMemcpyDeviceToHost, ctx->st));
+    ctx->sync();
+  });
+}
+
+gpk_status gpk_precond_logdet(gpk_ctx* ctx, double* out) {
+  return guard(ctx, [&] {
+    require(ctx->pkind != 0, "gpkrylov_cuda: no preconditioner");
+    *out = ctx->pkind == 1 ? 0.0 : ctx->plogdet;
+  });
+}
+
+gpk_status gpk_precond_trace_inv_deriv(gpk_ctx* ctx, int which, double* out) {
+  return guard(ctx, [&] {
+    require(ctx->pkind != 0, "gpkrylov_cuda: no preconditioner");
+    require(which >= 0 && which <= ctx->d + 1, "DiagPlusLowRank: hyperparameter index out of range");
+    if (ctx->pkind == 1) {
+      *out = 0.0;
+      return;
+    }
+    if (which <= ctx->d && ctx->k > 0) require(ctx->have_dl, "DiagPlusLowRank: derivative factors not attached");
+    *out = ctx->trace_det[which];
+  });
+}
+
+gpk_status gpk_mbcg(gpk_ctx* ctx, const double* B, int64_t ldb, int t, const gpk_cg_cfg* cfg, double* X, int64_t ldx,
+                    int* iters, int* converged, double* alpha, double* beta, double* resid_hist) {
+  return guard(ctx, [&] {
+    gpk_ctx* c = ctx;
+    c->require_ready();
+    require(cfg != nullptr, "gpk_mbcg: null config");
+    require(c->pkind != 0, "gpkrylov_cuda: no preconditioner");
+    require(t >= 1, "batched_pcg: rhs rows do not match operator");
+    require(cfg->max_iters >= 1, "CgConfig: max_iters must be >= 1");
+    require(cfg->rel_tol > 0.0 && cfg->rel_tol < 1.0, "CgConfig: rel_tol must be in (0, 1)");
+    const int n = c->n;
+    for (int q = 0; q < t; ++q)
+      for (int i = 0; i < n; ++i)
+        if (!std::isfinite(B[q * ldb + i])) fail(GPK_INPUT_ERROR, "KernelOperator: non-finite entries in input vector");
+    const int mi = cfg->max_iters;
+    DBuf<double> db, dx;
+    db.ensure(static_cast<size_t>(t) * c->ldn);
+    dx.ensure(static_cast<size_t>(t) * c->ldn);
+    CK(cudaMemcpy2DAsync(db.p, c->ldn * sizeof(double), B, ldb * sizeof(double), n * sizeof(double), t,
+                         cudaMemcpyHostToDevice, c->st));
+    const bool fp64 = cfg->precision == GPK_PREC_FP64;
+    gpk_ctx::CgOut r;
+    try {
+      r = c->mbcg(db.p, c->ldn, t, mi, cfg->rel_tol, fp64, dx.p, c->ldn, alpha, beta, resid_hist);
+    } catch (const GpkError& e) {
+      int col;
+      const std::string m = strip_col(e.msg, &col);
+      fail(GPK_SOLVER_ERROR, "batched_pcg: column " + std::to_string(col) + ": " + m);  // krylov.hpp:149-151
+    }
+    if (!fp64 && cfg->refine > 0) {
+      double mr;
+      c->refine(db.p, c->ldn, t, dx.p, c->ldn, r, mi, cfg->rel_tol, cfg->refine, &mr);
+    }
+    CK(cudaMemcpy2DAsync(X, ldx * sizeof(double), dx.p, c->ldn * sizeof(double), n * sizeof(double), t,
+                         cudaMemcpyDeviceToHost, c->st));
+    c->sync();
+    for (int q = 0; q < t; ++q) {
+      if (iters) iters[q] = r.iters[q];
+      if (converged) converged[q] = r.converged[q];
+    }
+  });
+}
+
+gpk_status gpk_evaluate_mll_device(gpk_ctx* ctx, const double* dy, const double* dZ, int64_t ldz, int l,
+                                   uint64_t probe_seed, const gpk_mll_cfg* cfg, gpk_mll_result* res) {
+  return guard(ctx, [&] { evaluate_impl(ctx, dy, dZ, ldz, l, probe_seed, cfg, res); });
+}
+
+gpk_status gpk_evaluate_mll(gpk_ctx* ctx, const double* y, const double* Z, int64_t ldz, int l, uint64_t probe_seed,
+                            const gpk_mll_cfg* cfg, gpk_mll_result* res) {
+  return guard(ctx, [&] {
+    gpk_ctx* c = ctx;
+    c->require_ready();
+    require(l >= 1, "make_probes: need at least one probe");
+    const int n = c->n;
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(y[i])) fail(GPK_INPUT_ERROR, "KernelOperator: non-finite entries in input vector");
+    DBuf<double> dy, dz;
+    dy.ensure(n);
+    dz.ensure(static_cast<size_t>(l) * c->ldn);
+    c->h2d(dy.p, y, sizeof(double) * n);
+    CK(cudaMemcpy2DAsync(dz.p, c->ldn * sizeof(double), Z, ldz * sizeof(double), n * sizeof(double), l,
+                         cudaMemcpyHostToDevice, c->st));
+    evaluate_impl(c, dy.p, dz.p, c->ldn, l, probe_seed, cfg, res);
+  });
+}
+
+gpk_status gpk_make_probes(int64_t n, int count, uint64_t seed, double* out) {
+  return guard(nullptr, [&] { make_probes_impl(n, count, seed, out); });
+}
+
+uint64_t gpk_mix_seed(uint64_t seed, uint64_t salt) { return mix_seed_impl(seed, salt); }
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// Internal launcher interface between the host driver and the sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gpk {
+
+enum { kRBF = 0, kMatern12 = 1, kMatern32 = 2, kMatern52 = 3 };
+enum { kModeValue = 0, kModeDls = 1 };  // K entries / dK/dlengthscale_j entries
+
+struct MvmArgs {
+  int n;                     // rows/cols of K
+  int n_pad;                 // padded to a multiple of 128
+  int t;                     // active columns
+  long long ldo;             // output leading dimension (column-major)
+  int jdim;                  // lengthscale index for kModeDls
+  int jtiles_per_split;      // j-tiles (of 32) handled by one split
+  double scale;              // output scale (o^2, 2o, -2 o^2 / l_j / c_fam, ...)
+  long long split_stride;    // element offset between split-K partial outputs
+};
+
+// Packed-operand geometry for a given column count.
+struct MvmShape {
+  int tn;    // columns per thread (8 column groups)
+  int vld;   // leading dimension (elements) of the packed V rows
+  int cgs;   // column-group stride
+};
+MvmShape mvm_shape(int t, bool fp64, int mode);
+int dpad_for(int d);  // padded dimension of the packed coordinates
+// Scale applied to the scaled coordinates in FP32 mode: s' = c_fam * s.
+double prescale_c(int family);
+
+// Fused kernel MVM on packed operands: X [n_pad][DP], V [n_pad][vld] (mvm_shape layout).
+// out: column-major [t][ldo] fp64 (split-K partials use split_stride, then reduced).
+cudaError_t launch_fused_kmvm(bool fp64, int family, int dp, int mode, const void* X, const void* V,
+                              double* out, const MvmArgs& a, int splits, cudaStream_t st);
+cudaError_t launch_reduce_splits(const double* part, int splits, long long split_stride, int t, int n,
+                                 long long ldpart, double* out, long long ldo, cudaStream_t st);
+
+// Pack fp64 column-major X (n x d) into the scaled row-major MVM layouts.
+cudaError_t launch_pack_x(const double* X, long long ldx, int n, int d, int n_pad, const double* ls,
+                          double prescale, int dp32, float* X32, int dp64, double* X64s, double* sx_colmajor,
+                          double* sqnorm, cudaStream_t st);
+// Pack fp64 column-major V (t columns, ld) into the packed MVM layout; optional slot->column map.
+cudaError_t launch_pack_v32(const double* V, long long ldv, const int* colmap, int t, int n, int n_pad,
+                            MvmShape sh, float* V32, cudaStream_t st);
+cudaError_t launch_pack_v64(const double* V, long long ldv, const int* colmap, int t, int n, int n_pad,
+                            MvmShape sh, double* V64, cudaStream_t st);
+
+// Reference-formula kernel column (kernels.hpp:235-243) / derivative column (:252-267), fp64.
+// which < 0: K[:, p];  which == 0: outputscale;  1..d: lengthscale which-1.
+cudaError_t launch_kernel_column(int family, const double* sx, const double* x, const double* sq, int n, int d,
+                                 long long p, int which, double o2, double fac, double* out, cudaStream_t st);
+
+// Bilinear derivative contraction (backward pass, fast mode): for w = 0..d
+//   quad[w]  = sum_ab dK_w[a,b] u_a u_b
+//   gamma[w] = sum_ab dK_w[a,b] sum_i S[a,i] Z[b,i]
+// returns the raw (unscaled) sums; the host applies the factors.
+cudaError_t launch_deriv_contract(bool fp64, int family, int dp, const void* X, const void* U, const void* Zt,
+                                  int n, int n_pad, int l, int d, double* partials, int* nblocks,
+                                  cudaStream_t st);
+
+}  // namespace gpk

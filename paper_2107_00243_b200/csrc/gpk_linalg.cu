@@ -1,0 +1,563 @@
+// mBCG vector kernels, Woodbury skinny GEMMs, pivoted Cholesky (fp64).
+//
+// All n-length state is fp64, column-major [slot][ldn].  Every reduction uses a
+// fixed partition of rows into 1024-row chunks and a fixed tree, so results are
+// deterministic and a column's value never depends on the other columns of the
+// block (batched_pcg contract, krylov.hpp:131-132).
+#include <cfloat>
+
+#include "gpk_common.cuh"
+#include "gpk_linalg.h"
+
+namespace gpk {
+
+constexpr int kRB = 1024;  // rows per reduction chunk
+constexpr int kVT = 256;   // threads per vector-kernel block
+
+// ---------------------------------------------------------------------------
+// per-column dot partials:  part[slot][chunk] = sum_{i in chunk} f(i, slot)
+// ---------------------------------------------------------------------------
+template <int OP>
+__global__ void dot_partials_kernel(const double* __restrict__ A, const double* __restrict__ B, double sig2, int n,
+                                    long long ldn, int nrb, double* __restrict__ part) {
+  __shared__ double red[kVT / 32];
+  const int s = blockIdx.y;
+  const int b = blockIdx.x;
+  const double* a = A + s * ldn;
+  const double* bb = B + s * ldn;
+  double acc = 0.0;
+  for (int q = 0; q < kRB / kVT; ++q) {
+    const int i = b * kRB + q * kVT + threadIdx.x;
+    if (i < n) {
+      if constexpr (OP == 0) acc += a[i] * bb[i];                        // a . b
+      if constexpr (OP == 1) acc += a[i] * (bb[i] + sig2 * a[i]);        // p . (K p + s2 p)
+    }
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) part[static_cast<long long>(s) * nrb + b] = t;
+}
+
+// total[slot] = sum over chunks in a fixed tree
+GPK_DEV double reduce_chunks(const double* __restrict__ part, int nrb, double* red) {
+  double acc = 0.0;
+  for (int c = threadIdx.x; c < nrb; c += blockDim.x) acc += part[c];
+  return block_sum(acc, red);
+}
+
+int num_chunks(int n) { return (n + kRB - 1) / kRB; }
+
+cudaError_t launch_dot_partials(int op, const double* A, const double* B, double sig2, int n, long long ldn, int t,
+                                double* part, cudaStream_t st) {
+  if (t <= 0) return cudaSuccess;
+  dim3 g(num_chunks(n), t);
+  if (op == 0) dot_partials_kernel<0><<<g, kVT, 0, st>>>(A, B, sig2, n, ldn, g.x, part);
+  else dot_partials_kernel<1><<<g, kVT, 0, st>>>(A, B, sig2, n, ldn, g.x, part);
+  return cudaGetLastError();
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ part, int nrb, double* __restrict__ out) {
+  __shared__ double red[kVT / 32];
+  const double v = reduce_chunks(part + static_cast<long long>(blockIdx.x) * nrb, nrb, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = v;
+}
+
+cudaError_t launch_reduce_partials(const double* part, int nrb, int t, double* out, cudaStream_t st) {
+  if (t <= 0) return cudaSuccess;
+  reduce_partials_kernel<<<t, kVT, 0, st>>>(part, nrb, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// CG scalar steps (krylov.hpp:76-119), one block per active slot
+// ---------------------------------------------------------------------------
+__global__ void cg_init_kernel(const double* __restrict__ part_rz, const double* __restrict__ part_zz, int nrb,
+                               SlotState* __restrict__ ss) {
+  __shared__ double red[kVT / 32];
+  const int s = blockIdx.x;
+  const double rz = reduce_chunks(part_rz + static_cast<long long>(s) * nrb, nrb, red);
+  const double zz = reduce_chunks(part_zz + static_cast<long long>(s) * nrb, nrb, red);
+  if (threadIdx.x == 0) {
+    SlotState& x = ss[s];
+    x.rz = rz;
+    x.norm0 = sqrt(zz);  // ||P^{-1} b|| (krylov.hpp:59-60)
+    x.iters = 0;
+    x.status = 0;
+    x.alpha_prev = 0.0;
+    x.beta_prev = 0.0;
+    x.flag = (x.norm0 == 0.0) ? kFlagConverged : 0;  // zero rhs: converged, 0 iterations (:61-64)
+    x.alpha = 0.0;
+  }
+}
+
+__global__ void cg_alpha_kernel(const double* __restrict__ part_pap, int nrb, int k, SlotState* __restrict__ ss,
+                                double* __restrict__ alpha_hist, int max_iters) {
+  __shared__ double red[kVT / 32];
+  const int s = blockIdx.x;
+  const double pap = reduce_chunks(part_pap + static_cast<long long>(s) * nrb, nrb, red);
+  if (threadIdx.x == 0) {
+    SlotState& x = ss[s];
+    const double alpha = x.rz / pap;
+    x.alpha = alpha;
+    if (!isfinite(alpha) || alpha <= 0.0) {  // krylov.hpp:79-83
+      x.status = kStatusAlpha;
+      x.bad = alpha;
+      x.iters = k;
+      x.flag = kFlagError;
+      x.alpha = 0.0;  // freeze the column
+      return;
+    }
+    if (alpha_hist) alpha_hist[static_cast<long long>(x.col) * max_iters + (k - 1)] = alpha;
+  }
+}
+
+__global__ void cg_beta_kernel(const double* __restrict__ part_rz, const double* __restrict__ part_zz, int nrb,
+                               int k, double rel_tol, SlotState* __restrict__ ss, double* __restrict__ beta_hist,
+                               double* __restrict__ resid_hist, int max_iters) {
+  __shared__ double red[kVT / 32];
+  const int s = blockIdx.x;
+  const double rz_new = reduce_chunks(part_rz + static_cast<long long>(s) * nrb, nrb, red);
+  const double zz = reduce_chunks(part_zz + static_cast<long long>(s) * nrb, nrb, red);
+  if (threadIdx.x == 0) {
+    SlotState& x = ss[s];
+    if (x.flag != 0) {
+      x.beta = 0.0;
+      return;
+    }
+    if (!isfinite(rz_new) || rz_new < 0.0) {  // krylov.hpp:97-100
+      x.status = kStatusRz;
+      x.bad = rz_new;
+      x.iters = k;
+      x.flag = kFlagError;
+      x.beta = 0.0;
+      return;
+    }
+    const double pres = sqrt(zz);  // :102
+    const long long base = static_cast<long long>(x.col) * max_iters + (k - 1);
+    if (resid_hist) resid_hist[base] = pres;
+    x.iters = k;
+    if (pres <= rel_tol * x.norm0 || rz_new == 0.0) {  // :106-113
+      x.flag = kFlagConverged;
+      x.beta = 0.0;
+      return;
+    }
+    const double beta = rz_new / x.rz;  // :115
+    if (beta_hist) beta_hist[base] = beta;
+    x.beta = beta;
+    x.rz = rz_new;
+  }
+}
+
+// x += alpha p ; r -= alpha (Kp + s2 p)     (krylov.hpp:94-95)
+__global__ void cg_update_xr_kernel(double* __restrict__ X, double* __restrict__ R, const double* __restrict__ P,
+                                    const double* __restrict__ Y, double sig2, int n, long long ldn,
+                                    const SlotState* __restrict__ ss) {
+  const int s = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const SlotState& x = ss[s];
+  if (x.flag == kFlagError) return;
+  const double a = x.alpha;
+  const long long o = s * ldn + i;
+  const double p = P[o];
+  const double ap = Y[o] + sig2 * p;
+  X[o] += a * p;
+  R[o] -= a * ap;
+}
+
+// p = z + beta p  for slots that keep iterating   (krylov.hpp:116)
+__global__ void cg_update_p_kernel(double* __restrict__ P, const double* __restrict__ Z, int n, long long ldn,
+                                   const SlotState* __restrict__ ss) {
+  const int s = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const SlotState& x = ss[s];
+  if (x.flag != 0) return;
+  const long long o = s * ldn + i;
+  P[o] = Z[o] + x.beta * P[o];
+}
+
+cudaError_t launch_cg_init(const double* part_rz, const double* part_zz, int nrb, int t, SlotState* ss,
+                           cudaStream_t st) {
+  cg_init_kernel<<<t, kVT, 0, st>>>(part_rz, part_zz, nrb, ss);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_alpha(const double* part, int nrb, int t, int k, SlotState* ss, double* alpha_hist,
+                            int max_iters, cudaStream_t st) {
+  cg_alpha_kernel<<<t, kVT, 0, st>>>(part, nrb, k, ss, alpha_hist, max_iters);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_beta(const double* part_rz, const double* part_zz, int nrb, int t, int k, double rel_tol,
+                           SlotState* ss, double* beta_hist, double* resid_hist, int max_iters, cudaStream_t st) {
+  cg_beta_kernel<<<t, kVT, 0, st>>>(part_rz, part_zz, nrb, k, rel_tol, ss, beta_hist, resid_hist, max_iters);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_update_xr(double* X, double* R, const double* P, const double* Y, double sig2, int n,
+                                long long ldn, int t, const SlotState* ss, cudaStream_t st) {
+  dim3 g((n + kVT - 1) / kVT, t);
+  cg_update_xr_kernel<<<g, kVT, 0, st>>>(X, R, P, Y, sig2, n, ldn, ss);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_update_p(double* P, const double* Z, int n, long long ldn, int t, const SlotState* ss,
+                               cudaStream_t st) {
+  dim3 g((n + kVT - 1) / kVT, t);
+  cg_update_p_kernel<<<g, kVT, 0, st>>>(P, Z, n, ldn, ss);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// elementwise helpers
+// ---------------------------------------------------------------------------
+// dst[s][i] = src[map ? map[s] : s][i] * scale (gather + scale), or zero when src is null
+__global__ void gather_cols_kernel(const double* __restrict__ src, long long lds, const int* __restrict__ map,
+                                   double scale, int n, double* __restrict__ dst, long long ldd) {
+  const int s = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = 0.0;
+  if (src) v = src[static_cast<long long>(map ? map[s] : s) * lds + i] * scale;
+  dst[static_cast<long long>(s) * ldd + i] = v;
+}
+cudaError_t launch_gather_cols(const double* src, long long lds, const int* map, double scale, int n, int t,
+                               double* dst, long long ldd, cudaStream_t st) {
+  if (t <= 0) return cudaSuccess;
+  dim3 g((n + kVT - 1) / kVT, t);
+  gather_cols_kernel<<<g, kVT, 0, st>>>(src, lds, map, scale, n, dst, ldd);
+  return cudaGetLastError();
+}
+// dst[map[s]][i] = src[s][i] (scatter)
+__global__ void scatter_cols_kernel(const double* __restrict__ src, long long lds, const int* __restrict__ map, int n,
+                                    double* __restrict__ dst, long long ldd) {
+  const int s = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  dst[static_cast<long long>(map[s]) * ldd + i] = src[static_cast<long long>(s) * lds + i];
+}
+cudaError_t launch_scatter_cols(const double* src, long long lds, const int* map, int n, int t, double* dst,
+                                long long ldd, cudaStream_t st) {
+  if (t <= 0) return cudaSuccess;
+  dim3 g((n + kVT - 1) / kVT, t);
+  scatter_cols_kernel<<<g, kVT, 0, st>>>(src, lds, map, n, dst, ldd);
+  return cudaGetLastError();
+}
+// a = alpha*a + beta*b (elementwise over t columns)
+__global__ void axpby_kernel(double* __restrict__ a, const double* __restrict__ b, double alpha, double beta, int n,
+                             long long ld) {
+  const int s = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long o = s * ld + i;
+  a[o] = alpha * a[o] + beta * b[o];
+}
+cudaError_t launch_axpby(double* a, const double* b, double alpha, double beta, int n, int t, long long ld,
+                         cudaStream_t st) {
+  if (t <= 0) return cudaSuccess;
+  dim3 g((n + kVT - 1) / kVT, t);
+  axpby_kernel<<<g, kVT, 0, st>>>(a, b, alpha, beta, n, ld);
+  return cudaGetLastError();
+}
+// Woodbury finish (preconditioners.hpp:114-118): z = r / s2 - T / s2  (T = C (L^T r))
+__global__ void woodbury_finish_kernel(const double* __restrict__ R, const double* __restrict__ T, double sig2, int n,
+                                       long long ldn, double* __restrict__ Z) {
+  const int s = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long o = s * ldn + i;
+  const double r = R[o] / sig2;
+  Z[o] = T ? r - T[o] / sig2 : r;
+}
+cudaError_t launch_woodbury_finish(const double* R, const double* T, double sig2, int n, long long ldn, int t,
+                                   double* Z, cudaStream_t st) {
+  if (t <= 0) return cudaSuccess;
+  dim3 g((n + kVT - 1) / kVT, t);
+  woodbury_finish_kernel<<<g, kVT, 0, st>>>(R, T, sig2, n, ldn, Z);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Skinny fp64 GEMMs for the Woodbury solve, Gram matrix and trace terms.
+//   G1: W[s][kk] = sum_i A[kk][i] * B[s][i]     (A^T B, A: [ka][lda], B: [tb][ldb])
+//       per 4096-row chunk partials, then a fixed-order chunk reduction.
+//   G2: T[s][i]  = sum_kk A[kk][i] * W[s][kk]   (A W,  sequential kk order)
+// ---------------------------------------------------------------------------
+constexpr int kG1Chunk = 4096;
+constexpr int kG1T = 32;  // tile along ka and tb
+
+__global__ void g1_kernel(const double* __restrict__ A, long long lda, int ka, const double* __restrict__ B,
+                          long long ldb, int tb, int n, double* __restrict__ part) {
+  __shared__ double As[32][kG1T + 1];
+  __shared__ double Bs[32][kG1T + 1];
+  const int chunk = blockIdx.x;
+  const int k0 = blockIdx.y * kG1T;
+  const int s0 = blockIdx.z * kG1T;
+  const int tx = threadIdx.x & 31;   // kk within tile
+  const int ty = threadIdx.x >> 5;   // 8 groups of 4 slots
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int i0 = chunk * kG1Chunk;
+  const int i1 = min(n, i0 + kG1Chunk);
+  for (int ib = i0; ib < i1; ib += 32) {
+    // load 32 rows x 32 cols of A and B (coalesced along rows)
+    for (int e = threadIdx.x; e < 32 * kG1T; e += blockDim.x) {
+      const int r = e & 31, c = e >> 5;
+      const int i = ib + r;
+      As[r][c] = (i < i1 && k0 + c < ka) ? A[static_cast<long long>(k0 + c) * lda + i] : 0.0;
+      Bs[r][c] = (i < i1 && s0 + c < tb) ? B[static_cast<long long>(s0 + c) * ldb + i] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+      const double av = As[r][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += av * Bs[r][ty * 4 + q];
+    }
+    __syncthreads();
+  }
+  const int kk = k0 + tx;
+  if (kk < ka) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int s = s0 + ty * 4 + q;
+      if (s < tb) part[(static_cast<long long>(chunk) * tb + s) * ka + kk] = acc[q];
+    }
+  }
+}
+
+__global__ void g1_reduce_kernel(const double* __restrict__ part, int nch, int ka, int tb, double* __restrict__ W,
+                                 long long ldw) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(ka) * tb) return;
+  const int s = static_cast<int>(idx / ka), kk = static_cast<int>(idx % ka);
+  double acc = 0.0;
+  for (int c = 0; c < nch; ++c) acc += part[(static_cast<long long>(c) * tb + s) * ka + kk];
+  W[s * ldw + kk] = acc;
+}
+
+size_t g1_workspace(int n, int ka, int tb) {
+  return static_cast<size_t>((n + kG1Chunk - 1) / kG1Chunk) * ka * tb;
+}
+
+cudaError_t launch_g1(const double* A, long long lda, int ka, const double* B, long long ldb, int tb, int n,
+                      double* part, double* W, long long ldw, cudaStream_t st) {
+  if (ka <= 0 || tb <= 0) return cudaSuccess;
+  const int nch = (n + kG1Chunk - 1) / kG1Chunk;
+  dim3 g(nch, (ka + kG1T - 1) / kG1T, (tb + kG1T - 1) / kG1T);
+  g1_kernel<<<g, 256, 0, st>>>(A, lda, ka, B, ldb, tb, n, part);
+  const long long tot = static_cast<long long>(ka) * tb;
+  g1_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(part, nch, ka, tb, W, ldw);
+  return cudaGetLastError();
+}
+
+// G2: one thread per row, 16 slots per thread; W staged through shared memory.
+constexpr int kG2S = 16;
+constexpr int kG2K = 64;
+__global__ void g2_kernel(const double* __restrict__ A, long long lda, int ka, const double* __restrict__ W,
+                          long long ldw, int tb, int n, double* __restrict__ T, long long ldt) {
+  __shared__ double Ws[kG2K][kG2S];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int s0 = blockIdx.y * kG2S;
+  double acc[kG2S];
+#pragma unroll
+  for (int q = 0; q < kG2S; ++q) acc[q] = 0.0;
+  for (int k0 = 0; k0 < ka; k0 += kG2K) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kG2K * kG2S; e += blockDim.x) {
+      const int kk = e / kG2S, q = e % kG2S;
+      Ws[kk][q] = (k0 + kk < ka && s0 + q < tb) ? W[static_cast<long long>(s0 + q) * ldw + k0 + kk] : 0.0;
+    }
+    __syncthreads();
+    if (i < n) {
+      const int kmax = min(kG2K, ka - k0);
+      for (int kk = 0; kk < kmax; ++kk) {
+        const double av = A[static_cast<long long>(k0 + kk) * lda + i];
+#pragma unroll
+        for (int q = 0; q < kG2S; ++q) acc[q] += av * Ws[kk][q];
+      }
+    }
+  }
+  if (i < n) {
+#pragma unroll
+    for (int q = 0; q < kG2S; ++q)
+      if (s0 + q < tb) T[static_cast<long long>(s0 + q) * ldt + i] = acc[q];
+  }
+}
+
+cudaError_t launch_g2(const double* A, long long lda, int ka, const double* W, long long ldw, int tb, int n,
+                      double* T, long long ldt, cudaStream_t st) {
+  if (tb <= 0) return cudaSuccess;
+  dim3 g((n + 127) / 128, (tb + kG2S - 1) / kG2S);
+  g2_kernel<<<g, 128, 0, st>>>(A, lda, ka, W, ldw, tb, n, T, ldt);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Pivoted Cholesky (preconditioners.hpp:236-264), fp64, operation order of the
+// reference: g = L[i,:s] . L[p,:s] (sequential), c_i -= g, L[i,s] = c_i / sqrt(d_p),
+// d_i -= L[i,s]^2.  Each block also emits its (max d, lowest index) for the next pivot.
+// ---------------------------------------------------------------------------
+__global__ void pchol_step_kernel(double* __restrict__ L, long long ldl, int s, long long p, double root,
+                                  const double* __restrict__ col, double* __restrict__ dg, int n,
+                                  double* __restrict__ bval, long long* __restrict__ bidx) {
+  extern __shared__ double lp[];  // L[p, 0..s)
+  __shared__ double sv[kVT / 32];
+  __shared__ long long si[kVT / 32];
+  for (int c = threadIdx.x; c < s; c += blockDim.x) lp[c] = L[static_cast<long long>(c) * ldl + p];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double best = -DBL_MAX;
+  long long bi = 0x7fffffffffffffffLL;
+  if (i < n) {
+    double g = 0.0;
+    for (int c = 0; c < s; ++c) g = __dadd_rn(g, __dmul_rn(L[static_cast<long long>(c) * ldl + i], lp[c]));
+    const double v = __ddiv_rn(__dsub_rn(col[i], g), root);
+    L[static_cast<long long>(s) * ldl + i] = v;
+    const double dn = __dsub_rn(dg[i], __dmul_rn(v, v));
+    dg[i] = dn;
+    best = dn;
+    bi = i;
+  }
+  // (max, lowest index) block reduction
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    sv[wid] = best;
+    si[wid] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < blockDim.x / 32; ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+        best = sv[w];
+        bi = si[w];
+      }
+    bval[blockIdx.x] = best;
+    bidx[blockIdx.x] = bi;
+  }
+}
+
+__global__ void argmax_finalize_kernel(const double* __restrict__ bval, const long long* __restrict__ bidx, int nb,
+                                       double* __restrict__ out_val, long long* __restrict__ out_idx) {
+  __shared__ double sv[kVT];
+  __shared__ long long si[kVT];
+  double best = -DBL_MAX;
+  long long bi = 0x7fffffffffffffffLL;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (bval[b] > best || (bval[b] == best && bidx[b] < bi)) {
+      best = bval[b];
+      bi = bidx[b];
+    }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double ov = sv[threadIdx.x + o];
+      const long long oi = si[threadIdx.x + o];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out_val = sv[0];
+    *out_idx = si[0];
+  }
+}
+
+// (max, lowest index) over an arbitrary vector (initial pivot).
+__global__ void argmax_blocks_kernel(const double* __restrict__ v, int n, double* __restrict__ bval,
+                                     long long* __restrict__ bidx) {
+  __shared__ double sv[kVT];
+  __shared__ long long si[kVT];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  sv[threadIdx.x] = i < n ? v[i] : -DBL_MAX;
+  si[threadIdx.x] = i < n ? i : 0x7fffffffffffffffLL;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double ov = sv[threadIdx.x + o];
+      const long long oi = si[threadIdx.x + o];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bval[blockIdx.x] = sv[0];
+    bidx[blockIdx.x] = si[0];
+  }
+}
+
+int pchol_blocks(int n) { return (n + kVT - 1) / kVT; }
+
+cudaError_t launch_argmax(const double* v, int n, double* bval, long long* bidx, double* out_val,
+                          long long* out_idx, cudaStream_t st) {
+  const int nb = pchol_blocks(n);
+  argmax_blocks_kernel<<<nb, kVT, 0, st>>>(v, n, bval, bidx);
+  argmax_finalize_kernel<<<1, kVT, 0, st>>>(bval, bidx, nb, out_val, out_idx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pchol_step(double* L, long long ldl, int s, long long p, double root, const double* col, double* dg,
+                              int n, double* bval, long long* bidx, double* out_val, long long* out_idx,
+                              cudaStream_t st) {
+  const int nb = pchol_blocks(n);
+  const size_t sm = sizeof(double) * static_cast<size_t>(s > 0 ? s : 1);
+  pchol_step_kernel<<<nb, kVT, sm, st>>>(L, ldl, s, p, root, col, dg, n, bval, bidx);
+  argmax_finalize_kernel<<<1, kVT, 0, st>>>(bval, bidx, nb, out_val, out_idx);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Frozen-pivot derivative factors (preconditioners.hpp:278-293), batched over
+// the non-noise parameters (blockIdx.y = w):
+//   dc = dKcol_w - dL_w[:, :s] L[p, :s]' - L[:, :s] dL_w[p, :s]'
+//   dL_w[:, s] = dc / L[p,s] - L[:, s] * (dc[p] / (2 L[p,s] L[p,s]))
+// ---------------------------------------------------------------------------
+__global__ void dl_step_kernel(const double* __restrict__ L, long long ldl, double* __restrict__ dL, long long wstride,
+                               int s, long long p, const double* __restrict__ dcol, long long dcol_stride, int n) {
+  extern __shared__ double sh[];  // [0,s): L[p,:s]; [s,2s): dL_w[p,:s]
+  __shared__ double dd_sh;
+  const int w = blockIdx.y;
+  double* dLw = dL + w * wstride;
+  const double* dcw = dcol + w * dcol_stride;
+  for (int c = threadIdx.x; c < s; c += blockDim.x) {
+    sh[c] = L[static_cast<long long>(c) * ldl + p];
+    sh[s + c] = dLw[static_cast<long long>(c) * ldl + p];
+  }
+  __syncthreads();
+  auto dc_at = [&](long long i) {
+    double g1 = 0.0, g2 = 0.0;
+    for (int c = 0; c < s; ++c) g1 = __dadd_rn(g1, __dmul_rn(dLw[static_cast<long long>(c) * ldl + i], sh[c]));
+    for (int c = 0; c < s; ++c) g2 = __dadd_rn(g2, __dmul_rn(L[static_cast<long long>(c) * ldl + i], sh[s + c]));
+    return __dsub_rn(__dsub_rn(dcw[i], g1), g2);
+  };
+  if (threadIdx.x == 0) dd_sh = dc_at(p);
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double root = L[static_cast<long long>(s) * ldl + p];
+  const double dc = dc_at(i);
+  const double corr = __ddiv_rn(dd_sh, __dmul_rn(__dmul_rn(2.0, root), root));
+  dLw[static_cast<long long>(s) * ldl + i] =
+      __dsub_rn(__ddiv_rn(dc, root), __dmul_rn(L[static_cast<long long>(s) * ldl + i], corr));
+}
+
+cudaError_t launch_dl_step(const double* L, long long ldl, double* dL, long long wstride, int nw, int s, long long p,
+                           const double* dcol, long long dcol_stride, int n, cudaStream_t st) {
+  dim3 g(pchol_blocks(n), nw);
+  const size_t sm = sizeof(double) * static_cast<size_t>(2 * (s > 0 ? s : 1));
+  dl_step_kernel<<<g, kVT, sm, st>>>(L, ldl, dL, wstride, s, p, dcol, dcol_stride, n);
+  return cudaGetLastError();
+}
+
+}  // namespace gpk

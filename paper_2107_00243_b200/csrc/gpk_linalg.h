@@ -1,0 +1,55 @@
+// Launchers for the mBCG vector kernels, Woodbury GEMMs and pivoted Cholesky.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace gpk {
+
+enum { kFlagConverged = 1, kFlagError = 2 };
+enum { kStatusOk = 0, kStatusAlpha = 1, kStatusRz = 2 };
+
+// Per-column CG scalars (krylov.hpp:66-68), resident on the device.
+struct SlotState {
+  double rz, norm0, alpha, beta, alpha_prev, beta_prev, bad;
+  int col, iters, status, flag;
+};
+
+int num_chunks(int n);
+cudaError_t launch_dot_partials(int op, const double* A, const double* B, double sig2, int n, long long ldn, int t,
+                                double* part, cudaStream_t st);
+cudaError_t launch_reduce_partials(const double* part, int nrb, int t, double* out, cudaStream_t st);
+cudaError_t launch_cg_init(const double* part_rz, const double* part_zz, int nrb, int t, SlotState* ss,
+                           cudaStream_t st);
+cudaError_t launch_cg_alpha(const double* part, int nrb, int t, int k, SlotState* ss, double* alpha_hist,
+                            int max_iters, cudaStream_t st);
+cudaError_t launch_cg_beta(const double* part_rz, const double* part_zz, int nrb, int t, int k, double rel_tol,
+                           SlotState* ss, double* beta_hist, double* resid_hist, int max_iters, cudaStream_t st);
+cudaError_t launch_cg_update_xr(double* X, double* R, const double* P, const double* Y, double sig2, int n,
+                                long long ldn, int t, const SlotState* ss, cudaStream_t st);
+cudaError_t launch_cg_update_p(double* P, const double* Z, int n, long long ldn, int t, const SlotState* ss,
+                               cudaStream_t st);
+cudaError_t launch_gather_cols(const double* src, long long lds, const int* map, double scale, int n, int t,
+                               double* dst, long long ldd, cudaStream_t st);
+cudaError_t launch_scatter_cols(const double* src, long long lds, const int* map, int n, int t, double* dst,
+                                long long ldd, cudaStream_t st);
+cudaError_t launch_axpby(double* a, const double* b, double alpha, double beta, int n, int t, long long ld,
+                         cudaStream_t st);
+cudaError_t launch_woodbury_finish(const double* R, const double* T, double sig2, int n, long long ldn, int t,
+                                   double* Z, cudaStream_t st);
+
+size_t g1_workspace(int n, int ka, int tb);
+cudaError_t launch_g1(const double* A, long long lda, int ka, const double* B, long long ldb, int tb, int n,
+                      double* part, double* W, long long ldw, cudaStream_t st);
+cudaError_t launch_g2(const double* A, long long lda, int ka, const double* W, long long ldw, int tb, int n,
+                      double* T, long long ldt, cudaStream_t st);
+
+int pchol_blocks(int n);
+cudaError_t launch_argmax(const double* v, int n, double* bval, long long* bidx, double* out_val,
+                          long long* out_idx, cudaStream_t st);
+cudaError_t launch_pchol_step(double* L, long long ldl, int s, long long p, double root, const double* col, double* dg,
+                              int n, double* bval, long long* bidx, double* out_val, long long* out_idx,
+                              cudaStream_t st);
+cudaError_t launch_dl_step(const double* L, long long ldl, double* dL, long long wstride, int nw, int s, long long p,
+                           const double* dcol, long long dcol_stride, int n, cudaStream_t st);
+
+}  // namespace gpk

@@ -1,0 +1,214 @@
+// Fused-MVM front end: operand packing, split-K reduction, shape selection,
+// and the reference-formula kernel columns used by the pivoted Cholesky.
+#include <cmath>
+
+#include "gpk_mvm.cuh"
+
+namespace gpk {
+
+template <int FAM>
+cudaError_t launch_fused_kmvm_fam(bool fp64, int dp, int mode, int tn, const void* X, const void* V, double* out,
+                                  const MvmArgs& a, dim3 g, cudaStream_t st);
+
+int dpad_for(int d) {
+  if (d <= 4) return 4;
+  if (d <= 12) return 12;
+  if (d <= 20) return 20;
+  if (d <= 32) return 32;
+  return -1;
+}
+
+static int pick_tn(int need, const int* set, int nset) {
+  for (int i = 0; i < nset; ++i)
+    if (set[i] >= need) return set[i];
+  return -1;
+}
+
+// Derivative launches use a coarser TN set (parity / reference-faithful path only).
+MvmShape mvm_shape(int t, bool fp64, int mode) {
+  static const int f32[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 16};
+  static const int f32d[] = {1, 2, 4, 8, 16};
+  static const int f64[] = {1, 2, 4, 8};
+  const int need = (t + kNCG - 1) / kNCG;
+  MvmShape s{};
+  if (fp64) s.tn = pick_tn(need, f64, 4);
+  else s.tn = mode == kModeValue ? pick_tn(need, f32, 12) : pick_tn(need, f32d, 5);
+  if (s.tn < 0) return s;
+  const int w = fp64 ? 2 : 4;
+  const int tnp = (s.tn + w - 1) / w * w;
+  s.cgs = (!fp64 && (tnp % 8) == 0) ? tnp + 4 : tnp;
+  s.vld = kNCG * s.cgs;
+  return s;
+}
+
+double prescale_c(int family) {
+  const double l2e = 1.4426950408889634;
+  switch (family) {
+    case kRBF: return 0.5 * l2e;
+    case kMatern12: return l2e * l2e;
+    case kMatern32: return 3.0 * l2e * l2e;
+    case kMatern52: return 5.0 * l2e * l2e;
+  }
+  return 1.0;
+}
+
+cudaError_t launch_fused_kmvm(bool fp64, int family, int dp, int mode, const void* X, const void* V, double* out,
+                              const MvmArgs& a, int splits, cudaStream_t st) {
+  const MvmShape sh = mvm_shape(a.t, fp64, mode);
+  if (sh.tn < 0) return cudaErrorInvalidValue;
+  dim3 g(a.n_pad / kBM, splits);
+  switch (family) {
+    case kRBF: return launch_fused_kmvm_fam<kRBF>(fp64, dp, mode, sh.tn, X, V, out, a, g, st);
+    case kMatern12: return launch_fused_kmvm_fam<kMatern12>(fp64, dp, mode, sh.tn, X, V, out, a, g, st);
+    case kMatern32: return launch_fused_kmvm_fam<kMatern32>(fp64, dp, mode, sh.tn, X, V, out, a, g, st);
+    case kMatern52: return launch_fused_kmvm_fam<kMatern52>(fp64, dp, mode, sh.tn, X, V, out, a, g, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// out[c][i] = sum_s part[s][c][i], fixed order s = 0..splits-1.
+__global__ void reduce_splits_kernel(const double* __restrict__ part, int splits, long long sstride, int t, int n,
+                                     long long ldp, double* __restrict__ out, long long ldo) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long total = static_cast<long long>(t) * n;
+  if (idx >= total) return;
+  const int c = static_cast<int>(idx / n);
+  const int i = static_cast<int>(idx % n);
+  double s = 0.0;
+  for (int k = 0; k < splits; ++k) s += part[k * sstride + c * ldp + i];
+  out[c * ldo + i] = s;
+}
+
+cudaError_t launch_reduce_splits(const double* part, int splits, long long sstride, int t, int n, long long ldpart,
+                                 double* out, long long ldo, cudaStream_t st) {
+  const long long total = static_cast<long long>(t) * n;
+  const int thr = 256;
+  reduce_splits_kernel<<<static_cast<unsigned>((total + thr - 1) / thr), thr, 0, st>>>(part, splits, sstride, t, n,
+                                                                                       ldpart, out, ldo);
+  return cudaGetLastError();
+}
+
+// kernels.hpp:166-168: scaled_x = X / l, sqnorms = row squared norms; plus the
+// packed row-major fp32 (pre-scaled) and fp64 operands of the fused MVM.
+__global__ void pack_x_kernel(const double* __restrict__ X, long long ldx, int n, int d, int n_pad,
+                              const double* __restrict__ ls, double prescale, int dp32, float* __restrict__ X32,
+                              int dp64, double* __restrict__ X64s, double* __restrict__ sx, double* __restrict__ sq) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  const double pre = sqrt(prescale);
+  double acc = 0.0;
+  for (int k = 0; k < dp32 || k < dp64; ++k) {
+    double v = 0.0;
+    if (i < n && k < d) {
+      // the reference divides by the lengthscale (kernels.hpp:166)
+      v = __ddiv_rn(X[k * ldx + i], ls[k]);
+      sx[static_cast<long long>(k) * n + i] = v;
+      acc = __dadd_rn(acc, __dmul_rn(v, v));
+    }
+    if (k < dp32) X32[static_cast<long long>(i) * dp32 + k] = static_cast<float>(v * pre);
+    if (k < dp64) X64s[static_cast<long long>(i) * dp64 + k] = v;
+  }
+  if (i < n) sq[i] = acc;
+}
+
+cudaError_t launch_pack_x(const double* X, long long ldx, int n, int d, int n_pad, const double* ls,
+                          double prescale, int dp32, float* X32, int dp64, double* X64s, double* sx, double* sq,
+                          cudaStream_t st) {
+  pack_x_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(X, ldx, n, d, n_pad, ls, prescale, dp32, X32, dp64, X64s, sx,
+                                                      sq);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void pack_v_kernel(const double* __restrict__ V, long long ldv, const int* __restrict__ colmap, int t,
+                              int n, int n_pad, int tn, int cgs, int vld, T* __restrict__ out) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long total = static_cast<long long>(n_pad) * vld;
+  if (idx >= total) return;
+  const int i = static_cast<int>(idx / vld);
+  const int e = static_cast<int>(idx % vld);
+  const int g = e / cgs, q = e % cgs;
+  const int c = g * tn + q;
+  double v = 0.0;
+  if (q < tn && c < t && i < n) {
+    const int col = colmap ? colmap[c] : c;
+    v = V[col * ldv + i];
+  }
+  out[idx] = static_cast<T>(v);
+}
+
+cudaError_t launch_pack_v32(const double* V, long long ldv, const int* colmap, int t, int n, int n_pad, MvmShape sh,
+                            float* V32, cudaStream_t st) {
+  const long long total = static_cast<long long>(n_pad) * sh.vld;
+  pack_v_kernel<float><<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(V, ldv, colmap, t, n, n_pad, sh.tn,
+                                                                                   sh.cgs, sh.vld, V32);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_v64(const double* V, long long ldv, const int* colmap, int t, int n, int n_pad, MvmShape sh,
+                            double* V64, cudaStream_t st) {
+  const long long total = static_cast<long long>(n_pad) * sh.vld;
+  pack_v_kernel<double><<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(V, ldv, colmap, t, n, n_pad,
+                                                                                    sh.tn, sh.cgs, sh.vld, V64);
+  return cudaGetLastError();
+}
+
+// kernels.hpp:235-243 (which < 0) and :252-267 (which >= 0), bit-faithful
+// operation order: s = (sq_r + sq_p) - 2 <sx_r, sx_p>, clamped; no FMA contraction.
+__device__ double ref_shape(int f, double s) {
+  switch (f) {
+    case kRBF: return exp(-0.5 * s);
+    case kMatern12: return exp(-sqrt(s));
+    case kMatern32: {
+      const double r = sqrt(__dmul_rn(3.0, s));
+      return __dmul_rn(__dadd_rn(1.0, r), exp(-r));
+    }
+    default: {
+      const double r = sqrt(__dmul_rn(5.0, s));
+      return __dmul_rn(__dadd_rn(__dadd_rn(1.0, r), __ddiv_rn(__dmul_rn(r, r), 3.0)), exp(-r));
+    }
+  }
+}
+__device__ double ref_shape_ds(int f, double s) {
+  switch (f) {
+    case kRBF: return __dmul_rn(-0.5, exp(-0.5 * s));
+    case kMatern12: {
+      if (s <= 0.0) return 0.0;
+      const double r = sqrt(s);
+      return __ddiv_rn(-exp(-r), __dmul_rn(2.0, r));
+    }
+    case kMatern32: return __dmul_rn(-1.5, exp(-sqrt(__dmul_rn(3.0, s))));
+    default: {
+      const double r = sqrt(__dmul_rn(5.0, s));
+      return __dmul_rn(__dmul_rn(-(5.0 / 6.0), __dadd_rn(1.0, r)), exp(-r));
+    }
+  }
+}
+
+__global__ void kernel_column_kernel(int f, const double* __restrict__ sx, const double* __restrict__ x,
+                                     const double* __restrict__ sq, int n, int d, long long p, int which, double o2,
+                                     double fac, double* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double g = 0.0;
+  for (int k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(sx[static_cast<long long>(k) * n + r], sx[k * n + p]));
+  double s = __dsub_rn(__dadd_rn(sq[r], sq[p]), __dmul_rn(2.0, g));
+  s = s > 0.0 ? s : 0.0;
+  if (which < 0) {
+    out[r] = __dmul_rn(o2, ref_shape(f, s));
+  } else if (which == 0) {
+    out[r] = __dmul_rn(fac, __dmul_rn(o2, ref_shape(f, s)));  // (2/o) * kernel_column
+  } else {
+    const int j = which - 1;
+    const double dx = __dsub_rn(x[static_cast<long long>(j) * n + r], x[static_cast<long long>(j) * n + p]);
+    out[r] = __dmul_rn(fac, __dmul_rn(ref_shape_ds(f, s), __dmul_rn(dx, dx)));
+  }
+}
+
+cudaError_t launch_kernel_column(int family, const double* sx, const double* x, const double* sq, int n, int d,
+                                 long long p, int which, double o2, double fac, double* out, cudaStream_t st) {
+  kernel_column_kernel<<<(n + 255) / 256, 256, 0, st>>>(family, sx, x, sq, n, d, p, which, o2, fac, out);
+  return cudaGetLastError();
+}
+
+}  // namespace gpk

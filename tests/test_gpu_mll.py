@@ -1,0 +1,232 @@
+"""GPU parity of the batched solver and of evaluate_mll against the oracle
+(live on small seeded problems, and against the committed golden fixtures at
+the BASELINE C1 workload)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_2107_00243_b200 as gk
+from paper_2107_00243_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def make_op(fam, x, p, d):
+    return gk.KernelOperator(gk.KernelSpec(fam), x, gk.Hyperparameters(p.log_o, np.array(p.log_ls), p.log_noise))
+
+
+# ---------------------------------------------------------------------------
+# batched solver (krylov.hpp)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("rank", [-1, 0, 8])
+def test_mbcg_fp64_matches_oracle_pcg(orc, rank):
+    n, d = 400, 2
+    x = orc.random_matrix(n, d, 26)
+    p = orc.Params(d, 1.0, 0.7, 0.05)
+    b = orc.random_matrix(n, 6, 260)
+    want, wit, wcv = orc.pcg_kernel(orc.RBF, x, p, b, rank=rank, max_iters=300, rel_tol=1e-8)
+    op = make_op("rbf", x, p, d)
+    prec = gk.IdentityPreconditioner(op) if rank < 0 else gk.pivoted_cholesky(op, rank)
+    res = gk.batched_pcg(op, b, prec, gk.CgConfig(300, 1e-8, True, "fp64", 0))
+    for c in range(6):
+        assert abs(res[c].iterations_used - wit[c]) <= 1
+        assert res[c].converged == bool(wcv[c])
+        assert rel(res[c].solution, want[:, c]) < 1e-7
+
+
+def test_mbcg_tridiagonal_matches_oracle(orc):
+    n = 300
+    x = orc.random_matrix(n, 1, 61)
+    p = orc.Params(1, 1.0, 0.4, 0.05)
+    k = orc.dense(orc.RBF, x, p)
+    z = orc.make_probes(n, 1, 99)[:, 0]
+    want = orc.pcg_dense(k, z, max_iters=40, rel_tol=1e-10, collect=True)
+    op = make_op("rbf", x, p, 1)
+    r = gk.pcg_solve(op, z, gk.IdentityPreconditioner(op), gk.CgConfig(40, 1e-10, True, "fp64", 0))
+    m = min(r.iterations_used, want["iterations"])
+    assert abs(r.iterations_used - want["iterations"]) <= 1
+    assert np.allclose(r.tridiag.diag[:m], want["tdiag"][:m], rtol=1e-7)
+    assert np.allclose(r.tridiag.subdiag[:m - 1], want["tsub"][:m - 1], rtol=1e-7)
+    assert np.allclose(r.residual_history[:m], want["residual_history"][:m], rtol=1e-6)
+
+
+def test_mbcg_batched_equals_independent_bitwise(orc):
+    n, d = 1000, 3
+    x = orc.random_matrix(n, d, 27)
+    p = orc.Params(d, 1.0, 0.6, 0.02)
+    b = orc.random_matrix(n, 12, 270)
+    op = make_op("matern32", x, p, d)
+    pc = gk.pivoted_cholesky(op, 20)
+    for prec in ("fp64", "fp32"):
+        cfg = gk.CgConfig(200, 1e-6, True, prec, 0)
+        batch = gk.batched_pcg(op, b, pc, cfg)
+        for c in (0, 5, 11):
+            single = gk.batched_pcg(op, b[:, [c]], pc, cfg)[0]
+            assert single.iterations_used == batch[c].iterations_used
+            assert np.array_equal(single.solution, batch[c].solution)
+            assert np.array_equal(single.tridiag.diag, batch[c].tridiag.diag)
+
+
+def test_mbcg_zero_rhs_and_max_iters(orc):
+    n = 200
+    x = orc.random_matrix(n, 2, 28)
+    p = orc.Params(2, 1.0, 0.5, 0.01)
+    op = make_op("rbf", x, p, 2)
+    pc = gk.pivoted_cholesky(op, 4)
+    b = orc.random_matrix(n, 3, 281)
+    b[:, 1] = 0.0
+    res = gk.batched_pcg(op, b, pc, gk.CgConfig(3, 1e-12, False, "fp64", 0))
+    assert res[1].iterations_used == 0 and res[1].converged and np.linalg.norm(res[1].solution) == 0.0
+    assert res[0].iterations_used == 3 and not res[0].converged
+    with pytest.raises(gk.InputError):
+        gk.batched_pcg(op, b, pc, gk.CgConfig(0, 1e-6))
+    with pytest.raises(gk.InputError):
+        gk.batched_pcg(op, b, pc, gk.CgConfig(10, 0.0))
+
+
+def test_preconditioning_does_not_increase_iterations(orc):
+    xb = orc.random_matrix(2000, 1, 27)
+    x, b = xb[:1000], xb[1000:, 0]
+    p = orc.Params(1, 1.0, 0.5, 1e-2)
+    op = make_op("rbf", x, p, 1)
+    plain = gk.pcg_solve(op, b, gk.IdentityPreconditioner(op), gk.CgConfig(1000, 1e-6, False, "fp64", 0))
+    pc = gk.pivoted_cholesky(op, 32)
+    pre = gk.pcg_solve(op, b, pc, gk.CgConfig(1000, 1e-6, False, "fp64", 0))
+    assert pre.iterations_used <= plain.iterations_used and pre.converged
+
+
+def test_fp32_refinement_meets_true_residual(orc):
+    # solves matching to relative residual 1e-6 (north star), audited in fp64 by the oracle
+    n, d = 1500, 3
+    x = orc.random_matrix(n, d, 71)
+    p = orc.Params(d, 1.0, 0.8, 0.01)
+    b = orc.random_matrix(n, 4, 72)
+    op = make_op("rbf", x, p, d)
+    pc = gk.pivoted_cholesky(op, 30)
+    L = pc.factor()
+    res = gk.batched_pcg(op, b, pc, gk.CgConfig(500, 1e-6, False, "fp32", 3))
+    kx = orc.kernel_apply(orc.RBF, x, p, np.stack([r.solution for r in res], 1))
+    for c in range(4):
+        assert res[c].converged
+        r_true = b[:, c] - kx[:, c]
+        num = np.linalg.norm(orc.dplr(0.01, L, r_true)["solve"])
+        den = np.linalg.norm(orc.dplr(0.01, L, b[:, c])["solve"])
+        assert num / den <= 1.05e-6
+
+
+# ---------------------------------------------------------------------------
+# evaluate_mll (gp_likelihood.hpp:51-103)
+# ---------------------------------------------------------------------------
+def c1_case():
+    w = workloads.config("C1")
+    x, y = workloads.generate(w)
+    hp = gk.Hyperparameters.from_raw(w.d, w.outputscale, lengthscales=w.lengthscales, noise=w.noise)
+    seed = gk.mix_seed(workloads.PROBE_SEED, 1)
+    z = gk.make_probes(w.n, w.probes, seed)
+    return w, x, y, hp, z
+
+
+def test_c1_inputs_match_golden():
+    g = json.load(open(os.path.join(GOLD, "c1_oracle.json")))
+    w, x, y, hp, z = c1_case()
+    assert float(np.sum(x * np.arange(1, x.size + 1).reshape(x.shape))) == pytest.approx(g["x_sha"], rel=1e-14)
+    assert float(y.sum()) == pytest.approx(g["y_sum"], rel=1e-14)
+
+
+@pytest.mark.parametrize("precision,backward,tol_v,tol_g", [
+    ("fp64", "faithful", 1e-7, 1e-6),
+    ("fp64", "fused", 1e-6, 1e-4),
+    ("fp32", "fused", 1e-4, 1e-4),
+    ("fp32", "faithful", 1e-4, 1e-4),
+])
+def test_c1_evaluate_mll_matches_oracle(precision, backward, tol_v, tol_g):
+    g = json.load(open(os.path.join(GOLD, "c1_oracle.json")))
+    w, x, y, hp, z = c1_case()
+    op = gk.KernelOperator(gk.KernelSpec("rbf"), x, hp)
+    pc = gk.pivoted_cholesky_with_derivatives(op, w.rank)
+    assert pc.pivots() == g["pivots"]  # identical pivot sequence
+    cfg = gk.MllConfig(gk.CgConfig(w.max_iters, w.rel_tol, False, precision, 2), True, backward)
+    r = gk.evaluate_mll(y, op, pc, z, cfg)
+    assert r.value == pytest.approx(g["value"], rel=tol_v)
+    assert r.logdet == pytest.approx(g["logdet"], rel=tol_v)
+    assert r.quad == pytest.approx(g["quad"], rel=tol_v)
+    assert r.solve_iterations == g["solve_iterations"]
+    for wi in range(len(g["gradient"])):
+        assert r.gradient[wi] == pytest.approx(g["gradient"][wi], rel=tol_g), wi
+    if backward == "faithful":
+        np.testing.assert_allclose(r.backward_gammas, np.array(g["backward_gammas"]), rtol=10 * tol_g, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", range(8))
+@pytest.mark.parametrize("backward", ["faithful", "fused"])
+def test_grid_evaluate_mll_matches_oracle(orc, case, backward):
+    g = json.load(open(os.path.join(GOLD, "grid_oracle.json")))[case]
+    x = orc.random_matrix(g["n"], g["d"], g["x_seed"])
+    y = np.sin(2 * x[:, 0]) + 0.1 * orc.random_matrix(g["n"], 1, g["y_seed"])[:, 0]
+    fam = ["rbf", "matern12", "matern32", "matern52"][g["family"]]
+    hp = gk.Hyperparameters.from_raw(g["d"], 1.1, 0.8, 0.05)
+    op = gk.KernelOperator(gk.KernelSpec(fam), x, hp)
+    pc = gk.pivoted_cholesky_with_derivatives(op, g["rank"])
+    z = gk.make_probes(g["n"], g["l"], g["probe_seed"])
+    r = gk.evaluate_mll(y, op, pc, z, gk.MllConfig(gk.CgConfig(200, 1e-8, False, "fp64", 0), True, backward))
+    assert r.value == pytest.approx(g["value"], rel=1e-9)
+    np.testing.assert_allclose(r.gradient, g["gradient"], rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(r.forward_gammas, g["forward_gammas"], rtol=1e-7, atol=1e-12)
+
+
+def test_identity_and_unshared_probes_match_oracle(orc):
+    n, d = 250, 2
+    x = orc.random_matrix(n, d, 85)
+    y = orc.random_matrix(n, 1, 86)[:, 0]
+    p = orc.Params(d, 1.0, 0.7, 0.05)
+    z = orc.make_probes(n, 4, 9)
+    for share in (True, False):
+        want = orc.evaluate_mll(orc.RBF, x, p, y, z, seed=9, prec="identity", share_probes=share, max_iters=300,
+                                rel_tol=1e-9)
+        op = make_op("rbf", x, p, d)
+        ip = gk.IdentityPreconditioner(op)
+        for backward in ("faithful", "fused"):
+            r = gk.evaluate_mll(y, op, ip, gk.ProbeBatch(z, 9, 4),
+                                gk.MllConfig(gk.CgConfig(300, 1e-9, False, "fp64", 0), share, backward))
+            assert r.value == pytest.approx(want["value"], rel=1e-9)
+            np.testing.assert_allclose(r.gradient, want["gradient"], rtol=1e-6, atol=1e-9)
+
+
+def test_line_search_frozen_preconditioner(orc):
+    # preconditioner from the step's start theta, K_hat at a trial theta (optimizer.hpp:437 vs :450-451)
+    n, d = 300, 2
+    x = orc.random_matrix(n, d, 87)
+    y = orc.random_matrix(n, 1, 88)[:, 0]
+    p0 = gk.Hyperparameters.from_raw(d, 1.0, 0.7, 0.05)
+    p1 = gk.Hyperparameters.from_raw(d, 1.2, 0.6, 0.04)
+    op = gk.KernelOperator(gk.KernelSpec("matern52"), x, p0)
+    pc = gk.pivoted_cholesky_with_derivatives(op, 10)
+    op.with_params(p1)
+    z = gk.make_probes(n, 6, 3)
+    cfg = gk.MllConfig(gk.CgConfig(300, 1e-10, False, "fp64", 0), True, "faithful")
+    r = gk.evaluate_mll(y, op, pc, z, cfg)
+    v, gr = orc.mll_exact(orc.MATERN52, x, orc.Params(d, 1.2, 0.6, 0.04), y)
+    assert r.value == pytest.approx(v, rel=5e-2)
+    assert np.all(np.isfinite(r.gradient))
+
+
+def test_evaluate_rejects_bad_input(orc):
+    n = 64
+    x = orc.random_matrix(n, 1, 89)
+    op = make_op("rbf", x, orc.Params(1), 1)
+    pc = gk.pivoted_cholesky_with_derivatives(op, 4)
+    z = gk.make_probes(n, 2, 1)
+    bad = np.zeros(n)
+    bad[0] = np.inf
+    with pytest.raises(gk.InputError):
+        gk.evaluate_mll(bad, op, pc, z, gk.MllConfig())
+    with pytest.raises(gk.InputError):
+        gk.evaluate_mll(np.zeros(n + 1), op, pc, z, gk.MllConfig())
