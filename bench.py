@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py — seconds per mLL + gradient evaluation on the BASELINE workload.
+
+One step = one optimizer step's hot path as optimize() runs it
+(optimizer.hpp:448-453 begin_step + :437 objective):  KernelOperator at theta
+(set data + params), pivoted-Cholesky preconditioner of rank k with frozen-
+pivot derivative factors, and evaluate_mll (value + gradient) over [y, Z].
+
+  value : device-resident inputs (X, y, Z already in HBM), gpk_*_device entry points
+  e2e   : the reference-facing C-ABI with HOST buffers (H2D of X, y, Z and D2H of the
+          result inside the timed region)
+
+Default workload: BASELINE configs[1] (C2: n=16384, d=18, Matern-3/2, l=50,
+rank 100; ranks 0 and 500 in "sweep").  --impl reference times the reference
+algorithm's CPU restatement (oracle/, the reference itself cannot be built
+here: Eigen is absent) on the host cores on a bounded sample, extrapolated to a
+full evaluation.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2107_00243_b200 import workloads  # noqa: E402
+
+METRIC = "s per mLL+gradient eval"
+UNIT = "s/eval"
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank_env):
+    import torch
+
+    from paper_2107_00243_b200 import capi
+
+    rank, world, local = rank_env
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = capi.lib()
+    w = workloads.config(args.workload, rank=args.rank)
+    x, y = workloads.generate(w)
+    n, d, l = w.n, w.d, w.probes
+    seed = int(lib.gpk_mix_seed(workloads.PROBE_SEED, 1))
+    z = np.empty((n, l), order="F")
+    assert lib.gpk_make_probes(n, l, C.c_uint64(seed), z.ctypes.data_as(C.POINTER(C.c_double))) == 0
+    log_o, log_ls, log_noise = w.log_params
+    log_ls = np.ascontiguousarray(log_ls)
+    xf = np.asfortranarray(x)
+    # pinned host copies for the e2e arm
+    X_h = torch.from_numpy(np.ascontiguousarray(xf.T)).pin_memory()     # (d, n) == column-major n x d
+    y_h = torch.from_numpy(y.copy()).pin_memory()
+    Z_h = torch.from_numpy(np.ascontiguousarray(z.T)).pin_memory()      # (l, n) == column-major n x l
+    X_d, y_d, Z_d = X_h.to(dev), y_h.to(dev), Z_h.to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
+
+    ctx = C.c_void_p()
+    assert lib.gpk_create(local, C.byref(ctx)) == 0, "gpk_create failed"
+    stream = torch.cuda.ExternalStream(lib.gpk_stream(ctx), device=dev)
+    prec = capi.GPK_PREC_FP64 if args.precision == "fp64" else capi.GPK_PREC_FP32
+    cfg = capi.gpk_mll_cfg(capi.gpk_cg_cfg(w.max_iters, w.rel_tol, 0, prec, args.refine), 1, 1,
+                           0 if args.backward == "fused" else 1)
+    grad = np.zeros(d + 2)
+    fg = np.zeros(l)
+    fi = np.zeros(l, dtype=np.int32)
+    res = capi.gpk_mll_result()
+    res.gradient = grad.ctypes.data_as(C.POINTER(C.c_double))
+    res.forward_gammas = fg.ctypes.data_as(C.POINTER(C.c_double))
+    res.forward_cg_iterations = fi.ctypes.data_as(C.POINTER(C.c_int))
+    Dp = C.POINTER(C.c_double)
+
+    def check(rc):
+        if rc != 0:
+            raise RuntimeError(lib.gpk_last_error(ctx).decode())
+
+    def step_device(rank_k):
+        check(lib.gpk_set_data_device(ctx, C.c_void_p(X_d.data_ptr()), n, d, n))
+        check(lib.gpk_set_params(ctx, w.family, 1.0, log_o, log_ls.ctypes.data_as(Dp), log_noise))
+        if rank_k < 0:
+            check(lib.gpk_precond_identity(ctx))
+        else:
+            check(lib.gpk_pivoted_cholesky(ctx, rank_k, 0.0, w.noise, None, None, None))
+            check(lib.gpk_precond_deriv_factors(ctx))
+        check(lib.gpk_evaluate_mll_device(ctx, C.c_void_p(y_d.data_ptr()), C.c_void_p(Z_d.data_ptr()), n, l,
+                                          C.c_uint64(seed), C.byref(cfg), C.byref(res)))
+
+    def step_host(rank_k):
+        check(lib.gpk_set_data(ctx, X_h.numpy().ctypes.data_as(Dp), n, d, n))
+        check(lib.gpk_set_params(ctx, w.family, 1.0, log_o, log_ls.ctypes.data_as(Dp), log_noise))
+        check(lib.gpk_pivoted_cholesky(ctx, rank_k, 0.0, w.noise, None, None, None))
+        check(lib.gpk_precond_deriv_factors(ctx))
+        check(lib.gpk_evaluate_mll(ctx, y_h.numpy().ctypes.data_as(Dp), Z_h.numpy().ctypes.data_as(Dp), n, l,
+                                   C.c_uint64(seed), C.byref(cfg), C.byref(res)))
+
+    def timed(fn, steps, warmup, rank_k):
+        for _ in range(warmup):
+            fn(rank_k)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        times = []
+        l0 = lib.gpk_launch_count(ctx)
+        check(lib.gpk_profile_reset(ctx))
+        for _ in range(steps):
+            flush.zero_()  # flush L2 between timed iterations (outside the timed region)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn(rank_k)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        torch.cuda.synchronize()
+        launches = (lib.gpk_launch_count(ctx) - l0) // steps
+        return times, launches
+
+    # ---- headline: device-resident value, with live per-launch kernel timing
+    check(lib.gpk_profile_enable(ctx, 1))
+    with ClockSampler(local) as clk:
+        times, launches = timed(step_device, args.steps, args.warmup, w.rank)
+    ms = C.c_double()
+    cnt = C.c_longlong()
+    fl = C.c_double()
+    en = C.c_double()
+    check(lib.gpk_profile_read(ctx, 0, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en)))
+    mvm = {"ms": ms.value, "launches": cnt.value, "flops": fl.value}
+    check(lib.gpk_profile_read(ctx, 1, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en)))
+    dc = {"ms": ms.value, "launches": cnt.value, "flops": fl.value}
+    check(lib.gpk_profile_enable(ctx, 0))
+    telemetry = {"value": res.value, "gradient": grad.tolist(), "logdet": res.logdet,
+                 "solve_iterations": res.solve_iterations, "total_cg_iterations": res.total_cg_iterations,
+                 "forward_cg_iterations_mean": float(np.mean(fi)), "refine_passes": res.refine_passes,
+                 "max_true_rel_residual": res.max_true_rel_residual, "seconds_solve": res.seconds_solve,
+                 "seconds_backward": res.seconds_backward}
+    # ---- e2e through the host C-ABI
+    e2e_times, _ = timed(step_host, max(1, args.steps), 1, w.rank)
+    sweep = {}
+    if not args.no_sweep and w.ranks:
+        for rk in w.ranks:
+            if rk == w.rank:
+                continue
+            tt, _ = timed(step_device, 1, 1, rk)
+            sweep[str(rk)] = {"s_per_eval": tt[0], "total_cg_iterations": res.total_cg_iterations,
+                              "value": res.value}
+    lib.gpk_destroy(ctx)
+    h2d = X_h.numel() * 8 + y_h.numel() * 8 + Z_h.numel() * 8
+    d2h = 8 * (d + 2) + 8 * l + 4 * l + 8 * 8
+    return dict(times=times, e2e_times=e2e_times, launches=launches, mvm=mvm, dc=dc, clocks=clk.summary(),
+                telemetry=telemetry, sweep=sweep, h2d=h2d, d2h=d2h, w=w)
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the reference algorithm's restatement (oracle/) on the host cores
+# ---------------------------------------------------------------------------
+def cpu_sample(w, iters_fwd, budget_s=20.0):
+    """Times MatrixFree applies (kernels.hpp:184-195, 1024-row blocks) with OpenMP over
+    columns (the reference's probe parallelism, krylov.hpp:141 / trace_estimation.hpp:163)
+    and extrapolates the reference's apply count for one evaluate_mll."""
+    import oracle
+
+    cores = oracle.num_threads()
+    x, y = workloads.generate(w)
+    p = oracle.Params(w.d, w.outputscale, lengthscales=w.lengthscales, noise=w.noise)
+    n = w.n
+    # bounded sample: rows subset so that one apply on each core takes ~budget/2
+    t_cols = cores
+    v = np.asfortranarray(np.random.default_rng(0).standard_normal((n, t_cols)))
+    # probe one small apply to size the sample
+    rows = min(n, 2048)
+    xs = x[:rows]
+    t0 = time.perf_counter()
+    oracle.kernel_apply_parallel(w.family, xs, p, v[:rows, :t_cols])
+    t_small = time.perf_counter() - t0
+    # per-apply time scales with rows^2 (n^2 entries per apply)
+    t_apply = t_small * (n / rows) ** 2
+    sample = f"{t_cols} concurrent MatrixFree applies on {rows} of {n} rows (oracle port), scaled by (n/rows)^2"
+    if t_apply < budget_s:  # full-size sample fits the budget: measure it directly
+        t0 = time.perf_counter()
+        oracle.kernel_apply_parallel(w.family, x, p, v)
+        t_apply = time.perf_counter() - t0
+        sample = f"{t_cols} concurrent full-size MatrixFree applies (n={n}, oracle port)"
+    l, d = w.probes, w.d
+    m = iters_fwd
+    # wall-clock apply rounds of evaluate_mll (gp_likelihood.hpp:51-103): the y solve runs alone,
+    # probe solves run `cores` at a time, then (d+1) backward batches of l solves, plus the
+    # (d+1) deriv_applies on u and (d+1) l on the probes.
+    rounds = m + math.ceil(l / cores) * m + (d + 1) * (math.ceil(l / cores) * (m + 1) + 1)
+    return {"value": rounds * t_apply, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": sample + f"; extrapolated x{rounds} apply rounds (m={m} CG iterations)",
+            "seconds_per_apply_round": t_apply, "extrapolated": True}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--rank", type=int, default=None)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--backward", default="fused", choices=["fused", "faithful"])
+    ap.add_argument("--refine", type=int, default=2)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=None, help="CG iterations for the CPU extrapolation")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    peaks, peaks_src = load_peaks()
+    w = workloads.config(args.workload, rank=args.rank)
+    config = {"workload": f"{w.name}: n={w.n} d={w.d} {['rbf', 'matern12', 'matern32', 'matern52'][w.family]} "
+                          f"l={w.probes} rank={w.rank} max_iters={w.max_iters} tol={w.rel_tol}",
+              "n": w.n, "d": w.d, "probes": w.probes, "precond_rank": w.rank, "precision": args.precision,
+              "backward": args.backward, "l2": "flushed between timed steps (256 MB write)",
+              "step": "set_data + set_params + pivoted_cholesky(+deriv factors) + evaluate_mll(value+grad)",
+              "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        iters = args.cpu_iters or w.max_iters
+        cb = cpu_sample(w, iters)
+        cb["cpu_model"] = cpu_model()
+        line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["value"] * 1e3,
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded stand-in for the BASELINE config)", "config": config,
+                "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                            "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    r = run_ours(args, (rank, world, local))
+    import torch
+
+    per_step = max(r["times"]) if False else float(np.mean(r["times"]))
+    e2e = float(np.mean(r["e2e_times"]))
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([per_step, e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per_step, e2e = float(t[0]), float(t[1])
+    # replicas: N independent evaluations per step -> whole-job seconds per evaluation
+    value = per_step / world
+    e2e_value = e2e / world
+    mvm = r["mvm"]
+    fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    achieved = (mvm["flops"] / mvm["launches"]) / (mvm["ms"] / mvm["launches"] / 1e3) / 1e12 if mvm["launches"] else 0
+    clk = r["clocks"]
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak if fp32_peak else None, "traffic": None,
+                "kernel": "fused_kmvm_kernel (fused kernel MVM)",
+                "peak_source": f"FP32 CUDA-core peak = 148 SM x 128 FMA/clk x 2 x sm_max_mhz ({peaks_src} "
+                               f"MEASURED_PEAKS.json sm_max_mhz); tensor cores not used (SURVEY.md §7.3-1)",
+                "flops_per_launch": mvm["flops"] / max(mvm["launches"], 1),
+                "avg_launch_ms": mvm["ms"] / max(mvm["launches"], 1), "launches_per_step":
+                    mvm["launches"] / max(args.steps, 1),
+                "share_of_step": (mvm["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
+    if clk.get("sm_mhz"):
+        roofline["frac_at_inrun_clock"] = achieved / (148 * 128 * 2 * clk["sm_mhz"] * 1e6 / 1e12)
+    dcp = r["dc"]
+    if dcp["launches"]:
+        roofline["deriv_pass"] = {"achieved": (dcp["flops"] / dcp["ms"] * 1e3) / 1e12, "unit": "TFLOP/s",
+                                  "avg_launch_ms": dcp["ms"] / dcp["launches"],
+                                  "share_of_step": (dcp["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 kernel entries / f64 CG state"
+            if args.precision == "fp32" else "f64",
+            "data": "synthetic (seeded stand-in for the BASELINE config; UCI data unavailable offline)",
+            "config": config, "gpu_launches": r["launches"],
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
+            "roofline": roofline, "clocks": {"sm_mhz": clk.get("sm_mhz"), "sm_max_mhz": clk.get("sm_max_mhz"),
+                                             "reasons": clk.get("reasons", [])},
+            "telemetry": r["telemetry"], "sweep": r["sweep"]}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        iters = args.cpu_iters or int(round(r["telemetry"]["forward_cg_iterations_mean"])) or w.max_iters
+        cb = cpu_sample(w, iters)
+        cb["cpu_model"] = cpu_model()
+        line["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -149,6 +149,17 @@ uint64_t gpk_mix_seed(uint64_t seed, uint64_t salt);
 /* Number of this library's kernels launched on ctx since creation. */
 long long gpk_launch_count(const gpk_ctx* ctx);
 
+/* The CUDA stream (cudaStream_t) all of ctx's work is issued on. */
+void* gpk_stream(const gpk_ctx* ctx);
+
+/* Live per-launch timing of the two dominant kernels with CUDA events on ctx's
+ * stream (off by default).  kind 0: fused kernel MVM, 1: fused derivative pass.
+ * Returns accumulated device milliseconds, launch count and algorithmic flops /
+ * kernel entries since the last reset. */
+gpk_status gpk_profile_enable(gpk_ctx* ctx, int on);
+gpk_status gpk_profile_read(gpk_ctx* ctx, int kind, double* ms, long long* launches, double* flops, double* entries);
+gpk_status gpk_profile_reset(gpk_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

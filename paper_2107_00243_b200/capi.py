@@ -73,6 +73,10 @@ SIGNATURES = {
     "gpk_make_probes": (C.c_int, [C.c_int64, C.c_int, C.c_uint64, _D]),
     "gpk_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "gpk_launch_count": (C.c_longlong, [_V]),
+    "gpk_stream": (_V, [_V]),
+    "gpk_profile_enable": (C.c_int, [_V, C.c_int]),
+    "gpk_profile_read": (C.c_int, [_V, C.c_int, _D, C.POINTER(C.c_longlong), _D, _D]),
+    "gpk_profile_reset": (C.c_int, [_V]),
 }
 
 
@@ -102,5 +106,5 @@ def lib():
 def header_functions():
     """Function names declared in include/gpkrylov_cuda.h."""
     src = open(HEADER_PATH).read()
-    return sorted(set(re.findall(r"^\s*(?:gpk_status|void|const char\*|uint64_t|long long)\s+(gpk_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:gpk_status|void\*?|const char\*|uint64_t|long long)\s+(gpk_\w+)\s*\(",
                                  src, flags=re.M)))

@@ -266,6 +266,59 @@ struct gpk_ctx {
 
   // ---- telemetry
   long long entries = 0, flops = 0;
+  struct Prof {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    std::vector<double> pflops, pentries;
+    double ms = 0.0, fl = 0.0, en = 0.0;
+    long long launches = 0;
+  };
+  bool prof_on = false;
+  Prof prof[2];
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t ev_get() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  // bracket one launch of kind `kd` with events when profiling is on
+  std::pair<cudaEvent_t, cudaEvent_t> prof_begin(int kd) {
+    (void)kd;
+    if (!prof_on) return {nullptr, nullptr};
+    cudaEvent_t a = ev_get(), b = ev_get();
+    CK(cudaEventRecord(a, st));
+    return {a, b};
+  }
+  void prof_end(int kd, std::pair<cudaEvent_t, cudaEvent_t> ev, double fl, double en) {
+    if (!ev.first) return;
+    CK(cudaEventRecord(ev.second, st));
+    prof[kd].pending.push_back(ev);
+    prof[kd].pflops.push_back(fl);
+    prof[kd].pentries.push_back(en);
+  }
+  void prof_collect() {
+    for (auto& p : prof) {
+      if (p.pending.empty()) continue;
+      CK(cudaEventSynchronize(p.pending.back().second));
+      for (size_t i = 0; i < p.pending.size(); ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, p.pending[i].first, p.pending[i].second));
+        p.ms += ms;
+        p.fl += p.pflops[i];
+        p.en += p.pentries[i];
+        p.launches += 1;
+        ev_pool.push_back(p.pending[i].first);
+        ev_pool.push_back(p.pending[i].second);
+      }
+      p.pending.clear();
+      p.pflops.clear();
+      p.pentries.clear();
+    }
+  }
 
   void set_device() { CK(cudaSetDevice(device)); }
   void sync() { CK(cudaStreamSynchronize(st)); }
@@ -302,12 +355,27 @@ struct gpk_ctx {
     packed = true;
   }
 
+  // split-K factor: a function of n only (so a column's summation order never
+  // depends on t), chosen so the grid fills whole waves of 2 x 148 CTA slots
   int splits_for() const {
     const int rb = n_pad / 128;
     const int ntiles = n_pad / 32;
-    int s = (2 * 148 + rb - 1) / rb;
-    s = std::max(1, std::min(s, ntiles / 4));
-    const int per = (ntiles + s - 1) / s;
+    const double slots = 2.0 * 148.0;
+    int best = 1;
+    double best_eff = 0.0;
+    const int smax = std::max(1, std::min(64, ntiles / 8));
+    for (int s = 1; s <= smax; ++s) {
+      const int per = (ntiles + s - 1) / s;
+      const int se = (ntiles + per - 1) / per;  // effective splits
+      const double wv = rb * static_cast<double>(se) / slots;
+      const double eff = wv / std::ceil(wv);
+      if (eff > best_eff + 0.02) {
+        best_eff = eff;
+        best = s;
+      }
+      if (wv >= 1.0 && eff >= 0.97) break;
+    }
+    const int per = (ntiles + best - 1) / best;
     return (ntiles + per - 1) / per;
   }
 
@@ -348,22 +416,26 @@ struct gpk_ctx {
       else if (which == 0) a.scale = 2.0 * o;
       else a.scale = (-2.0 * o2 / ls[which - 1]) / c;
       const void* xp = fp64 ? static_cast<const void*>(X64s.p) : static_cast<const void*>(X32.p);
+      const int cf[] = {2, 3, 6, 9};
+      const double fl = static_cast<double>(n) * n * (2.0 * tc + 3.0 * d + cf[family]);
+      auto ev = prof_begin(0);
       if (splits == 1) {
         a.ldo = ldo;
         a.split_stride = 0;
         check_launch(gpk::launch_fused_kmvm(fp64, family, dp, mode, xp, vp, out + c0 * ldo, a, 1, st), 1,
                      "fused_kmvm");
+        prof_end(0, ev, fl, static_cast<double>(n) * n);
       } else {
         a.ldo = n_pad;
         a.split_stride = static_cast<long long>(tc) * n_pad;
         w_y.ensure(static_cast<size_t>(splits) * tc * n_pad);
         check_launch(gpk::launch_fused_kmvm(fp64, family, dp, mode, xp, vp, w_y.p, a, splits, st), 1, "fused_kmvm");
+        prof_end(0, ev, fl, static_cast<double>(n) * n);
         check_launch(gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, n, n_pad, out + c0 * ldo, ldo, st),
                      1, "reduce_splits");
       }
       entries += static_cast<long long>(n) * n;
-      const int cf[] = {2, 3, 6, 9};
-      flops += static_cast<long long>(n) * n * (2LL * tc + 3LL * d + cf[family]);
+      flops += static_cast<long long>(fl);
     }
   }
 
@@ -630,7 +702,8 @@ struct gpk_ctx {
       for (int q = 0; q < nb; ++q) ts[q] = 0.5 * scale[q];
       CgOut c2 = mbcg(Rb.p, ldn, nb, max_iters, rel_tol, false, Eb.p, ldn, nullptr, nullptr, nullptr, &ts);
       (void)c2;
-      // X[:, bad] += E
+      // X[:, bad] += E   (the inner solve reused w_map: upload the column list again)
+      h2d(w_map.p, bad.data(), sizeof(int) * nb);
       w_tmp2.ensure(static_cast<size_t>(nb) * ldn);
       check_launch(gpk::launch_gather_cols(Xd, ldx, w_map.p, 1.0, n, nb, w_tmp2.p, ldn, st), 1, "gather");
       check_launch(gpk::launch_axpby(w_tmp2.p, Eb.p, 1.0, 1.0, n, nb, ldn, st), 1, "axpy");
@@ -906,9 +979,15 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
       const int na = 2 * (c->dp + 1);
       DBuf<double> part;
       part.ensure(static_cast<size_t>(nblk) * na);
+      auto ev = c->prof_begin(1);
       c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, n, n_pad, l, d, part.p, &nblk,
                                                  c->st),
                       1, "deriv_contract");
+      {
+        const int cf[] = {2, 3, 6, 9};
+        const double nn = static_cast<double>(n) * n;
+        c->prof_end(1, ev, nn * ((l + 1) + 2.0 * (d + 1) + 3.0 * d + cf[c->family] + 4.0), nn);
+      }
       std::vector<double> hp(static_cast<size_t>(nblk) * na);
       c->d2h(hp.data(), part.p, sizeof(double) * hp.size());
       std::vector<double> tot(na, 0.0);
@@ -1051,6 +1130,32 @@ void gpk_destroy(gpk_ctx* ctx) {
 
 const char* gpk_last_error(const gpk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 long long gpk_launch_count(const gpk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void* gpk_stream(const gpk_ctx* ctx) { return ctx ? static_cast<void*>(ctx->st) : nullptr; }
+
+gpk_status gpk_profile_enable(gpk_ctx* ctx, int on) {
+  return guard(ctx, [&] { ctx->prof_on = on != 0; });
+}
+gpk_status gpk_profile_read(gpk_ctx* ctx, int kind, double* ms, long long* launches, double* flops,
+                            double* entries) {
+  return guard(ctx, [&] {
+    require(kind == 0 || kind == 1, "gpk_profile_read: kind must be 0 or 1");
+    ctx->prof_collect();
+    const auto& p = ctx->prof[kind];
+    if (ms) *ms = p.ms;
+    if (launches) *launches = p.launches;
+    if (flops) *flops = p.fl;
+    if (entries) *entries = p.en;
+  });
+}
+gpk_status gpk_profile_reset(gpk_ctx* ctx) {
+  return guard(ctx, [&] {
+    ctx->prof_collect();
+    for (auto& p : ctx->prof) {
+      p.ms = p.fl = p.en = 0.0;
+      p.launches = 0;
+    }
+  });
+}
 
 static void set_data_common(gpk_ctx* c, const double* X, int64_t n, int64_t d, int64_t ldx, bool device) {
   require(n >= 1, "KernelOperator: empty dataset");
@@ -1204,29 +1309,29 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
     const int nb = gpk::pchol_blocks(n);
     c->w_argval.ensure(nb + 1);
     c->w_argidx.ensure(nb + 1);
-    long long p = 0;  // argmax of the constant diagonal: lowest index
-    double dp = kmax;
+    // the whole factorisation is enqueued at once; the pivot (argmax, lowest index on
+    // ties) and the stopping rules (:250-253) live in a device-resident state
     int step = 0;
-    for (; step < rank; ++step) {
-      if (dp < -1e-10 * kmax)
-        fail(GPK_NUMERICAL_ERROR, "pivoted_cholesky: negative pivot " + num(dp) + " at step " + std::to_string(step) +
-                                      "; matrix not PSD");
-      if (dp <= diag_tol) break;
-      c->check_launch(gpk::launch_kernel_column(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, p, -1, c->o2, 1.0, col.p,
-                                                c->st),
-                      1, "kernel_column");
-      const double root = std::sqrt(dp);
-      c->check_launch(gpk::launch_pchol_step(c->L.p, n, step, p, root, col.p, dg.p, n, c->w_argval.p, c->w_argidx.p,
-                                             c->w_argval.p + nb, c->w_argidx.p + nb, c->st),
-                      2, "pchol_step");
-      c->pivots.push_back(p);
-      double hv;
-      long long hi;
-      CK(cudaMemcpyAsync(&hv, c->w_argval.p + nb, sizeof(double), cudaMemcpyDeviceToHost, c->st));
-      CK(cudaMemcpyAsync(&hi, c->w_argidx.p + nb, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
-      c->sync();
-      dp = hv;
-      p = hi;
+    if (rank > 0 && !(kmax <= diag_tol)) {  // step 0: diagonal o^2, pivot 0
+      DBuf<gpk::PivotState> ps;
+      DBuf<long long> dpiv;
+      ps.ensure(1);
+      dpiv.ensure(rank);
+      gpk::PivotState h0{};
+      h0.dp = kmax;
+      h0.p = 0;
+      c->h2d(ps.p, &h0, sizeof(h0));
+      c->check_launch(gpk::launch_pchol_dev(c->family, c->sx.p, c->sq.p, n, c->d, c->o2, c->L.p, rank, diag_tol, kmax,
+                                            col.p, dg.p, c->w_argval.p, c->w_argidx.p, ps.p, dpiv.p, c->st),
+                      3 * rank, "pivoted_cholesky");
+      gpk::PivotState hs{};
+      c->d2h(&hs, ps.p, sizeof(hs));
+      step = hs.done;  // steps whose column was produced
+      if (hs.negative)
+        fail(GPK_NUMERICAL_ERROR, "pivoted_cholesky: negative pivot " + num(hs.dp) + " at step " +
+                                      std::to_string(step) + "; matrix not PSD");
+      c->pivots.resize(step);
+      if (step > 0) c->d2h(c->pivots.data(), dpiv.p, sizeof(long long) * step);
     }
     c->k = step;
     if (achieved) *achieved = step;
@@ -1290,20 +1395,23 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
     c->have_dl = false;
     if (k > 0) {
       c->dL.ensure(static_cast<size_t>(nw) * n * k);
-      DBuf<double> dcol;
+      DBuf<double> dcol, facs;
       dcol.ensure(static_cast<size_t>(nw) * n);
+      facs.ensure(nw);
+      std::vector<double> hf(nw);
+      for (int w = 0; w < nw; ++w) {  // kernels.hpp:262 (outputscale) and :270-272 (lengthscales)
+        hf[w] = 2.0 / c->o;
+        if (w >= 1) {
+          const double lj = c->ls[w - 1];
+          hf[w] = -2.0 * c->o2 / (lj * lj * lj);
+        }
+      }
+      c->h2d(facs.p, hf.data(), sizeof(double) * nw);
       for (int s = 0; s < k; ++s) {
         const long long p = c->pivots[s];
-        for (int w = 0; w < nw; ++w) {
-          double fac = 2.0 / c->o;
-          if (w >= 1) {
-            const double lj = c->ls[w - 1];
-            fac = -2.0 * c->o2 / (lj * lj * lj);
-          }
-          c->check_launch(gpk::launch_kernel_column(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, p, w, c->o2, fac,
-                                                    dcol.p + static_cast<size_t>(w) * n, c->st),
-                          1, "kernel_deriv_column");
-        }
+        c->check_launch(gpk::launch_kernel_deriv_columns(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, p, nw, facs.p,
+                                                         c->o2, dcol.p, c->st),
+                        1, "kernel_deriv_columns");
         c->check_launch(gpk::launch_dl_step(c->L.p, n, c->dL.p, static_cast<long long>(n) * k, nw, s, p, dcol.p, n, n,
                                             c->st),
                         1, "dl_step");

@@ -499,6 +499,118 @@ __global__ void argmax_blocks_kernel(const double* __restrict__ v, int n, double
 
 int pchol_blocks(int n) { return (n + kVT - 1) / kVT; }
 
+// ---------------------------------------------------------------------------
+// Device-resident pivot state: the whole factorisation is enqueued without host
+// round trips; a stopped state turns the remaining steps into no-ops.
+// ---------------------------------------------------------------------------
+cudaError_t launch_pchol_column_dev(int f, const double* sx, const double* sq, int n, int d, double o2,
+                                    const PivotState* ps, double* out, cudaStream_t st);  // gpk_mvm.cu
+
+__global__ void pchol_step_dev_kernel(double* __restrict__ L, long long ldl, int s, const double* __restrict__ col,
+                                      double* __restrict__ dg, int n, const PivotState* __restrict__ ps,
+                                      double* __restrict__ bval, long long* __restrict__ bidx) {
+  extern __shared__ double lp[];
+  __shared__ double sv[kVT / 32];
+  __shared__ long long si[kVT / 32];
+  if (ps->stopped) return;
+  const long long p = ps->p;
+  const double root = sqrt(ps->dp);  // preconditioners.hpp:256 (correctly rounded, as std::sqrt)
+  for (int c = threadIdx.x; c < s; c += blockDim.x) lp[c] = L[static_cast<long long>(c) * ldl + p];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double best = -DBL_MAX;
+  long long bi = 0x7fffffffffffffffLL;
+  if (i < n) {
+    double g = 0.0;
+    for (int c = 0; c < s; ++c) g = __dadd_rn(g, __dmul_rn(L[static_cast<long long>(c) * ldl + i], lp[c]));
+    const double v = __ddiv_rn(__dsub_rn(col[i], g), root);
+    L[static_cast<long long>(s) * ldl + i] = v;
+    const double dn = __dsub_rn(dg[i], __dmul_rn(v, v));
+    dg[i] = dn;
+    best = dn;
+    bi = i;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    sv[wid] = best;
+    si[wid] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < blockDim.x / 32; ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+        best = sv[w];
+        bi = si[w];
+      }
+    bval[blockIdx.x] = best;
+    bidx[blockIdx.x] = bi;
+  }
+}
+
+// next pivot (max remaining diagonal, lowest index on ties) and the stopping
+// rules of preconditioners.hpp:250-253 for step s+1
+__global__ void pchol_next_kernel(const double* __restrict__ bval, const long long* __restrict__ bidx, int nb, int s,
+                                  double kmax, double diag_tol, PivotState* __restrict__ ps,
+                                  long long* __restrict__ pivots) {
+  __shared__ double sv[kVT];
+  __shared__ long long si[kVT];
+  if (ps->stopped) return;
+  double best = -DBL_MAX;
+  long long bi = 0x7fffffffffffffffLL;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (bval[b] > best || (bval[b] == best && bidx[b] < bi)) {
+      best = bval[b];
+      bi = bidx[b];
+    }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double ov = sv[threadIdx.x + o];
+      const long long oi = si[threadIdx.x + o];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pivots[s] = ps->p;  // the pivot used at step s
+    ps->dp = sv[0];
+    ps->p = si[0];
+    ps->done = s + 1;
+    if (sv[0] < -1e-10 * kmax) {
+      ps->stopped = 1;
+      ps->negative = 1;
+    } else if (sv[0] <= diag_tol) {
+      ps->stopped = 1;
+    }
+  }
+}
+
+cudaError_t launch_pchol_dev(int family, const double* sx, const double* sq, int n, int d, double o2, double* L,
+                             int rank, double diag_tol, double kmax, double* col, double* dg, double* bval,
+                             long long* bidx, PivotState* ps, long long* pivots, cudaStream_t st) {
+  const int nb = pchol_blocks(n);
+  for (int s = 0; s < rank; ++s) {
+    launch_pchol_column_dev(family, sx, sq, n, d, o2, ps, col, st);
+    const size_t sm = sizeof(double) * static_cast<size_t>(s > 0 ? s : 1);
+    pchol_step_dev_kernel<<<nb, kVT, sm, st>>>(L, n, s, col, dg, n, ps, bval, bidx);
+    pchol_next_kernel<<<1, kVT, 0, st>>>(bval, bidx, nb, s, kmax, diag_tol, ps, pivots);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_argmax(const double* v, int n, double* bval, long long* bidx, double* out_val,
                           long long* out_idx, cudaStream_t st) {
   const int nb = pchol_blocks(n);

@@ -44,6 +44,20 @@ cudaError_t launch_g2(const double* A, long long lda, int ka, const double* W, l
                       double* T, long long ldt, cudaStream_t st);
 
 int pchol_blocks(int n);
+struct PivotState {
+  double dp;        // remaining diagonal at the current pivot
+  long long p;      // current pivot
+  int stopped;      // a stopping rule fired
+  int negative;     // ... because of a negative pivot
+  int done;         // steps completed
+  int pad;
+};
+cudaError_t launch_pchol_dev(int family, const double* sx, const double* sq, int n, int d, double o2, double* L,
+                             int rank, double diag_tol, double kmax, double* col, double* dg, double* bval,
+                             long long* bidx, PivotState* ps, long long* pivots, cudaStream_t st);
+cudaError_t launch_kernel_deriv_columns(int family, const double* sx, const double* x, const double* sq, int n, int d,
+                                        long long p, int nw, const double* facs, double o2, double* out,
+                                        cudaStream_t st);
 cudaError_t launch_argmax(const double* v, int n, double* bval, long long* bidx, double* out_val,
                           long long* out_idx, cudaStream_t st);
 cudaError_t launch_pchol_step(double* L, long long ldl, int s, long long p, double root, const double* col, double* dg,

@@ -2,6 +2,7 @@
 // and the reference-formula kernel columns used by the pivoted Cholesky.
 #include <cmath>
 
+#include "gpk_linalg.h"
 #include "gpk_mvm.cuh"
 
 namespace gpk {
@@ -208,6 +209,57 @@ __global__ void kernel_column_kernel(int f, const double* __restrict__ sx, const
 cudaError_t launch_kernel_column(int family, const double* sx, const double* x, const double* sq, int n, int d,
                                  long long p, int which, double o2, double fac, double* out, cudaStream_t st) {
   kernel_column_kernel<<<(n + 255) / 256, 256, 0, st>>>(family, sx, x, sq, n, d, p, which, o2, fac, out);
+  return cudaGetLastError();
+}
+
+// pivot column with the pivot index read from the device-resident state
+__global__ void pchol_column_dev_kernel(int f, const double* __restrict__ sx, const double* __restrict__ sq, int n,
+                                        int d, double o2, const PivotState* __restrict__ ps,
+                                        double* __restrict__ out) {
+  if (ps->stopped) return;
+  const long long p = ps->p;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double g = 0.0;
+  for (int k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(sx[static_cast<long long>(k) * n + r], sx[k * n + p]));
+  double s = __dsub_rn(__dadd_rn(sq[r], sq[p]), __dmul_rn(2.0, g));
+  s = s > 0.0 ? s : 0.0;
+  out[r] = __dmul_rn(o2, ref_shape(f, s));
+}
+
+cudaError_t launch_pchol_column_dev(int f, const double* sx, const double* sq, int n, int d, double o2,
+                                    const PivotState* ps, double* out, cudaStream_t st) {
+  pchol_column_dev_kernel<<<(n + 255) / 256, 256, 0, st>>>(f, sx, sq, n, d, o2, ps, out);
+  return cudaGetLastError();
+}
+
+// all derivative columns of pivot p at once (blockIdx.y = parameter w = 0..nw-1)
+__global__ void kernel_deriv_columns_kernel(int f, const double* __restrict__ sx, const double* __restrict__ x,
+                                            const double* __restrict__ sq, int n, int d, long long p,
+                                            const double* __restrict__ facs, double o2, double* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int w = blockIdx.y;
+  if (r >= n) return;
+  double g = 0.0;
+  for (int k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(sx[static_cast<long long>(k) * n + r], sx[k * n + p]));
+  double s = __dsub_rn(__dadd_rn(sq[r], sq[p]), __dmul_rn(2.0, g));
+  s = s > 0.0 ? s : 0.0;
+  double v;
+  if (w == 0) {
+    v = __dmul_rn(facs[0], __dmul_rn(o2, ref_shape(f, s)));
+  } else {
+    const int j = w - 1;
+    const double dx = __dsub_rn(x[static_cast<long long>(j) * n + r], x[static_cast<long long>(j) * n + p]);
+    v = __dmul_rn(facs[w], __dmul_rn(ref_shape_ds(f, s), __dmul_rn(dx, dx)));
+  }
+  out[static_cast<long long>(w) * n + r] = v;
+}
+
+cudaError_t launch_kernel_deriv_columns(int family, const double* sx, const double* x, const double* sq, int n, int d,
+                                        long long p, int nw, const double* facs, double o2, double* out,
+                                        cudaStream_t st) {
+  dim3 g((n + 255) / 256, nw);
+  kernel_deriv_columns_kernel<<<g, 256, 0, st>>>(family, sx, x, sq, n, d, p, facs, o2, out);
   return cudaGetLastError();
 }
 

@@ -118,7 +118,8 @@ GPK_DEV T kentry(T s, T dsel) {
 
 // ---------------------------------------------------------------------------
 template <typename T, int FAM, int DP, int TN, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+// 2 CTAs (16 warps) per SM: <= 128 registers per thread
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && TN <= 9) ? 2 : 1)
     fused_kmvm_kernel(const T* __restrict__ X, const T* __restrict__ V, double* __restrict__ out, MvmArgs a) {
   using L = VLayout<T, TN>;
   using Vec = typename VecT<T>::V;
@@ -185,79 +186,106 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < TN; ++c) acc64[r][c] = 0.0;
   }
 
+  // one kernel entry K[pr, j] of the tile staged in xs (two partial sums
+  // shorten the FFMA dependency chain of the distance)
+  auto entry_at = [&](const T* xs, int j) -> T {
+    const Vec* xj = reinterpret_cast<const Vec*>(xs + j * DP);
+    T s0 = T(0), s1 = T(0), dsel = T(0);
+#pragma unroll
+    for (int k = 0; k < DP / W; ++k) {
+      const Vec v = xj[k];
+      T df[W];
+      if constexpr (W == 4) {
+        df[0] = xr[4 * k] - v.x; df[1] = xr[4 * k + 1] - v.y; df[2] = xr[4 * k + 2] - v.z; df[3] = xr[4 * k + 3] - v.w;
+      } else {
+        df[0] = xr[2 * k] - v.x; df[1] = xr[2 * k + 1] - v.y;
+      }
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if (q & 1) s1 = fma(df[q], df[q], s1);
+        else s0 = fma(df[q], df[q], s0);
+        if constexpr (MODE == kModeDls) dsel = (W * k + q == a.jdim) ? df[q] : dsel;
+      }
+    }
+    return kentry<T, FAM, MODE>(s0 + s1, dsel);
+  };
+  // one rank-1 update of the 4 x TN register tile
+  auto mma_step = [&](const T* kb, const T* vs, int kk) {
+    T av[4];
+    if constexpr (W == 4) {
+      const float4 t4 = *reinterpret_cast<const float4*>(kb + kk * kBM + rg * 4);
+      av[0] = t4.x; av[1] = t4.y; av[2] = t4.z; av[3] = t4.w;
+    } else {
+      const double2 t0 = *reinterpret_cast<const double2*>(kb + kk * kBM + rg * 4);
+      const double2 t1 = *reinterpret_cast<const double2*>(kb + kk * kBM + rg * 4 + 2);
+      av[0] = t0.x; av[1] = t0.y; av[2] = t1.x; av[3] = t1.y;
+    }
+    T bv[L::TNP];
+    const Vec* vrow = reinterpret_cast<const Vec*>(vs + kk * VLD);
+#pragma unroll
+    for (int q = 0; q < L::TNP / W; ++q) {
+      const Vec v = vrow[q];
+      if constexpr (W == 4) {
+        bv[4 * q] = v.x; bv[4 * q + 1] = v.y; bv[4 * q + 2] = v.z; bv[4 * q + 3] = v.w;
+      } else {
+        bv[2 * q] = v.x; bv[2 * q + 1] = v.y;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < TN; ++c) acc[r][c] = fma(av[r], bv[c], acc[r][c]);
+  };
+
+  // prologue: entries of tile 0
+  if (nt > 0) {
+    mbar_wait(&bar[0], 0);
+#pragma unroll 2
+    for (int q = 0; q < kBK / 2; ++q) {
+      const int j = ph * (kBK / 2) + q;
+      Ks[j * kBM + pr] = entry_at(Xs, j);
+    }
+  }
+  __syncthreads();
+
+  // steady state: contraction of tile `it` software-pipelined with the entries of tile it+1
   for (int it = 0; it < nt; ++it) {
     const int stage = it % kStages;
-    mbar_wait(&bar[stage], (it / kStages) & 1);
-    T* kb = Ks + (it & 1) * (kBK * kBM);
-    // ---- phase 1: kernel entries K[pr, ph*16 .. ph*16+15]
-    const T* xs = Xs + stage * kBK * DP;
-#pragma unroll 2
-    for (int jj = 0; jj < kBK / 2; ++jj) {
-      const int j = ph * (kBK / 2) + jj;
-      const Vec* xj = reinterpret_cast<const Vec*>(xs + j * DP);
-      T s = T(0), dsel = T(0);
-#pragma unroll
-      for (int k = 0; k < DP / W; ++k) {
-        const Vec v = xj[k];
-        T df[W];
-        if constexpr (W == 4) {
-          df[0] = xr[4 * k] - v.x; df[1] = xr[4 * k + 1] - v.y; df[2] = xr[4 * k + 2] - v.z; df[3] = xr[4 * k + 3] - v.w;
-        } else {
-          df[0] = xr[2 * k] - v.x; df[1] = xr[2 * k + 1] - v.y;
-        }
-#pragma unroll
-        for (int q = 0; q < W; ++q) {
-          s = fma(df[q], df[q], s);
-          if constexpr (MODE == kModeDls) dsel = (W * k + q == a.jdim) ? df[q] : dsel;
-        }
-      }
-      kb[j * kBM + pr] = kentry<T, FAM, MODE>(s, dsel);
-    }
-    __syncthreads();
-    if (tid == 0 && it >= 1 && it - 1 + kStages < nt) {
-      fence_proxy_async();
-      issue((it - 1) % kStages, jt0 + it - 1 + kStages);
-    }
-    // ---- phase 2: acc[4][TN] += K[rows, kk] * V[kk, cols]
+    const bool has_next = it + 1 < nt;
+    const int nstage = (it + 1) % kStages;
+    if (has_next) mbar_wait(&bar[nstage], ((it + 1) / kStages) & 1);
+    const T* kb = Ks + (it & 1) * (kBK * kBM);
+    T* kn = Ks + ((it + 1) & 1) * (kBK * kBM);
+    const T* xsn = Xs + nstage * kBK * DP;
     const T* vs = Vs + stage * kBK * VLD + cg * L::CGS;
+    if (has_next) {
+#pragma unroll 2
+      for (int q = 0; q < kBK / 2; ++q) {
+        const int j = ph * (kBK / 2) + q;
+        kn[j * kBM + pr] = entry_at(xsn, j);
+        mma_step(kb, vs, 2 * q);
+        mma_step(kb, vs, 2 * q + 1);
+      }
+    } else {
 #pragma unroll 4
-    for (int kk = 0; kk < kBK; ++kk) {
-      T av[4];
-      if constexpr (W == 4) {
-        const float4 t4 = *reinterpret_cast<const float4*>(kb + kk * kBM + rg * 4);
-        av[0] = t4.x; av[1] = t4.y; av[2] = t4.z; av[3] = t4.w;
-      } else {
-        const double2 t0 = *reinterpret_cast<const double2*>(kb + kk * kBM + rg * 4);
-        const double2 t1 = *reinterpret_cast<const double2*>(kb + kk * kBM + rg * 4 + 2);
-        av[0] = t0.x; av[1] = t0.y; av[2] = t1.x; av[3] = t1.y;
-      }
-      T bv[L::TNP];
-      const Vec* vrow = reinterpret_cast<const Vec*>(vs + kk * VLD);
-#pragma unroll
-      for (int q = 0; q < L::TNP / W; ++q) {
-        const Vec v = vrow[q];
-        if constexpr (W == 4) {
-          bv[4 * q] = v.x; bv[4 * q + 1] = v.y; bv[4 * q + 2] = v.z; bv[4 * q + 3] = v.w;
-        } else {
-          bv[2 * q] = v.x; bv[2 * q + 1] = v.y;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < TN; ++c) acc[r][c] = fma(av[r], bv[c], acc[r][c]);
+      for (int kk = 0; kk < kBK; ++kk) mma_step(kb, vs, kk);
     }
     if constexpr (sizeof(T) == 4) {
       // fp32 within 4 j-tiles (128 entries), fp64 across them
       if ((it & 3) == 3 || it == nt - 1) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < TN; ++c) {
-          acc64[r][c] += static_cast<double>(acc[r][c]);
-          acc[r][c] = 0.0f;
-        }
+          for (int c = 0; c < TN; ++c) {
+            acc64[r][c] += static_cast<double>(acc[r][c]);
+            acc[r][c] = 0.0f;
+          }
       }
+    }
+    __syncthreads();  // tile `it` fully consumed (X in the previous iteration, V now); K[it+1] complete
+    if (tid == 0 && it + kStages < nt) {
+      fence_proxy_async();
+      issue(stage, jt0 + it + kStages);
     }
   }
 

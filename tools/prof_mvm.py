@@ -1,0 +1,29 @@
+"""Standalone fused-MVM driver for ncu / timing: python tools/prof_mvm.py [n d t family precision reps]."""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2107_00243_b200 as gk  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+d = int(sys.argv[2]) if len(sys.argv) > 2 else 18
+t = int(sys.argv[3]) if len(sys.argv) > 3 else 51
+fam = sys.argv[4] if len(sys.argv) > 4 else "matern32"
+prec = sys.argv[5] if len(sys.argv) > 5 else "fp32"
+reps = int(sys.argv[6]) if len(sys.argv) > 6 else 5
+rng = np.random.default_rng(0)
+x = rng.standard_normal((n, d))
+v = rng.standard_normal((n, t))
+op = gk.KernelOperator(gk.KernelSpec(fam), x, gk.Hyperparameters.from_raw(d, 1.0, 2.0, 0.01))
+lib = op.ctx.lib
+import ctypes as C
+lib.gpk_profile_enable(op.ctx.h, 1)
+for r in range(reps):
+    op.apply(v, precision=prec)
+ms, cnt, fl, en = C.c_double(), C.c_longlong(), C.c_double(), C.c_double()
+lib.gpk_profile_read(op.ctx.h, 0, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en))
+print(f"n={n} d={d} t={t} {fam} {prec}: {ms.value/cnt.value:.3f} ms/launch, {fl.value/ms.value*1e3/1e12:.2f} TFLOP/s "
+      f"({en.value/ms.value*1e3/1e9:.1f} G entries/s) over {cnt.value} launches")
