@@ -114,7 +114,8 @@ def run_ours(args, rank_env):
     w = workloads.config(args.workload, rank=args.rank)
     x, y = workloads.generate(w)
     n, d, l = w.n, w.d, w.probes
-    seed = int(lib.gpk_mix_seed(workloads.PROBE_SEED, 1))
+    # replicas (N > 1): each rank evaluates with its own probe batch (optimizer step rank+1)
+    seed = int(lib.gpk_mix_seed(workloads.PROBE_SEED, 1 + rank))
     z = np.empty((n, l), order="F")
     assert lib.gpk_make_probes(n, l, C.c_uint64(seed), z.ctypes.data_as(C.POINTER(C.c_double))) == 0
     log_o, log_ls, log_noise = w.log_params

@@ -9,7 +9,9 @@
 // The heavy lifting runs in the sm_100a kernels (gpk_mvm*.cu, gpk_deriv.cu,
 // gpk_linalg.cu); this file owns the control flow, O(m^2) tridiagonal
 // eigen-solves, O(k^3) inner Cholesky and error mapping.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -37,6 +39,16 @@ void require(bool c, const std::string& m) {
   if (!c) fail(GPK_INPUT_ERROR, m);
 }
 
+#define CB(x)                                                                            \
+  do {                                                                                   \
+    cublasStatus_t s_ = (x);                                                             \
+    if (s_ != CUBLAS_STATUS_SUCCESS) fail(GPK_CUDA_ERROR, std::string(#x) + ": cuBLAS status " + std::to_string(s_)); \
+  } while (0)
+#define CS(x)                                                                            \
+  do {                                                                                   \
+    cusolverStatus_t s_ = (x);                                                           \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) fail(GPK_CUDA_ERROR, std::string(#x) + ": cuSOLVER status " + std::to_string(s_)); \
+  } while (0)
 #define CK(x)                                                                                    \
   do {                                                                                           \
     cudaError_t e_ = (x);                                                                        \
@@ -156,49 +168,6 @@ double unbiased_variance(const std::vector<double>& v) {
   return ss / static_cast<double>(v.size() - 1);
 }
 
-// host Cholesky (lower, column-major) and inverse of the k x k inner matrix
-bool host_cholesky(std::vector<double>& a, int k) {
-  for (int j = 0; j < k; ++j) {
-    double s = a[j + j * k];
-    for (int c = 0; c < j; ++c) s -= a[j + c * k] * a[j + c * k];
-    if (!(s > 0.0) || !std::isfinite(s)) return false;
-    const double l = std::sqrt(s);
-    a[j + j * k] = l;
-    for (int i = j + 1; i < k; ++i) {
-      double t = a[i + j * k];
-      for (int c = 0; c < j; ++c) t -= a[i + c * k] * a[j + c * k];
-      a[i + j * k] = t / l;
-    }
-  }
-  for (int j = 0; j < k; ++j)
-    for (int i = 0; i < j; ++i) a[i + j * k] = 0.0;
-  return true;
-}
-std::vector<double> host_chol_inverse(const std::vector<double>& l, int k) {
-  std::vector<double> inv(static_cast<size_t>(k) * k, 0.0), col(k);
-  for (int j = 0; j < k; ++j) {
-    std::fill(col.begin(), col.end(), 0.0);
-    col[j] = 1.0;
-    for (int i = 0; i < k; ++i) {
-      double s = col[i];
-      for (int c = 0; c < i; ++c) s -= l[i + c * k] * col[c];
-      col[i] = s / l[i + i * k];
-    }
-    for (int i = k - 1; i >= 0; --i) {
-      double s = col[i];
-      for (int c = i + 1; c < k; ++c) s -= l[c + i * k] * col[c];
-      col[i] = s / l[i + i * k];
-    }
-    for (int i = 0; i < k; ++i) inv[i + j * k] = col[i];
-  }
-  for (int j = 0; j < k; ++j)  // exact symmetry
-    for (int i = j + 1; i < k; ++i) {
-      const double v = 0.5 * (inv[i + j * k] + inv[j + i * k]);
-      inv[i + j * k] = inv[j + i * k] = v;
-    }
-  return inv;
-}
-
 // ---------------------------------------------------------------------------
 // small kernels local to the driver
 // ---------------------------------------------------------------------------
@@ -209,6 +178,10 @@ __global__ void to_padded_kernel(const double* __restrict__ src, long long lds, 
   if (idx >= static_cast<long long>(t) * n_pad) return;
   const int c = static_cast<int>(idx / n_pad), i = static_cast<int>(idx % n_pad);
   dst[idx] = static_cast<T>(i < n ? src[c * lds + i] : 0.0);
+}
+__global__ void add_diag_kernel(double* __restrict__ a, int k, double v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) a[static_cast<long long>(i) * (k + 1)] += v;
 }
 __global__ void fill_kernel(double* __restrict__ p, long long cnt, double v) {
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -318,6 +291,26 @@ struct gpk_ctx {
       p.pflops.clear();
       p.pentries.clear();
     }
+  }
+
+  // library handles for the one-off k x k preconditioner factorisation
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  void ensure_handles() {
+    if (!blas) {
+      CB(cublasCreate(&blas));
+      CB(cublasSetStream(blas, st));
+    }
+    if (!solver) {
+      CS(cusolverDnCreate(&solver));
+      CS(cusolverDnSetStream(solver, st));
+    }
+  }
+  void release_handles() {
+    if (blas) cublasDestroy(blas);
+    if (solver) cusolverDnDestroy(solver);
+    blas = nullptr;
+    solver = nullptr;
   }
 
   void set_device() { CK(cudaSetDevice(device)); }
@@ -1124,6 +1117,13 @@ void gpk_destroy(gpk_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->st);
+  ctx->release_handles();
+  for (auto& p : ctx->prof)
+    for (auto& e : p.pending) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->st);
   delete ctx;
 }
@@ -1338,29 +1338,44 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
     if (pivots_out)
       for (int s = 0; s < step; ++s) pivots_out[s] = c->pivots[s];
     if (remaining_diag) c->d2h(remaining_diag, dg.p, sizeof(double) * n);
-    // DiagPlusLowRank: inner = L'L + s2 I, Cholesky, C = L inner^{-1}, logdet
+    // DiagPlusLowRank (:84-95): inner = L'L + s2 I, Cholesky inner = R R', C = L inner^{-1}
+    // = (L R^-T) R^-1, log det P (:127-133) -- k x k work on the device (cuBLAS/cuSOLVER)
     c->pnoise = noise;
     const int k = c->k;
-    double ld = static_cast<double>(n) * std::log(noise);  // :127-133
+    double ld = static_cast<double>(n) * std::log(noise);
     if (k > 0) {
-      DBuf<double> G, part;
+      c->ensure_handles();
+      DBuf<double> G;
+      DBuf<int> info;
       G.ensure(static_cast<size_t>(k) * k);
-      part.ensure(gpk::g1_workspace(n, k, k));
-      c->check_launch(gpk::launch_g1(c->L.p, n, k, c->L.p, n, k, n, part.p, G.p, k, c->st), 2, "gram");
-      std::vector<double> inner(static_cast<size_t>(k) * k);
-      c->d2h(inner.data(), G.p, sizeof(double) * inner.size());
-      for (int a = 0; a < k; ++a) inner[a + a * k] += noise;
-      if (!host_cholesky(inner, k))
+      info.ensure(1);
+      const double one = 1.0, zero = 0.0;
+      CB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, k, n, &one, c->L.p, n, &zero, G.p, k));
+      add_diag_kernel<<<(k + 255) / 256, 256, 0, c->st>>>(G.p, k, noise);
+      c->check_launch(cudaGetLastError(), 2, "gram");
+      int lwork = 0;
+      CS(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, k, G.p, k, &lwork));
+      DBuf<double> work;
+      work.ensure(static_cast<size_t>(std::max(lwork, 1)));
+      CS(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, k, G.p, k, work.p, lwork, info.p));
+      int hinfo = 0;
+      c->d2h(&hinfo, info.p, sizeof(int));
+      if (hinfo != 0)
         fail(GPK_NUMERICAL_ERROR, "DiagPlusLowRank: inner Cholesky failed (cannot happen for sigma^2 > 0)");
+      std::vector<double> diag(k);
+      CK(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.p, (k + 1) * sizeof(double), sizeof(double), k,
+                           cudaMemcpyDeviceToHost, c->st));
+      c->sync();
       double sl = 0.0;
-      for (int a = 0; a < k; ++a) sl += std::log(inner[a + a * k]);
+      for (int a = 0; a < k; ++a) sl += std::log(diag[a]);
       ld += 2.0 * sl - static_cast<double>(k) * std::log(noise);
-      const std::vector<double> inv = host_chol_inverse(inner, k);
-      DBuf<double> Inv;
-      Inv.ensure(static_cast<size_t>(k) * k);
-      c->h2d(Inv.p, inv.data(), sizeof(double) * inv.size());
       c->C.ensure(static_cast<size_t>(n) * k);
-      c->check_launch(gpk::launch_g2(c->L.p, n, k, Inv.p, k, k, n, c->C.p, n, c->st), 1, "cache");
+      CK(cudaMemcpyAsync(c->C.p, c->L.p, sizeof(double) * static_cast<size_t>(n) * k, cudaMemcpyDeviceToDevice, c->st));
+      CB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, n, k, &one,
+                     G.p, k, c->C.p, n));
+      CB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, k, &one,
+                     G.p, k, c->C.p, n));
+      c->launches += 4;
       c->sync();
     }
     c->plogdet = ld;
@@ -1407,14 +1422,49 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
         }
       }
       c->h2d(facs.p, hf.data(), sizeof(double) * nw);
-      for (int s = 0; s < k; ++s) {
-        const long long p = c->pivots[s];
-        c->check_launch(gpk::launch_kernel_deriv_columns(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, p, nw, facs.p,
-                                                         c->o2, dcol.p, c->st),
-                        1, "kernel_deriv_columns");
-        c->check_launch(gpk::launch_dl_step(c->L.p, n, c->dL.p, static_cast<long long>(n) * k, nw, s, p, dcol.p, n, n,
-                                            c->st),
-                        1, "dl_step");
+      // Left-looking blocks of kB columns: the contribution of all earlier columns to a block is two
+      // strided-batched GEMMs over the parameters, the recursion inside the block one kernel per column
+      // (same formula as preconditioners.hpp:283-290, summation regrouped by block).
+      constexpr int kB = 32;
+      const long long wstride = static_cast<long long>(n) * k;
+      DBuf<double> DC, Lp, dLp;
+      DBuf<long long> dpiv;
+      DC.ensure(static_cast<size_t>(nw) * n * kB);
+      Lp.ensure(static_cast<size_t>(k) * kB);
+      dLp.ensure(static_cast<size_t>(nw) * k * kB);
+      dpiv.ensure(k);
+      c->h2d(dpiv.p, c->pivots.data(), sizeof(long long) * k);
+      c->ensure_handles();
+      for (int s0 = 0; s0 < k; s0 += kB) {
+        const int bb = std::min(kB, k - s0);
+        // DC_w[:, q] = dK_w column of pivot s0+q
+        for (int q = 0; q < bb; ++q)
+          c->check_launch(gpk::launch_kernel_deriv_columns(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d,
+                                                           c->pivots[s0 + q], nw, facs.p, c->o2,
+                                                           dcol.p, c->st),
+                          1, "kernel_deriv_columns"),
+              c->check_launch(gpk::launch_gather_cols(dcol.p, n, nullptr, 1.0, n, nw, DC.p + static_cast<size_t>(q) * n,
+                                                      static_cast<long long>(n) * kB, c->st),
+                              1, "gather");
+        if (s0 > 0) {
+          // Lp[c][q] = L[piv_q, c], dLp_w[c][q] = dL_w[piv_q, c]   (s0 x bb, column-major)
+          c->check_launch(gpk::launch_gather_pivot_rows(c->L.p, n, 0, 1, dpiv.p + s0, s0, bb, Lp.p, c->st), 1,
+                          "gather_pivot_rows");
+          c->check_launch(gpk::launch_gather_pivot_rows(c->dL.p, n, wstride, nw, dpiv.p + s0, s0, bb, dLp.p, c->st),
+                          1, "gather_pivot_rows");
+          const double m1 = -1.0, one = 1.0;
+          // DC_w -= dL_w[:, :s0] Lp ;  DC_w -= L[:, :s0] dLp_w
+          CB(cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, bb, s0, &m1, c->dL.p, n, wstride, Lp.p,
+                                       s0, 0, &one, DC.p, n, static_cast<long long>(n) * kB, nw));
+          CB(cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, bb, s0, &m1, c->L.p, n, 0, dLp.p, s0,
+                                       static_cast<long long>(s0) * bb, &one, DC.p, n,
+                                       static_cast<long long>(n) * kB, nw));
+          c->launches += 2;
+        }
+        for (int q = 0; q < bb; ++q)
+          c->check_launch(gpk::launch_dl_inblock(c->L.p, n, c->dL.p, wstride, nw, s0, q, c->pivots[s0 + q], DC.p,
+                                                 static_cast<long long>(n) * kB, n, c->st),
+                          1, "dl_inblock");
       }
       // tr(P^{-1} dP_w) = 2 sum(C o dL_w)  (algebraically equal to preconditioners.hpp:138-145)
       const int nrb = gpk::num_chunks(n * k);

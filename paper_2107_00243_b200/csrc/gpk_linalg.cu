@@ -4,6 +4,7 @@
 // fixed partition of rows into 1024-row chunks and a fixed tree, so results are
 // deterministic and a column's value never depends on the other columns of the
 // block (batched_pcg contract, krylov.hpp:131-132).
+#include <algorithm>
 #include <cfloat>
 
 #include "gpk_common.cuh"
@@ -279,44 +280,64 @@ cudaError_t launch_woodbury_finish(const double* R, const double* T, double sig2
 //       per 4096-row chunk partials, then a fixed-order chunk reduction.
 //   G2: T[s][i]  = sum_kk A[kk][i] * W[s][kk]   (A W,  sequential kk order)
 // ---------------------------------------------------------------------------
-constexpr int kG1Chunk = 4096;
-constexpr int kG1T = 32;  // tile along ka and tb
+constexpr int kG1T = 64;   // output tile 64 (ka) x 64 (tb), 4 x 4 per thread
+constexpr int kG1R = 16;   // rows per shared-memory sub-tile
 
-__global__ void g1_kernel(const double* __restrict__ A, long long lda, int ka, const double* __restrict__ B,
-                          long long ldb, int tb, int n, double* __restrict__ part) {
-  __shared__ double As[32][kG1T + 1];
-  __shared__ double Bs[32][kG1T + 1];
+// rows per chunk: a function of n only (~256 chunks), multiple of kG1R
+static int g1_chunk(int n) {
+  int ch = (n + 255) / 256;
+  ch = (ch + kG1R - 1) / kG1R * kG1R;
+  return ch < 128 ? 128 : ch;
+}
+
+__global__ void __launch_bounds__(256) g1_kernel(const double* __restrict__ A, long long lda, int ka,
+                                                 const double* __restrict__ B, long long ldb, int tb, int n, int ch,
+                                                 double* __restrict__ part) {
+  __shared__ double As[kG1R][kG1T + 2];
+  __shared__ double Bs[kG1R][kG1T + 2];
   const int chunk = blockIdx.x;
   const int k0 = blockIdx.y * kG1T;
   const int s0 = blockIdx.z * kG1T;
-  const int tx = threadIdx.x & 31;   // kk within tile
-  const int ty = threadIdx.x >> 5;   // 8 groups of 4 slots
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const int i0 = chunk * kG1Chunk;
-  const int i1 = min(n, i0 + kG1Chunk);
-  for (int ib = i0; ib < i1; ib += 32) {
-    // load 32 rows x 32 cols of A and B (coalesced along rows)
-    for (int e = threadIdx.x; e < 32 * kG1T; e += blockDim.x) {
-      const int r = e & 31, c = e >> 5;
+  const int tx = threadIdx.x & 15;  // 4 consecutive kk
+  const int ty = threadIdx.x >> 4;  // 4 consecutive slots
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  const int i0 = chunk * ch;
+  const int i1 = min(n, i0 + ch);
+  for (int ib = i0; ib < i1; ib += kG1R) {
+    for (int e = threadIdx.x; e < kG1R * kG1T; e += blockDim.x) {
+      const int r = e % kG1R, c = e / kG1R;  // 16 consecutive rows of one column per half-warp
       const int i = ib + r;
       As[r][c] = (i < i1 && k0 + c < ka) ? A[static_cast<long long>(k0 + c) * lda + i] : 0.0;
       Bs[r][c] = (i < i1 && s0 + c < tb) ? B[static_cast<long long>(s0 + c) * ldb + i] : 0.0;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int r = 0; r < 32; ++r) {
-      const double av = As[r][tx];
+#pragma unroll 4
+    for (int r = 0; r < kG1R; ++r) {
+      double av[4], bv[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] += av * Bs[r][ty * 4 + q];
+      for (int q = 0; q < 4; ++q) {
+        av[q] = As[r][tx * 4 + q];
+        bv[q] = Bs[r][ty * 4 + q];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
     __syncthreads();
   }
-  const int kk = k0 + tx;
-  if (kk < ka) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int s = s0 + ty * 4 + q;
-      if (s < tb) part[(static_cast<long long>(chunk) * tb + s) * ka + kk] = acc[q];
+  for (int a = 0; a < 4; ++a) {
+    const int kk = k0 + tx * 4 + a;
+    if (kk >= ka) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int s = s0 + ty * 4 + b;
+      if (s < tb) part[(static_cast<long long>(chunk) * tb + s) * ka + kk] = acc[a][b];
     }
   }
 }
@@ -332,15 +353,17 @@ __global__ void g1_reduce_kernel(const double* __restrict__ part, int nch, int k
 }
 
 size_t g1_workspace(int n, int ka, int tb) {
-  return static_cast<size_t>((n + kG1Chunk - 1) / kG1Chunk) * ka * tb;
+  const int ch = g1_chunk(n);
+  return static_cast<size_t>((n + ch - 1) / ch) * ka * tb;
 }
 
 cudaError_t launch_g1(const double* A, long long lda, int ka, const double* B, long long ldb, int tb, int n,
                       double* part, double* W, long long ldw, cudaStream_t st) {
   if (ka <= 0 || tb <= 0) return cudaSuccess;
-  const int nch = (n + kG1Chunk - 1) / kG1Chunk;
+  const int ch = g1_chunk(n);
+  const int nch = (n + ch - 1) / ch;
   dim3 g(nch, (ka + kG1T - 1) / kG1T, (tb + kG1T - 1) / kG1T);
-  g1_kernel<<<g, 256, 0, st>>>(A, lda, ka, B, ldb, tb, n, part);
+  g1_kernel<<<g, 256, 0, st>>>(A, lda, ka, B, ldb, tb, n, ch, part);
   const long long tot = static_cast<long long>(ka) * tb;
   g1_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(part, nch, ka, tb, W, ldw);
   return cudaGetLastError();
@@ -662,6 +685,70 @@ __global__ void dl_step_kernel(const double* __restrict__ L, long long ldl, doub
   const double corr = __ddiv_rn(dd_sh, __dmul_rn(__dmul_rn(2.0, root), root));
   dLw[static_cast<long long>(s) * ldl + i] =
       __dsub_rn(__ddiv_rn(dc, root), __dmul_rn(L[static_cast<long long>(s) * ldl + i], corr));
+}
+
+// Blocked variant (columns s0..s0+b-1 after the block update DC_w -= dL_w[:, :s0] Lp + L[:, :s0] dLp_w was
+// applied by GEMMs): in-block step for column j = s0 + q of every parameter w (blockIdx.y):
+//   dc = DC_w[:, q] - dL_w[:, s0:j] L[p, s0:j]' - L[:, s0:j] dL_w[p, s0:j]'
+//   dL_w[:, j] = dc / L[p,j] - L[:, j] * (dc[p] / (2 L[p,j] L[p,j]))
+// dc[p] is recomputed per CTA with the same operation order as row p's own value.
+__global__ void dl_inblock_kernel(const double* __restrict__ L, long long ldl, double* __restrict__ dL,
+                                  long long wstride, int s0, int q, long long p, const double* __restrict__ DC,
+                                  long long dcw_stride, int n) {
+  __shared__ double lp[64], dlp[64];
+  __shared__ double dd_sh;
+  const int w = blockIdx.y;
+  double* dLw = dL + w * wstride;
+  const double* dcw = DC + w * dcw_stride + static_cast<long long>(q) * ldl;
+  for (int c = threadIdx.x; c < q; c += blockDim.x) {
+    lp[c] = L[static_cast<long long>(s0 + c) * ldl + p];
+    dlp[c] = dLw[static_cast<long long>(s0 + c) * ldl + p];
+  }
+  __syncthreads();
+  auto dc_at = [&](long long i) {
+    double g1 = 0.0, g2 = 0.0;
+    for (int c = 0; c < q; ++c) g1 = __dadd_rn(g1, __dmul_rn(dLw[static_cast<long long>(s0 + c) * ldl + i], lp[c]));
+    for (int c = 0; c < q; ++c) g2 = __dadd_rn(g2, __dmul_rn(L[static_cast<long long>(s0 + c) * ldl + i], dlp[c]));
+    return __dsub_rn(__dsub_rn(dcw[i], g1), g2);
+  };
+  if (threadIdx.x == 0) dd_sh = dc_at(p);
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = s0 + q;
+  const double root = L[static_cast<long long>(j) * ldl + p];
+  const double dc = dc_at(i);
+  const double corr = __ddiv_rn(dd_sh, __dmul_rn(__dmul_rn(2.0, root), root));
+  dLw[static_cast<long long>(j) * ldl + i] =
+      __dsub_rn(__ddiv_rn(dc, root), __dmul_rn(L[static_cast<long long>(j) * ldl + i], corr));
+}
+
+cudaError_t launch_dl_inblock(const double* L, long long ldl, double* dL, long long wstride, int nw, int s0, int q,
+                              long long p, const double* DC, long long dcw_stride, int n, cudaStream_t st) {
+  dim3 g(pchol_blocks(n), nw);
+  dl_inblock_kernel<<<g, kVT, 0, st>>>(L, ldl, dL, wstride, s0, q, p, DC, dcw_stride, n);
+  return cudaGetLastError();
+}
+
+// out[w][q][c] = M_w[piv[q], c] for c < s0  (column-major s0 x b blocks, one per w; wstride 0 => single)
+__global__ void gather_pivot_rows_kernel(const double* __restrict__ M, long long ldm, long long mstride,
+                                         const long long* __restrict__ piv, int s0, int b,
+                                         double* __restrict__ out) {
+  const int w = blockIdx.y;
+  const long long tot = static_cast<long long>(s0) * b;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(e % s0), q = static_cast<int>(e / s0);
+    out[w * tot + e] = M[w * mstride + static_cast<long long>(c) * ldm + piv[q]];
+  }
+}
+
+cudaError_t launch_gather_pivot_rows(const double* M, long long ldm, long long mstride, int nw,
+                                     const long long* piv, int s0, int b, double* out, cudaStream_t st) {
+  const long long tot = static_cast<long long>(s0) * b;
+  dim3 g(static_cast<unsigned>(std::min<long long>((tot + kVT - 1) / kVT, 1024)), nw);
+  gather_pivot_rows_kernel<<<g, kVT, 0, st>>>(M, ldm, mstride, piv, s0, b, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dl_step(const double* L, long long ldl, double* dL, long long wstride, int nw, int s, long long p,

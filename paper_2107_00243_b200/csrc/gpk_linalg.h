@@ -63,6 +63,10 @@ cudaError_t launch_argmax(const double* v, int n, double* bval, long long* bidx,
 cudaError_t launch_pchol_step(double* L, long long ldl, int s, long long p, double root, const double* col, double* dg,
                               int n, double* bval, long long* bidx, double* out_val, long long* out_idx,
                               cudaStream_t st);
+cudaError_t launch_dl_inblock(const double* L, long long ldl, double* dL, long long wstride, int nw, int s0, int q,
+                              long long p, const double* DC, long long dcw_stride, int n, cudaStream_t st);
+cudaError_t launch_gather_pivot_rows(const double* M, long long ldm, long long mstride, int nw,
+                                     const long long* piv, int s0, int b, double* out, cudaStream_t st);
 cudaError_t launch_dl_step(const double* L, long long ldl, double* dL, long long wstride, int nw, int s, long long p,
                            const double* dcol, long long dcol_stride, int n, cudaStream_t st);
 
