@@ -41,7 +41,10 @@ typedef enum { GPK_RBF = 0, GPK_MATERN12 = 1, GPK_MATERN32 = 2, GPK_MATERN52 = 3
  * FP32: fp32 entries (direct-difference distances, SFU exp) with fp32
  * accumulation per 32-column tile and fp64 accumulation across tiles; CG state
  * and all reductions stay fp64. */
-typedef enum { GPK_PREC_FP64 = 0, GPK_PREC_FP32 = 1 } gpk_precision;
+typedef enum { GPK_PREC_FP64 = 0, GPK_PREC_FP32 = 1, GPK_PREC_TF32X3 = 2 } gpk_precision;
+/* GPK_PREC_TF32X3: fp32 kernel entries as in FP32, contraction on the tcgen05 tensor
+ * cores in split precision (a_hi b_hi + a_hi b_lo + a_lo b_hi, tf32 parts), fp32
+ * accumulation in TMEM over 128 entries and fp64 across; derivative MVMs use FP32. */
 
 /* krylov.hpp:15-24 CgConfig (+ GPU fields). */
 typedef struct {

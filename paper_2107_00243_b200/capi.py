@@ -16,7 +16,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "gpkrylov_cuda.h")
 
 GPK_OK, GPK_INPUT_ERROR, GPK_NUMERICAL_ERROR, GPK_SOLVER_ERROR, GPK_CUDA_ERROR, GPK_NCCL_ERROR = range(6)
 GPK_RBF, GPK_MATERN12, GPK_MATERN32, GPK_MATERN52, GPK_RATQUAD = range(5)
-GPK_PREC_FP64, GPK_PREC_FP32 = 0, 1
+GPK_PREC_FP64, GPK_PREC_FP32, GPK_PREC_TF32X3 = 0, 1, 2
 
 
 class gpk_cg_cfg(C.Structure):

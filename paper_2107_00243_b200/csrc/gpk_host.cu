@@ -230,7 +230,8 @@ struct gpk_ctx {
   // ---- workspaces
   DBuf<double> w_part, w_y, w_kx, w_g1, w_W, w_T, w_B, w_tmp, w_tmp2, w_ps, w_hist;
   DBuf<double> st_X[2], st_R[2], st_P[2], st_Z;
-  DBuf<float> w_v32, w_f32;
+  DBuf<float> w_v32, w_f32, w_vhi, w_vlo;
+  bool use_tc = false;  // GPK_PREC_TF32X3: value MVMs on the tcgen05 tensor cores
   DBuf<double> w_v64, w_f64;
   DBuf<gpk::SlotState> w_ss[2];
   DBuf<int> w_map;
@@ -385,6 +386,44 @@ struct gpk_ctx {
     const int splits = splits_for();
     const int ntiles = n_pad / 32;
     const int per = (ntiles + splits - 1) / splits;
+    if (!fp64 && use_tc && which < 0) {  // tcgen05 path (value mode)
+      for (int c0 = 0; c0 < t; c0 += 128) {
+        const int tc = std::min(128, t - c0);
+        const int npad = gpk::tc_npad(tc);
+        w_vhi.ensure(static_cast<size_t>(n_pad) * npad);
+        w_vlo.ensure(static_cast<size_t>(n_pad) * npad);
+        check_launch(gpk::launch_pack_v_tc(V + c0 * ldv, ldv, tc, n, n_pad, npad, w_vhi.p, w_vlo.p, st), 1,
+                     "pack_v_tc");
+        gpk::MvmArgs a{};
+        a.n = n;
+        a.n_pad = n_pad;
+        a.t = tc;
+        a.jtiles_per_split = per;
+        a.scale = o2;
+        const int cf[] = {2, 3, 6, 9};
+        const double fl = static_cast<double>(n) * n * (2.0 * tc + 3.0 * d + cf[family]);
+        auto ev = prof_begin(0);
+        if (splits == 1) {
+          a.ldo = ldo;
+          check_launch(gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, out + c0 * ldo, a, 1, st), 1,
+                       "fused_kmvm_tc");
+          prof_end(0, ev, fl, static_cast<double>(n) * n);
+        } else {
+          a.ldo = n_pad;
+          a.split_stride = static_cast<long long>(tc) * n_pad;
+          w_y.ensure(static_cast<size_t>(splits) * tc * n_pad);
+          check_launch(gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, w_y.p, a, splits, st), 1,
+                       "fused_kmvm_tc");
+          prof_end(0, ev, fl, static_cast<double>(n) * n);
+          check_launch(
+              gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, n, n_pad, out + c0 * ldo, ldo, st), 1,
+              "reduce_splits");
+        }
+        entries += static_cast<long long>(n) * n;
+        flops += static_cast<long long>(fl);
+      }
+      return;
+    }
     for (int c0 = 0; c0 < t; c0 += chunk) {
       const int tc = std::min(chunk, t - c0);
       const gpk::MvmShape sh = gpk::mvm_shape(tc, fp64, mode);
@@ -762,7 +801,10 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   require(c->pkind != 0, "evaluate_mll: no preconditioner (gpk_pivoted_cholesky or gpk_precond_identity)");
   const int n = c->n, d = c->d, np = d + 2;
   const long long ldn = c->ldn;
+  require(cfg->solver.precision >= GPK_PREC_FP64 && cfg->solver.precision <= GPK_PREC_TF32X3,
+          "CgConfig: unknown precision");
   const bool fp64 = cfg->solver.precision == GPK_PREC_FP64;
+  c->use_tc = cfg->solver.precision == GPK_PREC_TF32X3;
   const int mi = cfg->solver.max_iters;
   const double tol = cfg->solver.rel_tol;
   require(mi >= 1, "CgConfig: max_iters must be >= 1");
@@ -1220,6 +1262,8 @@ static void mvm_common(gpk_ctx* c, int which, const double* V, int64_t ldv, int 
   for (int q = 0; q < t; ++q)
     for (int i = 0; i < n; ++i)
       if (!std::isfinite(V[q * ldv + i])) fail(GPK_INPUT_ERROR, "KernelOperator: non-finite entries in input vector");
+  require(precision >= GPK_PREC_FP64 && precision <= GPK_PREC_TF32X3, "gpk_kernel_mvm: unknown precision");
+  c->use_tc = precision == GPK_PREC_TF32X3;
   DBuf<double> dv, dout;
   dv.ensure(static_cast<size_t>(t) * c->ldn);
   dout.ensure(static_cast<size_t>(t) * c->ldn);
@@ -1567,7 +1611,9 @@ gpk_status gpk_mbcg(gpk_ctx* ctx, const double* B, int64_t ldb, int t, const gpk
     dx.ensure(static_cast<size_t>(t) * c->ldn);
     CK(cudaMemcpy2DAsync(db.p, c->ldn * sizeof(double), B, ldb * sizeof(double), n * sizeof(double), t,
                          cudaMemcpyHostToDevice, c->st));
+    require(cfg->precision >= GPK_PREC_FP64 && cfg->precision <= GPK_PREC_TF32X3, "CgConfig: unknown precision");
     const bool fp64 = cfg->precision == GPK_PREC_FP64;
+    c->use_tc = cfg->precision == GPK_PREC_TF32X3;
     gpk_ctx::CgOut r;
     try {
       r = c->mbcg(db.p, c->ldn, t, mi, cfg->rel_tol, fp64, dx.p, c->ldn, alpha, beta, resid_hist);

@@ -47,6 +47,13 @@ cudaError_t launch_pack_v32(const double* V, long long ldv, const int* colmap, i
 cudaError_t launch_pack_v64(const double* V, long long ldv, const int* colmap, int t, int n, int n_pad,
                             MvmShape sh, double* V64, cudaStream_t st);
 
+// tcgen05 (tensor-core, 3xTF32) fused MVM: value mode, t <= 128 per launch.
+int tc_npad(int t);  // padded column count (multiple of 8) of the packed V tiles, -1 if t > 128
+cudaError_t launch_pack_v_tc(const double* V, long long ldv, int t, int n, int n_pad, int npad, float* vhi,
+                             float* vlo, cudaStream_t st);
+cudaError_t launch_fused_kmvm_tc(int family, int dp, const float* X, const float* vhi, const float* vlo, double* out,
+                                 const MvmArgs& a, int splits, cudaStream_t st);
+
 // Reference-formula kernel column (kernels.hpp:235-243) / derivative column (:252-267), fp64.
 // which < 0: K[:, p];  which == 0: outputscale;  1..d: lengthscale which-1.
 cudaError_t launch_kernel_column(int family, const double* sx, const double* x, const double* sq, int n, int d,

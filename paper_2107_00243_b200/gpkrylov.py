@@ -171,7 +171,7 @@ class _Ctx:
         _check(rc, self.h)
 
 
-PREC = {"fp64": capi.GPK_PREC_FP64, "fp32": capi.GPK_PREC_FP32}
+PREC = {"fp64": capi.GPK_PREC_FP64, "fp32": capi.GPK_PREC_FP32, "tf32x3": capi.GPK_PREC_TF32X3}
 
 
 class KernelOperator:
