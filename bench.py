@@ -131,7 +131,7 @@ def run_ours(args, rank_env):
     ctx = C.c_void_p()
     assert lib.gpk_create(local, C.byref(ctx)) == 0, "gpk_create failed"
     stream = torch.cuda.ExternalStream(lib.gpk_stream(ctx), device=dev)
-    prec = capi.GPK_PREC_FP64 if args.precision == "fp64" else capi.GPK_PREC_FP32
+    prec = {"fp64": capi.GPK_PREC_FP64, "fp32": capi.GPK_PREC_FP32, "tf32x3": capi.GPK_PREC_TF32X3}[args.precision]
     cfg = capi.gpk_mll_cfg(capi.gpk_cg_cfg(w.max_iters, w.rel_tol, 0, prec, args.refine), 1, 1,
                            0 if args.backward == "fused" else 1)
     grad = np.zeros(d + 2)
@@ -283,7 +283,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--rank", type=int, default=None)
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--precision", default="tf32x3", choices=["tf32x3", "fp32", "fp64"])
     ap.add_argument("--backward", default="fused", choices=["fused", "faithful"])
     ap.add_argument("--refine", type=int, default=2)
     ap.add_argument("--no-sweep", action="store_true")
@@ -343,17 +343,31 @@ def main():
     fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     achieved = (mvm["flops"] / mvm["launches"]) / (mvm["ms"] / mvm["launches"] / 1e3) / 1e12 if mvm["launches"] else 0
     clk = r["clocks"]
+    tc = args.precision == "tf32x3"
     roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak if fp32_peak else None, "traffic": None,
-                "kernel": "fused_kmvm_kernel (fused kernel MVM)",
-                "peak_source": f"FP32 CUDA-core peak = 148 SM x 128 FMA/clk x 2 x sm_max_mhz ({peaks_src} "
-                               f"MEASURED_PEAKS.json sm_max_mhz); tensor cores not used (SURVEY.md §7.3-1)",
+                "kernel": ("fused_kmvm_tc_kernel (tcgen05 3xTF32 contraction, entries on CUDA cores)" if tc
+                           else "fused_kmvm_kernel (SIMT fp32)"),
+                "peak_source": f"north-star roofline: FP32 CUDA-core peak = 148 SM x 128 FMA/clk x 2 x sm_max_mhz "
+                               f"({peaks_src} MEASURED_PEAKS.json sm_max_mhz); achieved = algorithmic flops "
+                               f"n^2 (2t + 3d + c_fam) per launch / CUDA-event launch time",
                 "flops_per_launch": mvm["flops"] / max(mvm["launches"], 1),
                 "avg_launch_ms": mvm["ms"] / max(mvm["launches"], 1), "launches_per_step":
                     mvm["launches"] / max(args.steps, 1),
                 "share_of_step": (mvm["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
     if clk.get("sm_mhz"):
         roofline["frac_at_inrun_clock"] = achieved / (148 * 128 * 2 * clk["sm_mhz"] * 1e6 / 1e12)
+    # the kernel's own bound: CUDA-core issue of the kernel-entry evaluation (the contraction runs
+    # on the tensor cores in tf32x3 mode): ~2*DP (difference + square-accumulate) + c_instr + split/store
+    dp = 4 if w.d <= 4 else 12 if w.d <= 12 else 20 if w.d <= 20 else 32
+    c_instr = {0: 2, 1: 4, 2: 5, 3: 7}[w.family] + (4 if tc else 0)
+    instr_per_entry = 2 * dp + 1 + c_instr + (0 if tc else 8 * ((w.probes + 1 + 7) // 8))
+    entry_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / instr_per_entry
+    if mvm["launches"]:
+        entries_per_s = w.n * w.n * mvm["launches"] / (mvm["ms"] / 1e3)
+        roofline["entries_per_s"] = entries_per_s
+        roofline["entry_issue_bound"] = {"instr_per_entry": instr_per_entry, "peak_entries_per_s": entry_peak,
+                                         "frac": entries_per_s / entry_peak}
     dcp = r["dc"]
     if dcp["launches"]:
         roofline["deriv_pass"] = {"achieved": (dcp["flops"] / dcp["ms"] * 1e3) / 1e12, "unit": "TFLOP/s",
@@ -361,8 +375,9 @@ def main():
                                   "share_of_step": (dcp["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 kernel entries / f64 CG state"
-            if args.precision == "fp32" else "f64",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": {"fp64": "f64", "fp32": "f32 entries+contraction / f64 CG state",
+                      "tf32x3": "f32 entries, 3xTF32 tensor-core contraction / f64 CG state"}[args.precision],
             "data": "synthetic (seeded stand-in for the BASELINE config; UCI data unavailable offline)",
             "config": config, "gpu_launches": r["launches"],
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},

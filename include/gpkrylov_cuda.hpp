@@ -61,7 +61,7 @@ struct CgConfig {  // krylov.hpp:15-24 (+ GPU fields)
   int max_iters = 100;
   double rel_tol = 1e-6;
   bool collect_tridiag = false;
-  gpk_precision precision = GPK_PREC_FP32;
+  gpk_precision precision = GPK_PREC_TF32X3;
   int refine = 2;
   gpk_cg_cfg c() const { return gpk_cg_cfg{max_iters, rel_tol, collect_tridiag ? 1 : 0, precision, refine}; }
 };

@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <random>
@@ -232,6 +233,11 @@ struct gpk_ctx {
   DBuf<double> st_X[2], st_R[2], st_P[2], st_Z;
   DBuf<float> w_v32, w_f32, w_vhi, w_vlo;
   bool use_tc = false;  // GPK_PREC_TF32X3: value MVMs on the tcgen05 tensor cores
+  int tc_flush = [] {   // j-tiles per TMEM accumulation group (env GPK_TC_FLUSH, default 2)
+    const char* e = std::getenv("GPK_TC_FLUSH");
+    const int v = e ? std::atoi(e) : 2;
+    return v >= 1 && v <= 8 ? v : 2;
+  }();
   DBuf<double> w_v64, w_f64;
   DBuf<gpk::SlotState> w_ss[2];
   DBuf<int> w_map;
@@ -400,6 +406,7 @@ struct gpk_ctx {
         a.t = tc;
         a.jtiles_per_split = per;
         a.scale = o2;
+        a.flush = tc_flush;
         const int cf[] = {2, 3, 6, 9};
         const double fl = static_cast<double>(n) * n * (2.0 * tc + 3.0 * d + cf[family]);
         auto ev = prof_begin(0);

@@ -17,6 +17,7 @@ struct MvmArgs {
   int jtiles_per_split;      // j-tiles (of 32) handled by one split
   double scale;              // output scale (o^2, 2o, -2 o^2 / l_j / c_fam, ...)
   long long split_stride;    // element offset between split-K partial outputs
+  int flush;                 // tcgen05 path: j-tiles per TMEM accumulation group (fp64 drain period)
 };
 
 // Packed-operand geometry for a given column count.

@@ -31,7 +31,7 @@ constexpr int BM = 128;
 constexpr int BK = 32;
 constexpr int S = 3;       // X/V stages
 constexpr int AS = 2;      // A-tile stages
-constexpr int F = 4;       // tiles per TMEM flush group
+// tiles per TMEM flush group: MvmArgs::flush (runtime; 1..8)
 constexpr int NPW = 16;    // producer warps
 constexpr int RPT = NPW / 4;              // producer threads per row
 constexpr int JPT = BK / RPT;             // entries per producer thread per tile (8)
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int jt0 = blockIdx.y * a.jtiles_per_split;
   const int jt1 = min(jt0 + a.jtiles_per_split, a.n_pad / BK);
   const int nt = jt1 - jt0;
+  const int F = a.flush > 0 ? a.flush : 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {

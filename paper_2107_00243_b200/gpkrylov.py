@@ -395,7 +395,7 @@ class CgConfig:
     max_iters: int = 100
     rel_tol: float = 1e-6
     collect_tridiag: bool = False
-    precision: str = "fp32"
+    precision: str = "tf32x3"
     refine: int = 2
 
     def c(self):

@@ -34,18 +34,20 @@ def test_mvm_fp64_matches_oracle(orc, fam, n, d, t):
 
 
 @pytest.mark.parametrize("fam", FAMS)
-@pytest.mark.parametrize("n,d,t", [(1000, 3, 9), (2051, 9, 51), (700, 18, 65)])
-def test_mvm_fp32_matches_oracle(orc, fam, n, d, t):
-    # fp32 entries (direct differences, SFU exp) with fp64 cross-tile accumulation
+@pytest.mark.parametrize("n,d,t", [(1000, 3, 9), (2051, 9, 51), (700, 18, 65), (300, 32, 130), (129, 1, 1)])
+@pytest.mark.parametrize("precision", ["fp32", "tf32x3"])
+def test_mvm_fp32_matches_oracle(orc, fam, n, d, t, precision):
+    # fp32 entries (direct differences, SFU exp); contraction on CUDA cores (fp32) or on the
+    # tcgen05 tensor cores in 3xTF32 split precision (tf32x3); fp64 across accumulation groups
     x = orc.random_matrix(n, d, 200 + n)
     p = orc.Params(d, 1.0, 0.8 * math.sqrt(d), 0.01)
     v = orc.random_matrix(n, t, 9)
     want = orc.kernel_apply(orc.FAMILIES[fam], x, p, v)
-    got = op_for(orc, fam, x, p).apply(v, precision="fp32")
-    assert rel(got, want) < 2e-6
+    got = op_for(orc, fam, x, p).apply(v, precision=precision)
+    assert rel(got, want) < (2e-6 if precision == "fp32" else 3e-6)
     # per column too
     for c in range(t):
-        assert rel(got[:, c], want[:, c]) < 5e-6
+        assert rel(got[:, c], want[:, c]) < (5e-6 if precision == "fp32" else 1e-5)
 
 
 @pytest.mark.parametrize("fam", FAMS)
@@ -68,7 +70,7 @@ def test_mvm_columns_are_independent_bitwise(orc):
     p = orc.Params(11, 1.0, 2.0, 0.01)
     v = orc.random_matrix(1500, 65, 6)
     op = op_for(orc, "matern32", x, p)
-    for prec in ("fp32", "fp64"):
+    for prec in ("fp32", "fp64", "tf32x3"):
         full = op.apply(v, precision=prec)
         for cols in ([0], [3, 17], list(range(40, 51))):
             part = op.apply(v[:, cols], precision=prec)

@@ -1,5 +1,5 @@
 """Per-phase wall-clock of one evaluation step through the C-ABI (every call is
-synchronous): python tools/phase_times.py [workload] [rank ...]"""
+synchronous): python tools/phase_times.py [workload] [rank ...]; env PRECS=fp32,tf32x3,fp64"""
 import ctypes as C
 import os
 import sys
@@ -12,6 +12,8 @@ from paper_2107_00243_b200 import capi, workloads  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "C2"
 ranks = [int(a) for a in sys.argv[2:]] or [0, 100, 500]
+precs = os.environ.get("PRECS", "fp32,fp64").split(",")
+PMAP = {"fp64": capi.GPK_PREC_FP64, "fp32": capi.GPK_PREC_FP32, "tf32x3": capi.GPK_PREC_TF32X3}
 lib = capi.lib()
 w = workloads.config(wl)
 x, y = workloads.generate(w)
@@ -25,7 +27,8 @@ lo, lls, ln = w.log_params
 lls = np.ascontiguousarray(lls)
 ctx = C.c_void_p()
 assert lib.gpk_create(0, C.byref(ctx)) == 0
-for prec in (capi.GPK_PREC_FP32, capi.GPK_PREC_FP64):
+for pname in precs:
+    prec = PMAP[pname]
     for rank in ranks:
         for rep in range(2):
             t = {}
@@ -49,10 +52,9 @@ for prec in (capi.GPK_PREC_FP32, capi.GPK_PREC_FP64):
             assert rc == 0, lib.gpk_last_error(ctx)
             t["evaluate"] = time.perf_counter() - t0
             if rep == 1:
-                print(f"{wl} rank={rank} {'fp32' if prec else 'fp64'}: " +
-                      " ".join(f"{k}={v*1e3:.1f}ms" for k, v in t.items()) +
+                print(f"{wl} rank={rank} {pname}: " + " ".join(f"{k}={v*1e3:.1f}ms" for k, v in t.items()) +
                       f" | solve={res.seconds_solve*1e3:.1f}ms bwd={res.seconds_backward*1e3:.1f}ms "
                       f"iters={res.total_cg_iterations} y_iters={res.solve_iterations} refine={res.refine_passes} "
-                      f"res={res.max_true_rel_residual:.1e} launches={res.gpu_launches} value={res.value:.6f} "
-                      f"grad0={g[0]:.6f} gradN={g[-1]:.6f}")
+                      f"res={res.max_true_rel_residual:.1e} launches={res.gpu_launches} value={res.value:.8f} "
+                      f"grad0={g[0]:.6f} grad1={g[1]:.6f} gradN={g[-1]:.6f}", flush=True)
 lib.gpk_destroy(ctx)
