@@ -72,6 +72,11 @@ GPK_DEV float to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+// round-to-nearest (ties away) to tf32 with integer ALU ops instead of the
+// quarter-rate conversion unit (finite inputs)
+GPK_DEV float to_tf32_alu(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 GPK_DEV void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
@@ -270,8 +275,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             s1 = fmaf(d3, d3, s1);
           }
           const float e = kval32<FAM>(s0 + s1);
-          eh[u] = to_tf32(e);
-          el[u] = to_tf32(e - eh[u]);
+          eh[u] = to_tf32_alu(e);
+          el[u] = e - eh[u];  // exact; the tensor core reads its leading tf32 bits
         }
         const uint32_t off = sw128_off(r, q * JPT + c4 * 4);
         st_shared_v4(ahi + off, eh[0], eh[1], eh[2], eh[3]);
