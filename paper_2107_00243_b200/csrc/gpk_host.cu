@@ -56,20 +56,26 @@ void require(bool c, const std::string& m) {
     if (e_ != cudaSuccess) fail(GPK_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// Device buffers come from the stream-ordered pool allocator on the context's
+// stream (pool release threshold = max): scratch allocated and freed inside a
+// call is recycled without any device synchronisation.
+thread_local cudaStream_t tl_stream = nullptr;
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t cap = 0;
+  cudaStream_t s = nullptr;
   void ensure(size_t cnt) {
     if (cnt == 0) cnt = 1;
     if (cnt <= cap) return;
-    if (p) cudaFree(p);
-    p = nullptr;
-    CK(cudaMalloc(&p, cnt * sizeof(T)));
+    release();
+    s = tl_stream;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), s));
     cap = cnt;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
     cap = 0;
   }
@@ -233,6 +239,11 @@ struct gpk_ctx {
   DBuf<double> st_X[2], st_R[2], st_P[2], st_Z;
   DBuf<float> w_v32, w_f32, w_vhi, w_vlo;
   bool use_tc = false;  // GPK_PREC_TF32X3: value MVMs on the tcgen05 tensor cores
+  int sync_every = [] {  // CG iterations between host round trips (env GPK_SYNC_EVERY, default 1:
+    const char* e = std::getenv("GPK_SYNC_EVERY");  // measured no gain from lazier syncs at C2)
+    const int v = e ? std::atoi(e) : 1;
+    return v >= 1 && v <= 64 ? v : 1;
+  }();
   int tc_flush = [] {   // j-tiles per TMEM accumulation group (env GPK_TC_FLUSH, default 2)
     const char* e = std::getenv("GPK_TC_FLUSH");
     const int v = e ? std::atoi(e) : 2;
@@ -671,8 +682,12 @@ struct gpk_ctx {
       check_launch(gpk::launch_dot_partials(0, Zs, Zs, 0.0, n, ldn, ta, pzz, st), 1, "dots");
       check_launch(gpk::launch_cg_beta(prz, pzz, nrb, ta, it, rel_tol, ss, dh_b, dh_r, max_iters, st), 1, "cg_beta");
       check_launch(gpk::launch_cg_update_p(Ps, Zs, n, ldn, ta, ss, st), 1, "cg_p");
-      d2h(hs.data(), ss, sizeof(gpk::SlotState) * ta);
-      handle_flags();
+      // Host round trip only every sync_every iterations: converged / failed columns freeze
+      // on the device (their flag) and are compacted out at the next sync.
+      if (it % sync_every == 0 || it == max_iters) {
+        d2h(hs.data(), ss, sizeof(gpk::SlotState) * ta);
+        handle_flags();
+      }
     }
     // columns that hit max_iters: not an error, converged = false (krylov.hpp:120)
     if (ta > 0) {
@@ -757,7 +772,10 @@ namespace {
 
 gpk_status guard(gpk_ctx* ctx, const std::function<void()>& f) {
   try {
-    if (ctx) ctx->set_device();
+    if (ctx) {
+      ctx->set_device();
+      tl_stream = ctx->st;
+    }
     f();
     if (ctx) ctx->err.clear();
     return GPK_OK;
@@ -1153,7 +1171,13 @@ gpk_status gpk_create(int device, gpk_ctx** out) {
   if (device < 0 || device >= ndev) return GPK_INPUT_ERROR;
   auto* c = new gpk_ctx();
   c->device = device;
-  const gpk_status s = guard(c, [&] { CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking)); });
+  const gpk_status s = guard(c, [&] {
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~0ull;  // never trim: freed scratch is reused without synchronisation
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  });
   if (s != GPK_OK) {
     delete c;
     return s;
@@ -1173,8 +1197,11 @@ void gpk_destroy(gpk_ctx* ctx) {
       cudaEventDestroy(e.second);
     }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
-  cudaStreamDestroy(ctx->st);
-  delete ctx;
+  cudaStream_t s = ctx->st;
+  tl_stream = s;
+  delete ctx;  // buffers return to the pool on their stream
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
 }
 
 const char* gpk_last_error(const gpk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }

@@ -97,6 +97,10 @@ __global__ void cg_alpha_kernel(const double* __restrict__ part_pap, int nrb, in
   const double pap = reduce_chunks(part_pap + static_cast<long long>(s) * nrb, nrb, red);
   if (threadIdx.x == 0) {
     SlotState& x = ss[s];
+    if (x.flag != 0) {  // converged / failed columns stay frozen until the host compacts them out
+      x.alpha = 0.0;
+      return;
+    }
     const double alpha = x.rz / pap;
     x.alpha = alpha;
     if (!isfinite(alpha) || alpha <= 0.0) {  // krylov.hpp:79-83
@@ -156,7 +160,7 @@ __global__ void cg_update_xr_kernel(double* __restrict__ X, double* __restrict__
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const SlotState& x = ss[s];
-  if (x.flag == kFlagError) return;
+  if (x.flag != 0) return;
   const double a = x.alpha;
   const long long o = s * ldn + i;
   const double p = P[o];
@@ -348,7 +352,18 @@ __global__ void g1_reduce_kernel(const double* __restrict__ part, int nch, int k
   if (idx >= static_cast<long long>(ka) * tb) return;
   const int s = static_cast<int>(idx / ka), kk = static_cast<int>(idx % ka);
   double acc = 0.0;
-  for (int c = 0; c < nch; ++c) acc += part[(static_cast<long long>(c) * tb + s) * ka + kk];
+  const double* p = part + static_cast<long long>(s) * ka + kk;
+  const long long stride = static_cast<long long>(tb) * ka;
+  // fixed chunk order; loads batched 8 deep (their addresses do not depend on the sum)
+  int c = 0;
+  for (; c + 8 <= nch; c += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = p[(c + q) * stride];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += v[q];
+  }
+  for (; c < nch; ++c) acc += p[c * stride];
   W[s * ldw + kk] = acc;
 }
 

@@ -72,6 +72,21 @@ GPK_DEV float to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+// paired fp32 (sm_100 FADD2 / FFMA2): two lanes of work per issue slot
+typedef unsigned long long f32x2;
+GPK_DEV f32x2 f2_sub(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+GPK_DEV f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+GPK_DEV float f2_hsum(f32x2 a) {
+  return __uint_as_float(static_cast<uint32_t>(a)) + __uint_as_float(static_cast<uint32_t>(a >> 32));
+}
 // round-to-nearest (ties away) to tf32 with integer ALU ops instead of the
 // quarter-rate conversion unit (finite inputs)
 GPK_DEV float to_tf32_alu(float x) {
@@ -218,14 +233,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = pw >> 2;             // quarter: j-range and column-chunk subset
     const int r = lg * 32 + lane;      // row within the tile == TMEM lane
     const int row = row0 + r;
-    float xr[DP];
+    f32x2 xr[DP / 2];  // this row's coordinates, packed in pairs
 #pragma unroll
     for (int k = 0; k < DP / 4; ++k) {
-      const float4 v = reinterpret_cast<const float4*>(X + static_cast<long long>(row) * DP)[k];
-      xr[4 * k] = v.x;
-      xr[4 * k + 1] = v.y;
-      xr[4 * k + 2] = v.z;
-      xr[4 * k + 3] = v.w;
+      const ulonglong2 v = reinterpret_cast<const ulonglong2*>(X + static_cast<long long>(row) * DP)[k];
+      xr[2 * k] = v.x;
+      xr[2 * k + 1] = v.y;
     }
     double acc64[HC * 8];
 #pragma unroll
@@ -262,19 +275,16 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = q * JPT + c4 * 4 + u;
-          const float4* xj = reinterpret_cast<const float4*>(xs + j * DP);
-          float s0 = 0.f, s1 = 0.f;
+          const ulonglong2* xj = reinterpret_cast<const ulonglong2*>(xs + j * DP);
+          f32x2 a0 = 0ull, a1 = 0ull;  // four partial sums of squared differences
 #pragma unroll
           for (int k = 0; k < DP / 4; ++k) {
-            const float4 v = xj[k];
-            const float d0 = xr[4 * k] - v.x, d1 = xr[4 * k + 1] - v.y, d2 = xr[4 * k + 2] - v.z,
-                        d3 = xr[4 * k + 3] - v.w;
-            s0 = fmaf(d0, d0, s0);
-            s1 = fmaf(d1, d1, s1);
-            s0 = fmaf(d2, d2, s0);
-            s1 = fmaf(d3, d3, s1);
+            const ulonglong2 v = xj[k];
+            const f32x2 d0 = f2_sub(xr[2 * k], v.x), d1 = f2_sub(xr[2 * k + 1], v.y);
+            a0 = f2_fma(d0, d0, a0);
+            a1 = f2_fma(d1, d1, a1);
           }
-          const float e = kval32<FAM>(s0 + s1);
+          const float e = kval32<FAM>(f2_hsum(a0) + f2_hsum(a1));
           eh[u] = to_tf32_alu(e);
           el[u] = e - eh[u];  // exact; the tensor core reads its leading tf32 bits
         }

@@ -11,7 +11,7 @@ from paper_2107_00243_b200 import capi, workloads  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "C2"
 rank = int(sys.argv[2]) if len(sys.argv) > 2 else 100
-prec = capi.GPK_PREC_FP64 if (len(sys.argv) > 3 and sys.argv[3] == "fp64") else capi.GPK_PREC_FP32
+prec = {"fp64": capi.GPK_PREC_FP64, "fp32": capi.GPK_PREC_FP32, "tf32x3": capi.GPK_PREC_TF32X3}[sys.argv[3] if len(sys.argv) > 3 else "tf32x3"]
 cuda = C.CDLL("libcuda.so.1")
 lib = capi.lib()
 w = workloads.config(wl)
