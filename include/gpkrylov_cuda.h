@@ -93,6 +93,24 @@ const char* gpk_last_error(const gpk_ctx* ctx);
 /* Version / build string (sm_100a). */
 const char* gpk_version(void);
 
+/* ---- row sharding across GPUs (one process or host thread per rank) ------
+ * A sharded context owns rows [r0, r1) of every n-length CG / probe array (X and
+ * the preconditioner factors are replicated); each CG iteration all-gathers the
+ * direction block and sums per-column dot products over ranks in rank order, so
+ * results are bitwise reproducible for a given world size.  Host entry points
+ * take full n-row buffers; each rank reads and writes back its own rows. */
+#define GPK_NCCL_ID_BYTES 128
+gpk_status gpk_nccl_unique_id(void* out /* GPK_NCCL_ID_BYTES */);
+/* NCCL communicator over `world` ranks, one GPU each (rank 0 creates the id, broadcasts it). */
+gpk_status gpk_create_sharded(int device, int rank, int world, const void* nccl_id, gpk_ctx** out);
+/* In-process rank group: host-staged collectives, one host thread per rank (any devices). */
+typedef struct gpk_group gpk_group;
+gpk_status gpk_group_create(int world, gpk_group** out);
+void gpk_group_destroy(gpk_group* g);
+gpk_status gpk_create_in_group(int device, gpk_group* g, int rank, gpk_ctx** out);
+/* This rank's rows after gpk_set_data. */
+gpk_status gpk_shard_rows(const gpk_ctx* ctx, int64_t* r0, int64_t* r1);
+
 /* KernelOperator ctor data (kernels.hpp:159-173): X is n x d, column-major, ld >= n. */
 gpk_status gpk_set_data(gpk_ctx* ctx, const double* X, int64_t n, int64_t d, int64_t ldx);
 gpk_status gpk_set_data_device(gpk_ctx* ctx, const double* dX, int64_t n, int64_t d, int64_t ldx);

@@ -77,6 +77,12 @@ SIGNATURES = {
     "gpk_profile_enable": (C.c_int, [_V, C.c_int]),
     "gpk_profile_read": (C.c_int, [_V, C.c_int, _D, C.POINTER(C.c_longlong), _D, _D]),
     "gpk_profile_reset": (C.c_int, [_V]),
+    "gpk_nccl_unique_id": (C.c_int, [_V]),
+    "gpk_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, _V, C.POINTER(_V)]),
+    "gpk_group_create": (C.c_int, [C.c_int, C.POINTER(_V)]),
+    "gpk_group_destroy": (None, [_V]),
+    "gpk_create_in_group": (C.c_int, [C.c_int, _V, C.c_int, C.POINTER(_V)]),
+    "gpk_shard_rows": (C.c_int, [_V, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }
 
 

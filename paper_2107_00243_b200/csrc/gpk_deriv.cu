@@ -75,7 +75,7 @@ GPK_DEV void shape_pair(T s, T& e, T& ds) {
 template <typename T, int FAM, int DP>
 __global__ void __launch_bounds__(kDThreads, 1)
     deriv_contract_kernel(const T* __restrict__ X, const T* __restrict__ U, const T* __restrict__ S,
-                          const T* __restrict__ Z, int n_pad, int l, double* __restrict__ partials) {
+                          const T* __restrict__ Z, int n_pad, int l, int a_begin, double* __restrict__ partials) {
   constexpr int NA = 2 * (DP + 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Ss = reinterpret_cast<T*>(smem_raw);  // [l][kDA]
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
   const int tid = threadIdx.x;
   const int ta = tid & 15;  // a-group (4 rows)
   const int tb = tid >> 4;  // b-group (4 cols)
-  const int a0 = blockIdx.x * kDA;
+  const int a0 = a_begin + blockIdx.x * kDA;  // this rank's a-rows (tiles never straddle shards)
   const int nbt = n_pad / kDB;
   const int bt0 = blockIdx.y * kDBTilesPerBlock;
   const int bt1 = min(bt0 + kDBTilesPerBlock, nbt);
@@ -184,57 +184,57 @@ __global__ void __launch_bounds__(kDThreads, 1)
 
 template <typename T, int FAM, int DP>
 static cudaError_t launch_dc_t(const void* X, const void* U, const void* S, const void* Z, int n_pad, int l,
-                               double* partials, int* nblocks, cudaStream_t st) {
+                               int a_begin, int a_rows, double* partials, int* nblocks, cudaStream_t st) {
   const size_t sm = sizeof(T) * (static_cast<size_t>(l) * (kDA + kDB) + (kDA + kDB) * DP + kDA + kDB);
   auto k = deriv_contract_kernel<T, FAM, DP>;
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
     if (e != cudaSuccess) return e;
   }
-  const int nat = n_pad / kDA;
+  const int nat = (a_rows + kDA - 1) / kDA;
   const int nbt = n_pad / kDB;
   dim3 g(nat, (nbt + kDBTilesPerBlock - 1) / kDBTilesPerBlock);
   *nblocks = static_cast<int>(g.x * g.y);
   if (partials == nullptr) return cudaSuccess;  // size query
   k<<<g, kDThreads, sm, st>>>(static_cast<const T*>(X), static_cast<const T*>(U), static_cast<const T*>(S),
-                              static_cast<const T*>(Z), n_pad, l, partials);
+                              static_cast<const T*>(Z), n_pad, l, a_begin, partials);
   return cudaGetLastError();
 }
 
 template <typename T, int FAM>
 static cudaError_t launch_dc_dp(int dp, const void* X, const void* U, const void* S, const void* Z, int n_pad, int l,
-                                double* partials, int* nblocks, cudaStream_t st) {
+                                int a_begin, int a_rows, double* partials, int* nblocks, cudaStream_t st) {
   switch (dp) {
-    case 4: return launch_dc_t<T, FAM, 4>(X, U, S, Z, n_pad, l, partials, nblocks, st);
-    case 12: return launch_dc_t<T, FAM, 12>(X, U, S, Z, n_pad, l, partials, nblocks, st);
-    case 20: return launch_dc_t<T, FAM, 20>(X, U, S, Z, n_pad, l, partials, nblocks, st);
-    case 32: return launch_dc_t<T, FAM, 32>(X, U, S, Z, n_pad, l, partials, nblocks, st);
+    case 4: return launch_dc_t<T, FAM, 4>(X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+    case 12: return launch_dc_t<T, FAM, 12>(X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+    case 20: return launch_dc_t<T, FAM, 20>(X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+    case 32: return launch_dc_t<T, FAM, 32>(X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
   }
   return cudaErrorInvalidValue;
 }
 
 template <typename T>
 static cudaError_t launch_dc_fam(int fam, int dp, const void* X, const void* U, const void* S, const void* Z,
-                                 int n_pad, int l, double* partials, int* nblocks, cudaStream_t st) {
+                                 int n_pad, int l, int a_begin, int a_rows, double* partials, int* nblocks,
+                                 cudaStream_t st) {
   switch (fam) {
-    case kRBF: return launch_dc_dp<T, kRBF>(dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
-    case kMatern12: return launch_dc_dp<T, kMatern12>(dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
-    case kMatern32: return launch_dc_dp<T, kMatern32>(dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
-    case kMatern52: return launch_dc_dp<T, kMatern52>(dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
+    case kRBF: return launch_dc_dp<T, kRBF>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+    case kMatern12: return launch_dc_dp<T, kMatern12>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+    case kMatern32: return launch_dc_dp<T, kMatern32>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+    case kMatern52: return launch_dc_dp<T, kMatern52>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
   }
   return cudaErrorInvalidValue;
 }
 
 // U/S/Z layout: U [n_pad], S and Z column-major [l][n_pad]; X [n_pad][dp].
 cudaError_t launch_deriv_contract(bool fp64, int family, int dp, const void* X, const void* U, const void* SZ,
-                                  int n, int n_pad, int l, int d, double* partials, int* nblocks, cudaStream_t st) {
-  (void)n;
-  (void)d;
+                                  int a_begin, int a_rows, int n_pad, int l, double* partials, int* nblocks,
+                                  cudaStream_t st) {
   const size_t elem = fp64 ? 8 : 4;
   const void* S = SZ;
   const void* Z = static_cast<const unsigned char*>(SZ) + elem * static_cast<size_t>(l) * n_pad;
-  return fp64 ? launch_dc_fam<double>(family, dp, X, U, S, Z, n_pad, l, partials, nblocks, st)
-              : launch_dc_fam<float>(family, dp, X, U, S, Z, n_pad, l, partials, nblocks, st);
+  return fp64 ? launch_dc_fam<double>(family, dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st)
+              : launch_dc_fam<float>(family, dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
 }
 
 }  // namespace gpk

@@ -12,8 +12,12 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -204,6 +208,98 @@ __global__ void residual_kernel(const double* __restrict__ B, long long ldb, con
   R[o] = B[s * ldb + i] - (KX[o] + sig2 * X[o]);
 }
 
+// rank-order sum of world partial vectors: out[i] = sum_r parts[r * count + i]
+__global__ void rank_sum_kernel(const double* __restrict__ parts, int world, long long count,
+                                double* __restrict__ out) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int r = 0; r < world; ++r) s += parts[r * count + i];
+  out[i] = s;
+}
+// full[c][r0_r + i] = gathered[r][c][i] for i < rows_r (the all-gathered row shards, padded to nmax)
+__global__ void unshard_cols_kernel(const double* __restrict__ g, int world, int t, long long nmax,
+                                    const int* __restrict__ r0s, const int* __restrict__ rows, double* __restrict__ full,
+                                    long long ldf) {
+  const int c = blockIdx.y;
+  const int r = blockIdx.z;
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= rows[r]) return;
+  full[c * ldf + r0s[r] + i] = g[(static_cast<long long>(r) * t + c) * nmax + i];
+}
+
+// ---------------------------------------------------------------------------
+// Communicators for row sharding (one rank per GPU).  Collectives used by the
+// mBCG path: all-gather of equal-size device buffers; sums are built from it
+// in rank order, so every rank and every run gets bitwise the same result.
+// ---------------------------------------------------------------------------
+struct Comm {
+  int rank = 0, world = 1;
+  virtual ~Comm() = default;
+  virtual void allgather(const void* send, void* recv, size_t bytes, cudaStream_t st) = 0;
+};
+
+struct NcclComm : Comm {
+  ncclComm_t c = nullptr;
+  ~NcclComm() override {
+    if (c) ncclCommDestroy(c);
+  }
+  void allgather(const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    const ncclResult_t r = ncclAllGather(send, recv, bytes, ncclChar, c, st);
+    if (r != ncclSuccess) fail(GPK_NCCL_ERROR, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+  }
+};
+
+}  // namespace
+
+// In-process rank group (one host thread per rank, any devices): host-staged
+// collectives with a generation barrier.  Used to run and test the sharded path
+// on a single GPU; kernels never wait on each other, only host threads do.
+struct gpk_group {
+  int world = 1;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  std::vector<std::vector<char>> host;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long long gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+namespace {
+struct GroupComm : Comm {
+  gpk_group* g = nullptr;
+  void allgather(const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    std::vector<char>& mine = g->host[rank];
+    mine.resize(bytes);
+    CK(cudaMemcpyAsync(mine.data(), send, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    g->barrier();
+    for (int r = 0; r < world; ++r)
+      CK(cudaMemcpyAsync(static_cast<char*>(recv) + r * bytes, g->host[r].data(), bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    g->barrier();
+  }
+};
+
+// contiguous row shards in units of 128 rows (fused-MVM row blocks never straddle ranks)
+void shard_of(int n, int rank, int world, int* r0, int* r1) {
+  const int nb = (n + 127) / 128;
+  const int base = nb / world, extra = nb % world;
+  const int b0 = rank * base + std::min(rank, extra);
+  const int b1 = b0 + base + (rank < extra ? 1 : 0);
+  *r0 = std::min(n, b0 * 128);
+  *r1 = std::min(n, b1 * 128);
+}
 }  // namespace
 
 // ===========================================================================
@@ -215,7 +311,76 @@ struct gpk_ctx {
 
   // ---- data (kernels.hpp:159-173)
   int n = 0, d = 0, n_pad = 0, dp = 0;
-  long long ldn = 0;
+  long long ldn = 0;  // leading dimension of the (local) n-length CG state
+
+  // ---- row sharding: this rank owns rows [r0, r1) (nl = r1 - r0) of every
+  // n-length CG / probe array; X, L, C, dL are replicated.  world == 1: r0 = 0, nl = n.
+  std::unique_ptr<Comm> comm;
+  int rank = 0, world = 1, r0 = 0, r1 = 0, nl = 0;
+  std::vector<int> all_r0, all_rows;
+  DBuf<int> d_r0, d_rows;
+  DBuf<double> w_send, w_recv, w_full, w_red;
+
+  void set_shard() {
+    all_r0.assign(world, 0);
+    all_rows.assign(world, 0);
+    for (int r = 0; r < world; ++r) {
+      int a, b;
+      shard_of(n, r, world, &a, &b);
+      all_r0[r] = a;
+      all_rows[r] = b - a;
+    }
+    r0 = all_r0[rank];
+    nl = all_rows[rank];
+    r1 = r0 + nl;
+    require(nl > 0, "gpkrylov_cuda: n too small for the number of ranks (each rank needs >= 1 row)");
+    ldn = (nl + 31) / 32 * 32;
+    if (world > 1) {
+      d_r0.ensure(world);
+      d_rows.ensure(world);
+      h2d(d_r0.p, all_r0.data(), sizeof(int) * world);
+      h2d(d_rows.p, all_rows.data(), sizeof(int) * world);
+    }
+  }
+  // full[c][*] (ld ldf, all n rows) <- every rank's local rows loc[c][*] (ld ldl)
+  void allgather_cols(const double* loc, long long ldl, int t, double* full, long long ldf) {
+    const long long nmax = *std::max_element(all_rows.begin(), all_rows.end());
+    w_send.ensure(static_cast<size_t>(t) * nmax);
+    w_recv.ensure(static_cast<size_t>(world) * t * nmax);
+    check_launch(gpk::launch_gather_cols(loc, ldl, nullptr, 1.0, nl, t, w_send.p, nmax, st), 1, "gather");
+    comm->allgather(w_send.p, w_recv.p, sizeof(double) * static_cast<size_t>(t) * nmax, st);
+    dim3 g(static_cast<unsigned>((nmax + 255) / 256), t, world);
+    unshard_cols_kernel<<<g, 256, 0, st>>>(w_recv.p, world, t, nmax, d_r0.p, d_rows.p, full, ldf);
+    check_launch(cudaGetLastError(), 1, "unshard");
+  }
+  // in-place rank-ordered sum over ranks of a device vector
+  void allreduce_sum(double* buf, long long count) {
+    if (world == 1 || count <= 0) return;
+    w_red.ensure(static_cast<size_t>(world) * count);
+    comm->allgather(buf, w_red.p, sizeof(double) * static_cast<size_t>(count), st);
+    rank_sum_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, st>>>(w_red.p, world, count, buf);
+    check_launch(cudaGetLastError(), 1, "rank_sum");
+  }
+  std::vector<double> allreduce_host(std::vector<double> v) {
+    if (world == 1 || v.empty()) return v;
+    DBuf<double> b;
+    b.ensure(v.size());
+    h2d(b.p, v.data(), sizeof(double) * v.size());
+    allreduce_sum(b.p, static_cast<long long>(v.size()));
+    d2h(v.data(), b.p, sizeof(double) * v.size());
+    return v;
+  }
+  // the full (all-row) view of a local column block: the block itself on one rank
+  const double* full_cols(const double* loc, long long ldl, int t, long long* ldf) {
+    if (world == 1) {
+      *ldf = ldl;
+      return loc;
+    }
+    w_full.ensure(static_cast<size_t>(t) * n);
+    allgather_cols(loc, ldl, t, w_full.p, n);
+    *ldf = n;
+    return w_full.p;
+  }
   bool have_data = false, have_params = false;
   DBuf<double> X, sx, sq, ls_dev, X64s;
   DBuf<float> X32;
@@ -392,17 +557,22 @@ struct gpk_ctx {
 
   // out[:, c] = op(V[:, c]) for c < t.  which < 0: K (noise-free, scaled o^2);
   // which == 0: dK/do; 1..d: dK/dl_j; d+1: identity (noise derivative).
-  void apply_kernel(const double* V, long long ldv, int t, double* out, long long ldo, bool fp64, int which) {
+  // V, out: this rank's rows (nl) of t columns; the direction block is all-gathered
+  // first when sharded (every rank contracts its rows against all n columns).
+  void apply_kernel(const double* Vloc, long long ldvloc, int t, double* out, long long ldo, bool fp64, int which) {
     if (t <= 0) return;
     if (which == d + 1) {
-      check_launch(gpk::launch_gather_cols(V, ldv, nullptr, 1.0, n, t, out, ldo, st), 1, "copy");
+      check_launch(gpk::launch_gather_cols(Vloc, ldvloc, nullptr, 1.0, nl, t, out, ldo, st), 1, "copy");
       return;
     }
+    long long ldv = 0;
+    const double* V = full_cols(Vloc, ldvloc, t, &ldv);
     const int mode = which >= 1 ? gpk::kModeDls : gpk::kModeValue;
     const int chunk = fp64 ? 64 : 128;
     const int splits = splits_for();
     const int ntiles = n_pad / 32;
     const int per = (ntiles + splits - 1) / splits;
+    const long long ldp = (nl + 127) / 128 * 128;  // split-K partial leading dimension (local rows)
     if (!fp64 && use_tc && which < 0) {  // tcgen05 path (value mode)
       for (int c0 = 0; c0 < t; c0 += 128) {
         const int tc = std::min(128, t - c0);
@@ -418,26 +588,28 @@ struct gpk_ctx {
         a.jtiles_per_split = per;
         a.scale = o2;
         a.flush = tc_flush;
+        a.row_begin = r0;
+        a.row_end = r1;
         const int cf[] = {2, 3, 6, 9};
-        const double fl = static_cast<double>(n) * n * (2.0 * tc + 3.0 * d + cf[family]);
+        const double fl = static_cast<double>(nl) * n * (2.0 * tc + 3.0 * d + cf[family]);
         auto ev = prof_begin(0);
         if (splits == 1) {
           a.ldo = ldo;
           check_launch(gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, out + c0 * ldo, a, 1, st), 1,
                        "fused_kmvm_tc");
-          prof_end(0, ev, fl, static_cast<double>(n) * n);
+          prof_end(0, ev, fl, static_cast<double>(nl) * n);
         } else {
-          a.ldo = n_pad;
-          a.split_stride = static_cast<long long>(tc) * n_pad;
-          w_y.ensure(static_cast<size_t>(splits) * tc * n_pad);
+          a.ldo = ldp;
+          a.split_stride = static_cast<long long>(tc) * ldp;
+          w_y.ensure(static_cast<size_t>(splits) * tc * ldp);
           check_launch(gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, w_y.p, a, splits, st), 1,
                        "fused_kmvm_tc");
-          prof_end(0, ev, fl, static_cast<double>(n) * n);
+          prof_end(0, ev, fl, static_cast<double>(nl) * n);
           check_launch(
-              gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, n, n_pad, out + c0 * ldo, ldo, st), 1,
+              gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, nl, ldp, out + c0 * ldo, ldo, st), 1,
               "reduce_splits");
         }
-        entries += static_cast<long long>(n) * n;
+        entries += static_cast<long long>(nl) * n;
         flops += static_cast<long long>(fl);
       }
       return;
@@ -466,59 +638,76 @@ struct gpk_ctx {
       else if (which == 0) a.scale = 2.0 * o;
       else a.scale = (-2.0 * o2 / ls[which - 1]) / c;
       const void* xp = fp64 ? static_cast<const void*>(X64s.p) : static_cast<const void*>(X32.p);
+      a.row_begin = r0;
+      a.row_end = r1;
       const int cf[] = {2, 3, 6, 9};
-      const double fl = static_cast<double>(n) * n * (2.0 * tc + 3.0 * d + cf[family]);
+      const double fl = static_cast<double>(nl) * n * (2.0 * tc + 3.0 * d + cf[family]);
       auto ev = prof_begin(0);
       if (splits == 1) {
         a.ldo = ldo;
         a.split_stride = 0;
         check_launch(gpk::launch_fused_kmvm(fp64, family, dp, mode, xp, vp, out + c0 * ldo, a, 1, st), 1,
                      "fused_kmvm");
-        prof_end(0, ev, fl, static_cast<double>(n) * n);
+        prof_end(0, ev, fl, static_cast<double>(nl) * n);
       } else {
-        a.ldo = n_pad;
-        a.split_stride = static_cast<long long>(tc) * n_pad;
-        w_y.ensure(static_cast<size_t>(splits) * tc * n_pad);
+        a.ldo = ldp;
+        a.split_stride = static_cast<long long>(tc) * ldp;
+        w_y.ensure(static_cast<size_t>(splits) * tc * ldp);
         check_launch(gpk::launch_fused_kmvm(fp64, family, dp, mode, xp, vp, w_y.p, a, splits, st), 1, "fused_kmvm");
-        prof_end(0, ev, fl, static_cast<double>(n) * n);
-        check_launch(gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, n, n_pad, out + c0 * ldo, ldo, st),
+        prof_end(0, ev, fl, static_cast<double>(nl) * n);
+        check_launch(gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, nl, ldp, out + c0 * ldo, ldo, st),
                      1, "reduce_splits");
       }
-      entries += static_cast<long long>(n) * n;
+      entries += static_cast<long long>(nl) * n;
       flops += static_cast<long long>(fl);
     }
   }
 
   // Z = P^{-1} R  (identity / Woodbury, preconditioners.hpp:114-118); column-major [t][ldn]
+  // Woodbury on this rank's rows: W = sum_ranks L[rows]^T R[rows] (k x t), Z = (R - C[rows] W) / s2
   void psolve(const double* R, int t, double* Z) {
     if (t <= 0) return;
     if (pkind == 1) {
-      check_launch(gpk::launch_gather_cols(R, ldn, nullptr, 1.0, n, t, Z, ldn, st), 1, "copy");
+      check_launch(gpk::launch_gather_cols(R, ldn, nullptr, 1.0, nl, t, Z, ldn, st), 1, "copy");
       return;
     }
     if (k == 0) {
-      check_launch(gpk::launch_woodbury_finish(R, nullptr, pnoise, n, ldn, t, Z, st), 1, "woodbury");
+      check_launch(gpk::launch_woodbury_finish(R, nullptr, pnoise, nl, ldn, t, Z, st), 1, "woodbury");
       return;
     }
-    w_g1.ensure(gpk::g1_workspace(n, k, t));
+    w_g1.ensure(gpk::g1_workspace(nl, k, t));
     w_W.ensure(static_cast<size_t>(k) * t);
     w_T.ensure(static_cast<size_t>(t) * ldn);
-    check_launch(gpk::launch_g1(L.p, n, k, R, ldn, t, n, w_g1.p, w_W.p, k, st), 2, "g1");
-    check_launch(gpk::launch_g2(C.p, n, k, w_W.p, k, t, n, w_T.p, ldn, st), 1, "g2");
-    check_launch(gpk::launch_woodbury_finish(R, w_T.p, pnoise, n, ldn, t, Z, st), 1, "woodbury");
+    check_launch(gpk::launch_g1(L.p + r0, n, k, R, ldn, t, nl, w_g1.p, w_W.p, k, st), 2, "g1");
+    allreduce_sum(w_W.p, static_cast<long long>(k) * t);
+    check_launch(gpk::launch_g2(C.p + r0, n, k, w_W.p, k, t, nl, w_T.p, ldn, st), 1, "g2");
+    check_launch(gpk::launch_woodbury_finish(R, w_T.p, pnoise, nl, ldn, t, Z, st), 1, "woodbury");
   }
 
-  // per-column dots a.b  (host result, fixed-order reduction)
+  // per-column dots a.b over all rows (host result, fixed-order reduction, rank-ordered sum)
   std::vector<double> col_dots(const double* A, const double* B, int t, long long ld) {
     std::vector<double> out(t);
     if (t <= 0) return out;
-    const int nrb = gpk::num_chunks(n);
+    const int nrb = gpk::num_chunks(nl);
     w_part.ensure(static_cast<size_t>(t) * nrb * 3 + t);
-    check_launch(gpk::launch_dot_partials(0, A, B, 0.0, n, ld, t, w_part.p, st), 1, "dots");
+    check_launch(gpk::launch_dot_partials(0, A, B, 0.0, nl, ld, t, w_part.p, st), 1, "dots");
     double* res = w_part.p + static_cast<size_t>(t) * nrb * 3;
     check_launch(gpk::launch_reduce_partials(w_part.p, nrb, t, res, st), 1, "reduce");
+    allreduce_sum(res, t);
     d2h(out.data(), res, sizeof(double) * t);
     return out;
+  }
+  // per-slot dot partials -> (partials, nrb) consumed by the cg_* kernels: the local chunk
+  // partials on one rank, else the rank-ordered global totals (nrb = 1)
+  const double* global_partials(double* part, int nrb, int t, double* tot, int* nrb_out) {
+    if (world == 1) {
+      *nrb_out = nrb;
+      return part;
+    }
+    check_launch(gpk::launch_reduce_partials(part, nrb, t, tot, st), 1, "reduce");
+    allreduce_sum(tot, t);
+    *nrb_out = 1;
+    return tot;
   }
 
   // -------------------------------------------------------------------------
@@ -542,7 +731,7 @@ struct gpk_ctx {
     out.bad.assign(t, 0.0);
     out.norm0.assign(t, 0.0);
     if (t <= 0) return out;
-    const int nrb = gpk::num_chunks(n);
+    const int nrb = gpk::num_chunks(nl);
     for (int b = 0; b < 2; ++b) {
       st_X[b].ensure(static_cast<size_t>(t) * ldn);
       st_R[b].ensure(static_cast<size_t>(t) * ldn);
@@ -551,7 +740,7 @@ struct gpk_ctx {
     }
     st_Z.ensure(static_cast<size_t>(t) * ldn);
     w_kx.ensure(static_cast<size_t>(t) * ldn);
-    w_part.ensure(static_cast<size_t>(t) * nrb * 3 + t);
+    w_part.ensure(static_cast<size_t>(t) * nrb * 3 + 3 * static_cast<size_t>(t));
     w_map.ensure(t);
     const bool hist = alpha_h || beta_h || resid_h;
     if (hist) w_hist.ensure(static_cast<size_t>(3) * t * max_iters);
@@ -573,16 +762,20 @@ struct gpk_ctx {
     }
     h2d(ss, hs.data(), sizeof(gpk::SlotState) * t);
     // x0 = 0, r = b, z = P^{-1} r, norm0 = ||z||, p = z, rz = r.z   (krylov.hpp:55-67)
-    check_launch(gpk::launch_gather_cols(nullptr, 0, nullptr, 0.0, n, t, Xs, ldn, st), 1, "zero");
-    check_launch(gpk::launch_gather_cols(B, ldb, nullptr, 1.0, n, t, Rs, ldn, st), 1, "gather");
+    check_launch(gpk::launch_gather_cols(nullptr, 0, nullptr, 0.0, nl, t, Xs, ldn, st), 1, "zero");
+    check_launch(gpk::launch_gather_cols(B, ldb, nullptr, 1.0, nl, t, Rs, ldn, st), 1, "gather");
     psolve(Rs, t, Zs);
     double* prz = w_part.p;
     double* pzz = w_part.p + static_cast<size_t>(t) * nrb;
     double* ppap = w_part.p + static_cast<size_t>(2) * t * nrb;
-    check_launch(gpk::launch_dot_partials(0, Rs, Zs, 0.0, n, ldn, t, prz, st), 1, "dots");
-    check_launch(gpk::launch_dot_partials(0, Zs, Zs, 0.0, n, ldn, t, pzz, st), 1, "dots");
-    check_launch(gpk::launch_cg_init(prz, pzz, nrb, t, ss, st), 1, "cg_init");
-    check_launch(gpk::launch_gather_cols(Zs, ldn, nullptr, 1.0, n, t, Ps, ldn, st), 1, "copy");
+    check_launch(gpk::launch_dot_partials(0, Rs, Zs, 0.0, nl, ldn, t, prz, st), 1, "dots");
+    check_launch(gpk::launch_dot_partials(0, Zs, Zs, 0.0, nl, ldn, t, pzz, st), 1, "dots");
+    double* tot = w_part.p + static_cast<size_t>(3) * t * nrb;  // global totals (sharded)
+    int nrg = nrb;
+    const double* grz = global_partials(prz, nrb, t, tot, &nrg);
+    const double* gzz = global_partials(pzz, nrb, t, tot + t, &nrg);
+    check_launch(gpk::launch_cg_init(grz, gzz, nrg, t, ss, st), 1, "cg_init");
+    check_launch(gpk::launch_gather_cols(Zs, ldn, nullptr, 1.0, nl, t, Ps, ldn, st), 1, "copy");
     d2h(hs.data(), ss, sizeof(gpk::SlotState) * t);
     for (int s = 0; s < t; ++s) out.norm0[s] = hs[s].norm0;
     int ta = t;
@@ -603,10 +796,10 @@ struct gpk_ctx {
       }
       // gather finished slots into w_kx then scatter by column
       h2d(w_map.p, slots.data(), sizeof(int) * slots.size());
-      check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, n, static_cast<int>(slots.size()), w_kx.p, ldn, st),
+      check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, nl, static_cast<int>(slots.size()), w_kx.p, ldn, st),
                    1, "gather");
       h2d(w_map.p, cols.data(), sizeof(int) * cols.size());
-      check_launch(gpk::launch_scatter_cols(w_kx.p, ldn, w_map.p, n, static_cast<int>(cols.size()), Xout, ldx, st), 1,
+      check_launch(gpk::launch_scatter_cols(w_kx.p, ldn, w_map.p, nl, static_cast<int>(cols.size()), Xout, ldx, st), 1,
                    "scatter");
       sync();
     };
@@ -615,9 +808,9 @@ struct gpk_ctx {
       const int nb = cur ^ 1;
       if (nt > 0) {
         h2d(w_map.p, keep.data(), sizeof(int) * nt);
-        check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, n, nt, st_X[nb].p, ldn, st), 1, "compact");
-        check_launch(gpk::launch_gather_cols(Rs, ldn, w_map.p, 1.0, n, nt, st_R[nb].p, ldn, st), 1, "compact");
-        check_launch(gpk::launch_gather_cols(Ps, ldn, w_map.p, 1.0, n, nt, st_P[nb].p, ldn, st), 1, "compact");
+        check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, nl, nt, st_X[nb].p, ldn, st), 1, "compact");
+        check_launch(gpk::launch_gather_cols(Rs, ldn, w_map.p, 1.0, nl, nt, st_R[nb].p, ldn, st), 1, "compact");
+        check_launch(gpk::launch_gather_cols(Ps, ldn, w_map.p, 1.0, nl, nt, st_P[nb].p, ldn, st), 1, "compact");
         std::vector<gpk::SlotState> ns(nt);
         for (int q = 0; q < nt; ++q) ns[q] = hs[keep[q]];
         h2d(w_ss[nb].p, ns.data(), sizeof(gpk::SlotState) * nt);
@@ -674,14 +867,17 @@ struct gpk_ctx {
     for (int it = 1; it <= max_iters && ta > 0; ++it) {
       w_kx.ensure(static_cast<size_t>(ta) * ldn);
       apply_kernel(Ps, ldn, ta, w_kx.p, ldn, fp64, -1);  // K p (noise-free)
-      check_launch(gpk::launch_dot_partials(1, Ps, w_kx.p, noise, n, ldn, ta, ppap, st), 1, "dots");
-      check_launch(gpk::launch_cg_alpha(ppap, nrb, ta, it, ss, dh_a, max_iters, st), 1, "cg_alpha");
-      check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, n, ldn, ta, ss, st), 1, "cg_xr");
+      check_launch(gpk::launch_dot_partials(1, Ps, w_kx.p, noise, nl, ldn, ta, ppap, st), 1, "dots");
+      const double* gpap = global_partials(ppap, nrb, ta, tot + 2 * t, &nrg);
+      check_launch(gpk::launch_cg_alpha(gpap, nrg, ta, it, ss, dh_a, max_iters, st), 1, "cg_alpha");
+      check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, nl, ldn, ta, ss, st), 1, "cg_xr");
       psolve(Rs, ta, Zs);
-      check_launch(gpk::launch_dot_partials(0, Rs, Zs, 0.0, n, ldn, ta, prz, st), 1, "dots");
-      check_launch(gpk::launch_dot_partials(0, Zs, Zs, 0.0, n, ldn, ta, pzz, st), 1, "dots");
-      check_launch(gpk::launch_cg_beta(prz, pzz, nrb, ta, it, rel_tol, ss, dh_b, dh_r, max_iters, st), 1, "cg_beta");
-      check_launch(gpk::launch_cg_update_p(Ps, Zs, n, ldn, ta, ss, st), 1, "cg_p");
+      check_launch(gpk::launch_dot_partials(0, Rs, Zs, 0.0, nl, ldn, ta, prz, st), 1, "dots");
+      check_launch(gpk::launch_dot_partials(0, Zs, Zs, 0.0, nl, ldn, ta, pzz, st), 1, "dots");
+      const double* grz2 = global_partials(prz, nrb, ta, tot, &nrg);
+      const double* gzz2 = global_partials(pzz, nrb, ta, tot + t, &nrg);
+      check_launch(gpk::launch_cg_beta(grz2, gzz2, nrg, ta, it, rel_tol, ss, dh_b, dh_r, max_iters, st), 1, "cg_beta");
+      check_launch(gpk::launch_cg_update_p(Ps, Zs, nl, ldn, ta, ss, st), 1, "cg_p");
       // Host round trip only every sync_every iterations: converged / failed columns freeze
       // on the device (their flag) and are compacted out at the next sync.
       if (it % sync_every == 0 || it == max_iters) {
@@ -722,9 +918,9 @@ struct gpk_ctx {
       // R = B - (K X + s2 X)  in fp64
       w_kx.ensure(static_cast<size_t>(t) * ldn);
       apply_kernel(Xd, ldx, t, w_kx.p, ldn, true, -1);
-      check_launch(gpk::launch_gather_cols(Xd, ldx, nullptr, 1.0, n, t, w_tmp2.p, ldn, st), 1, "copy");
-      dim3 g((n + 255) / 256, t);
-      residual_kernel<<<g, 256, 0, st>>>(B, ldb, w_kx.p, w_tmp2.p, noise, n, ldn, w_B.p);
+      check_launch(gpk::launch_gather_cols(Xd, ldx, nullptr, 1.0, nl, t, w_tmp2.p, ldn, st), 1, "copy");
+      dim3 g((nl + 255) / 256, t);
+      residual_kernel<<<g, 256, 0, st>>>(B, ldb, w_kx.p, w_tmp2.p, noise, nl, ldn, w_B.p);
       check_launch(cudaGetLastError(), 1, "residual");
       psolve(w_B.p, t, w_tmp.p);
       const std::vector<double> zz = col_dots(w_tmp.p, w_tmp.p, t, ldn);
@@ -750,7 +946,7 @@ struct gpk_ctx {
       Eb.ensure(static_cast<size_t>(nb) * ldn);
       w_map.ensure(nb);
       h2d(w_map.p, bad.data(), sizeof(int) * nb);
-      check_launch(gpk::launch_gather_cols(w_B.p, ldn, w_map.p, 1.0, n, nb, Rb.p, ldn, st), 1, "gather");
+      check_launch(gpk::launch_gather_cols(w_B.p, ldn, w_map.p, 1.0, nl, nb, Rb.p, ldn, st), 1, "gather");
       // relative tolerance of the correction solve: 0.5 * rel_tol * norm0 / ||P^-1 r_true|| (< 0.5)
       std::vector<double> ts(nb);
       for (int q = 0; q < nb; ++q) ts[q] = 0.5 * scale[q];
@@ -759,9 +955,9 @@ struct gpk_ctx {
       // X[:, bad] += E   (the inner solve reused w_map: upload the column list again)
       h2d(w_map.p, bad.data(), sizeof(int) * nb);
       w_tmp2.ensure(static_cast<size_t>(nb) * ldn);
-      check_launch(gpk::launch_gather_cols(Xd, ldx, w_map.p, 1.0, n, nb, w_tmp2.p, ldn, st), 1, "gather");
-      check_launch(gpk::launch_axpby(w_tmp2.p, Eb.p, 1.0, 1.0, n, nb, ldn, st), 1, "axpy");
-      check_launch(gpk::launch_scatter_cols(w_tmp2.p, ldn, w_map.p, n, nb, Xd, ldx, st), 1, "scatter");
+      check_launch(gpk::launch_gather_cols(Xd, ldx, w_map.p, 1.0, nl, nb, w_tmp2.p, ldn, st), 1, "gather");
+      check_launch(gpk::launch_axpby(w_tmp2.p, Eb.p, 1.0, 1.0, nl, nb, ldn, st), 1, "axpy");
+      check_launch(gpk::launch_scatter_cols(w_tmp2.p, ldn, w_map.p, nl, nb, Xd, ldx, st), 1, "scatter");
       sync();
     }
     return used;
@@ -848,8 +1044,9 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   DBuf<double> B, Xs;
   B.ensure(static_cast<size_t>(t) * ldn);
   Xs.ensure(static_cast<size_t>(t) * ldn);
-  c->check_launch(gpk::launch_gather_cols(dy, n, nullptr, 1.0, n, 1, B.p, ldn, c->st), 1, "gather");
-  c->check_launch(gpk::launch_gather_cols(dZ, ldz, nullptr, 1.0, n, l, B.p + ldn, ldn, c->st), 1, "gather");
+  const int nl = c->nl, r0 = c->r0;  // this rank's rows of y, Z and the CG state
+  c->check_launch(gpk::launch_gather_cols(dy + r0, n, nullptr, 1.0, nl, 1, B.p, ldn, c->st), 1, "gather");
+  c->check_launch(gpk::launch_gather_cols(dZ + r0, ldz, nullptr, 1.0, nl, l, B.p + ldn, ldn, c->st), 1, "gather");
   std::vector<double> ah(static_cast<size_t>(t) * mi), bh(static_cast<size_t>(t) * mi);
   gpk_ctx::CgOut cg;
   try {
@@ -905,7 +1102,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   res->value_sample_variance = unbiased_variance(scaled);
   res->logdet = plogdet + stoch;
   res->logdet_precond = plogdet;
-  const double quad = c->col_dots(dy, U, 1, n)[0];  // y.u
+  const double quad = c->col_dots(dy + r0, U, 1, ldn)[0];  // y.u
   res->quad = quad;
   const double kPi = 3.14159265358979323846;
   res->value = -0.5 * (quad + res->logdet + static_cast<double>(n) * std::log(2.0 * kPi));
@@ -917,7 +1114,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   if (cfg->with_gradient) {
     require(res->gradient != nullptr, "evaluate_mll: null gradient buffer");
     // backward probe batch (gp_likelihood.hpp:79-84)
-    const double* Zb = dZ;
+    const double* Zb = dZ + r0;  // this rank's rows of the backward batch
     long long ldzb = ldz;
     DBuf<double> Zu, Su;
     const double* Sb = S;
@@ -926,7 +1123,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
       std::vector<double> hz(static_cast<size_t>(n) * l);
       make_probes_impl(n, l, mix_seed_impl(seed, 0xb2dULL), hz.data());
       Zu.ensure(static_cast<size_t>(l) * ldn);
-      CK(cudaMemcpy2DAsync(Zu.p, ldn * sizeof(double), hz.data(), n * sizeof(double), n * sizeof(double), l,
+      CK(cudaMemcpy2DAsync(Zu.p, ldn * sizeof(double), hz.data() + r0, n * sizeof(double), nl * sizeof(double), l,
                            cudaMemcpyHostToDevice, c->st));
       Zb = Zu.p;
       ldzb = ldn;
@@ -935,7 +1132,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
     DBuf<double> Zc, Q;
     Zc.ensure(static_cast<size_t>(l) * ldn);
     Q.ensure(static_cast<size_t>(l) * ldn);
-    c->check_launch(gpk::launch_gather_cols(Zb, ldzb, nullptr, 1.0, n, l, Zc.p, ldn, c->st), 1, "gather");
+    c->check_launch(gpk::launch_gather_cols(Zb, ldzb, nullptr, 1.0, nl, l, Zc.p, ldn, c->st), 1, "gather");
     c->psolve(Zc.p, l, Q.p);
     std::vector<std::vector<double>> tw(np, std::vector<double>(l, 0.0));
     std::vector<double> tdet(np, 0.0);
@@ -951,20 +1148,22 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         DBuf<double> A, Bw, part;
         A.ensure(static_cast<size_t>(2) * l * k);
         Bw.ensure(static_cast<size_t>(2) * l * k);
-        part.ensure(gpk::g1_workspace(n, k, l));
-        c->check_launch(gpk::launch_g1(c->L.p, n, k, Q.p, ldn, l, n, part.p, A.p, k, c->st), 2, "g1");
-        c->check_launch(gpk::launch_g1(c->L.p, n, k, Zc.p, ldn, l, n, part.p, A.p + static_cast<size_t>(l) * k, k,
-                                       c->st),
+        part.ensure(gpk::g1_workspace(nl, k, l));
+        c->check_launch(gpk::launch_g1(c->L.p + r0, n, k, Q.p, ldn, l, nl, part.p, A.p, k, c->st), 2, "g1");
+        c->check_launch(gpk::launch_g1(c->L.p + r0, n, k, Zc.p, ldn, l, nl, part.p, A.p + static_cast<size_t>(l) * k,
+                                       k, c->st),
                         2, "g1");
+        c->allreduce_sum(A.p, 2LL * l * k);
         std::vector<double> hA(static_cast<size_t>(2) * l * k), hB(static_cast<size_t>(2) * l * k);
         c->d2h(hA.data(), A.p, sizeof(double) * hA.size());
         for (int w = 0; w <= d; ++w) {
           tdet[w] = c->trace_det[w];
           const double* dLw = c->dL.p + static_cast<size_t>(w) * n * k;
-          c->check_launch(gpk::launch_g1(dLw, n, k, Q.p, ldn, l, n, part.p, Bw.p, k, c->st), 2, "g1");
+          c->check_launch(gpk::launch_g1(dLw + r0, n, k, Q.p, ldn, l, nl, part.p, Bw.p, k, c->st), 2, "g1");
           c->check_launch(
-              gpk::launch_g1(dLw, n, k, Zc.p, ldn, l, n, part.p, Bw.p + static_cast<size_t>(l) * k, k, c->st), 2,
-              "g1");
+              gpk::launch_g1(dLw + r0, n, k, Zc.p, ldn, l, nl, part.p, Bw.p + static_cast<size_t>(l) * k, k, c->st),
+              2, "g1");
+          c->allreduce_sum(Bw.p, 2LL * l * k);
           c->d2h(hB.data(), Bw.p, sizeof(double) * hB.size());
           for (int i = 0; i < l; ++i) {
             // (dL' q_i).(L' z_i) + (L' q_i).(dL' z_i)   (LowRankDerivOp::apply, preconditioners.hpp:62-69)
@@ -1005,7 +1204,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
     }
     // noise: w_i = s_i (cached forward solves when shared, gp_likelihood.hpp:90)
     {
-      const double uu = c->col_dots(U, U, 1, n)[0];
+      const double uu = c->col_dots(U, U, 1, ldn)[0];
       quadw[d + 1] = uu;
       const std::vector<double> zs = c->col_dots(Zc.p, Sb, l, ldn);
       for (int i = 0; i < l; ++i) zw[d + 1][i] = zs[i];
@@ -1028,24 +1227,40 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
               src, lds, n, n_pad, tt, reinterpret_cast<float*>(dst));
         c->check_launch(cudaGetLastError(), 1, "to_padded");
       };
-      conv(U, n, 1, Up);
-      conv(Sb, ldsb, l, SZp);
-      conv(Zc.p, ldn, l, SZp + elem * static_cast<size_t>(l) * n_pad);
+      // the b-side of the pairs runs over all n rows: all-gather u, S, Z when sharded
+      const double *Uall = U, *Sall = Sb, *Zall = Zc.p;
+      long long ldU = ldn, ldS = ldsb, ldZ = ldn;
+      DBuf<double> Uf, Sf, Zf;
+      if (c->world > 1) {
+        Uf.ensure(static_cast<size_t>(n));
+        Sf.ensure(static_cast<size_t>(l) * n);
+        Zf.ensure(static_cast<size_t>(l) * n);
+        c->allgather_cols(U, ldn, 1, Uf.p, n);
+        c->allgather_cols(Sb, ldsb, l, Sf.p, n);
+        c->allgather_cols(Zc.p, ldn, l, Zf.p, n);
+        Uall = Uf.p;
+        Sall = Sf.p;
+        Zall = Zf.p;
+        ldU = ldS = ldZ = n;
+      }
+      conv(Uall, ldU, 1, Up);
+      conv(Sall, ldS, l, SZp);
+      conv(Zall, ldZ, l, SZp + elem * static_cast<size_t>(l) * n_pad);
       const void* Xp = fp64 ? static_cast<const void*>(c->X64s.p) : static_cast<const void*>(c->X32.p);
       int nblk = 0;
-      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, n, n_pad, l, d, nullptr, &nblk,
-                                                 c->st),
+      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, r0, nl, n_pad, l, nullptr,
+                                                 &nblk, c->st),
                       0, "deriv_contract");
       const int na = 2 * (c->dp + 1);
       DBuf<double> part;
       part.ensure(static_cast<size_t>(nblk) * na);
       auto ev = c->prof_begin(1);
-      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, n, n_pad, l, d, part.p, &nblk,
-                                                 c->st),
+      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, r0, nl, n_pad, l, part.p,
+                                                 &nblk, c->st),
                       1, "deriv_contract");
       {
         const int cf[] = {2, 3, 6, 9};
-        const double nn = static_cast<double>(n) * n;
+        const double nn = static_cast<double>(nl) * n;
         c->prof_end(1, ev, nn * ((l + 1) + 2.0 * (d + 1) + 3.0 * d + cf[c->family] + 4.0), nn);
       }
       std::vector<double> hp(static_cast<size_t>(nblk) * na);
@@ -1053,6 +1268,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
       std::vector<double> tot(na, 0.0);
       for (int b = 0; b < nblk; ++b)
         for (int q = 0; q < na; ++q) tot[q] += hp[static_cast<size_t>(b) * na + q];
+      tot = c->allreduce_host(tot);  // rank-ordered sum of the per-rank pair sums
       const double cpre = fp64 ? 1.0 : gpk::prescale_c(c->family);
       const int DP = c->dp;
       // outputscale: dK = 2 o shape ; lengthscale j: dK = (-2 o^2 / l_j) shape_ds ds_j^2
@@ -1068,7 +1284,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         gsum[1 + j] = fac * tot[DP + 2 + j];
         per_probe[1 + j] = false;
       }
-      c->entries += static_cast<long long>(n) * n;
+      c->entries += static_cast<long long>(nl) * n;
       // gradient for the non-noise parameters from the summed stochastic term
       for (int w = 0; w <= d; ++w) {
         double tsum = 0.0;
@@ -1105,8 +1321,8 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
       for (int w = 0; w <= d; ++w) {
         const std::vector<double> zs = c->col_dots(Zc.p, Wsol.p + static_cast<size_t>(w) * l * ldn, l, ldn);
         for (int i = 0; i < l; ++i) zw[w][i] = zs[i];
-        c->apply_kernel(U, n, 1, du.p, ldn, fp64, w);
-        quadw[w] = c->col_dots(U, du.p, 1, n)[0];
+        c->apply_kernel(U, ldn, 1, du.p, ldn, fp64, w);
+        quadw[w] = c->col_dots(U, du.p, 1, ldn)[0];
       }
       for (int w = 0; w <= d; ++w) {
         std::vector<double> gm(l);
@@ -1186,6 +1402,72 @@ gpk_status gpk_create(int device, gpk_ctx** out) {
   return GPK_OK;
 }
 
+gpk_status gpk_nccl_unique_id(void* out) {
+  if (!out) return GPK_INPUT_ERROR;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return GPK_NCCL_ERROR;
+  std::memcpy(out, &id, sizeof(id));
+  return GPK_OK;
+}
+
+gpk_status gpk_create_sharded(int device, int rank, int world, const void* nccl_id, gpk_ctx** out) {
+  if (!out || !nccl_id || world < 1 || rank < 0 || rank >= world) return GPK_INPUT_ERROR;
+  const gpk_status s0 = gpk_create(device, out);
+  if (s0 != GPK_OK) return s0;
+  gpk_ctx* c = *out;
+  const gpk_status s = guard(c, [&] {
+    auto nc = std::make_unique<NcclComm>();
+    nc->rank = rank;
+    nc->world = world;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    const ncclResult_t r = ncclCommInitRank(&nc->c, world, id, rank);
+    if (r != ncclSuccess) fail(GPK_NCCL_ERROR, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    c->comm = std::move(nc);
+    c->rank = rank;
+    c->world = world;
+  });
+  if (s != GPK_OK) {
+    gpk_destroy(c);
+    *out = nullptr;
+  }
+  return s;
+}
+
+gpk_status gpk_group_create(int world, gpk_group** out) {
+  if (!out || world < 1) return GPK_INPUT_ERROR;
+  auto* g = new gpk_group();
+  g->world = world;
+  g->host.resize(world);
+  *out = g;
+  return GPK_OK;
+}
+
+void gpk_group_destroy(gpk_group* g) { delete g; }
+
+gpk_status gpk_create_in_group(int device, gpk_group* g, int rank, gpk_ctx** out) {
+  if (!out || !g || rank < 0 || rank >= g->world) return GPK_INPUT_ERROR;
+  const gpk_status s0 = gpk_create(device, out);
+  if (s0 != GPK_OK) return s0;
+  gpk_ctx* c = *out;
+  auto gc = std::make_unique<GroupComm>();
+  gc->g = g;
+  gc->rank = rank;
+  gc->world = g->world;
+  c->comm = std::move(gc);
+  c->rank = rank;
+  c->world = g->world;
+  return GPK_OK;
+}
+
+gpk_status gpk_shard_rows(const gpk_ctx* ctx, int64_t* r0, int64_t* r1) {
+  if (!ctx || !r0 || !r1) return GPK_INPUT_ERROR;
+  if (!ctx->have_data) return GPK_INPUT_ERROR;
+  *r0 = ctx->r0;
+  *r1 = ctx->r1;
+  return GPK_OK;
+}
+
 void gpk_destroy(gpk_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
@@ -1242,7 +1524,7 @@ static void set_data_common(gpk_ctx* c, const double* X, int64_t n, int64_t d, i
   c->n = static_cast<int>(n);
   c->d = static_cast<int>(d);
   c->n_pad = static_cast<int>((n + 127) / 128 * 128);
-  c->ldn = (n + 31) / 32 * 32;
+  c->set_shard();  // this rank's rows [r0, r1) and the local leading dimension
   c->dp = gpk::dpad_for(c->d);
   c->X.ensure(static_cast<size_t>(n) * d);
   CK(cudaMemcpy2DAsync(c->X.p, n * sizeof(double), X, ldx * sizeof(double), n * sizeof(double), d,
@@ -1301,11 +1583,13 @@ static void mvm_common(gpk_ctx* c, int which, const double* V, int64_t ldv, int 
   DBuf<double> dv, dout;
   dv.ensure(static_cast<size_t>(t) * c->ldn);
   dout.ensure(static_cast<size_t>(t) * c->ldn);
-  CK(cudaMemcpy2DAsync(dv.p, c->ldn * sizeof(double), V, ldv * sizeof(double), n * sizeof(double), t,
+  // sharded: this rank uploads and writes back its rows [r0, r1) only
+  const int nl = c->nl, r0 = c->r0;
+  CK(cudaMemcpy2DAsync(dv.p, c->ldn * sizeof(double), V + r0, ldv * sizeof(double), nl * sizeof(double), t,
                        cudaMemcpyHostToDevice, c->st));
   c->apply_kernel(dv.p, c->ldn, t, dout.p, c->ldn, precision == GPK_PREC_FP64, which);
-  if (which < 0) c->check_launch(gpk::launch_axpby(dout.p, dv.p, 1.0, c->noise, n, t, c->ldn, c->st), 1, "axpy");
-  CK(cudaMemcpy2DAsync(out, ldo * sizeof(double), dout.p, c->ldn * sizeof(double), n * sizeof(double), t,
+  if (which < 0) c->check_launch(gpk::launch_axpby(dout.p, dv.p, 1.0, c->noise, nl, t, c->ldn, c->st), 1, "axpy");
+  CK(cudaMemcpy2DAsync(out + r0, ldo * sizeof(double), dout.p, c->ldn * sizeof(double), nl * sizeof(double), t,
                        cudaMemcpyDeviceToHost, c->st));
   c->sync();
 }
@@ -1592,14 +1876,14 @@ gpk_status gpk_precond_deriv_factor(gpk_ctx* ctx, int which, double* dL, int64_t
 gpk_status gpk_precond_solve(gpk_ctx* ctx, const double* V, int64_t ldv, int t, double* out, int64_t ldo) {
   return guard(ctx, [&] {
     require(ctx->pkind != 0, "gpkrylov_cuda: no preconditioner");
-    const int n = ctx->n;
+    const int nl = ctx->nl, r0 = ctx->r0;  // sharded: own rows only
     DBuf<double> dv, dz;
     dv.ensure(static_cast<size_t>(t) * ctx->ldn);
     dz.ensure(static_cast<size_t>(t) * ctx->ldn);
-    CK(cudaMemcpy2DAsync(dv.p, ctx->ldn * sizeof(double), V, ldv * sizeof(double), n * sizeof(double), t,
+    CK(cudaMemcpy2DAsync(dv.p, ctx->ldn * sizeof(double), V + r0, ldv * sizeof(double), nl * sizeof(double), t,
                          cudaMemcpyHostToDevice, ctx->st));
     ctx->psolve(dv.p, t, dz.p);
-    CK(cudaMemcpy2DAsync(out, ldo * sizeof(double), dz.p, ctx->ldn * sizeof(double), n * sizeof(double), t,
+    CK(cudaMemcpy2DAsync(out + r0, ldo * sizeof(double), dz.p, ctx->ldn * sizeof(double), nl * sizeof(double), t,
                          cudaMemcpyDeviceToHost, ctx->st));
     ctx->sync();
   });
@@ -1643,7 +1927,8 @@ gpk_status gpk_mbcg(gpk_ctx* ctx, const double* B, int64_t ldb, int t, const gpk
     DBuf<double> db, dx;
     db.ensure(static_cast<size_t>(t) * c->ldn);
     dx.ensure(static_cast<size_t>(t) * c->ldn);
-    CK(cudaMemcpy2DAsync(db.p, c->ldn * sizeof(double), B, ldb * sizeof(double), n * sizeof(double), t,
+    // sharded: this rank solves for its rows [r0, r1) of every column
+    CK(cudaMemcpy2DAsync(db.p, c->ldn * sizeof(double), B + c->r0, ldb * sizeof(double), c->nl * sizeof(double), t,
                          cudaMemcpyHostToDevice, c->st));
     require(cfg->precision >= GPK_PREC_FP64 && cfg->precision <= GPK_PREC_TF32X3, "CgConfig: unknown precision");
     const bool fp64 = cfg->precision == GPK_PREC_FP64;
@@ -1660,7 +1945,7 @@ gpk_status gpk_mbcg(gpk_ctx* ctx, const double* B, int64_t ldb, int t, const gpk
       double mr;
       c->refine(db.p, c->ldn, t, dx.p, c->ldn, r, mi, cfg->rel_tol, cfg->refine, &mr);
     }
-    CK(cudaMemcpy2DAsync(X, ldx * sizeof(double), dx.p, c->ldn * sizeof(double), n * sizeof(double), t,
+    CK(cudaMemcpy2DAsync(X + c->r0, ldx * sizeof(double), dx.p, c->ldn * sizeof(double), c->nl * sizeof(double), t,
                          cudaMemcpyDeviceToHost, c->st));
     c->sync();
     for (int q = 0; q < t; ++q) {
@@ -1686,11 +1971,11 @@ gpk_status gpk_evaluate_mll(gpk_ctx* ctx, const double* y, const double* Z, int6
       if (!std::isfinite(y[i])) fail(GPK_INPUT_ERROR, "KernelOperator: non-finite entries in input vector");
     DBuf<double> dy, dz;
     dy.ensure(n);
-    dz.ensure(static_cast<size_t>(l) * c->ldn);
+    dz.ensure(static_cast<size_t>(l) * n);
     c->h2d(dy.p, y, sizeof(double) * n);
-    CK(cudaMemcpy2DAsync(dz.p, c->ldn * sizeof(double), Z, ldz * sizeof(double), n * sizeof(double), l,
+    CK(cudaMemcpy2DAsync(dz.p, n * sizeof(double), Z, ldz * sizeof(double), n * sizeof(double), l,
                          cudaMemcpyHostToDevice, c->st));
-    evaluate_impl(c, dy.p, dz.p, c->ldn, l, probe_seed, cfg, res);
+    evaluate_impl(c, dy.p, dz.p, n, l, probe_seed, cfg, res);
   });
 }
 

@@ -18,6 +18,8 @@ struct MvmArgs {
   double scale;              // output scale (o^2, 2o, -2 o^2 / l_j / c_fam, ...)
   long long split_stride;    // element offset between split-K partial outputs
   int flush;                 // tcgen05 path: j-tiles per TMEM accumulation group (fp64 drain period)
+  int row_begin;             // first output row of this rank's shard (multiple of 128)
+  int row_end;               // one past the last output row; outputs are stored at row - row_begin
 };
 
 // Packed-operand geometry for a given column count.
@@ -64,8 +66,9 @@ cudaError_t launch_kernel_column(int family, const double* sx, const double* x, 
 //   quad[w]  = sum_ab dK_w[a,b] u_a u_b
 //   gamma[w] = sum_ab dK_w[a,b] sum_i S[a,i] Z[b,i]
 // returns the raw (unscaled) sums; the host applies the factors.
+// a-rows restricted to [a_begin, a_begin + a_rows) (this rank's shard), b over all n_pad rows.
 cudaError_t launch_deriv_contract(bool fp64, int family, int dp, const void* X, const void* U, const void* Zt,
-                                  int n, int n_pad, int l, int d, double* partials, int* nblocks,
+                                  int a_begin, int a_rows, int n_pad, int l, double* partials, int* nblocks,
                                   cudaStream_t st);
 
 }  // namespace gpk

@@ -57,7 +57,7 @@ cudaError_t launch_fused_kmvm(bool fp64, int family, int dp, int mode, const voi
                               const MvmArgs& a, int splits, cudaStream_t st) {
   const MvmShape sh = mvm_shape(a.t, fp64, mode);
   if (sh.tn < 0) return cudaErrorInvalidValue;
-  dim3 g(a.n_pad / kBM, splits);
+  dim3 g((a.row_end - a.row_begin + kBM - 1) / kBM, splits);
   switch (family) {
     case kRBF: return launch_fused_kmvm_fam<kRBF>(fp64, dp, mode, sh.tn, X, V, out, a, g, st);
     case kMatern12: return launch_fused_kmvm_fam<kMatern12>(fp64, dp, mode, sh.tn, X, V, out, a, g, st);

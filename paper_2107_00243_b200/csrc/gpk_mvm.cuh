@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && TN <= 9) ? 2 : 1)
   T* Ks = Vs + kStages * kBK * VLD;
 
   const int tid = threadIdx.x;
-  const int row0 = blockIdx.x * kBM;
+  const int row0 = a.row_begin + blockIdx.x * kBM;
   const int jt0 = blockIdx.y * a.jtiles_per_split;
   const int jt1 = min(jt0 + a.jtiles_per_split, a.n_pad / kBK);
   const int nt = jt1 - jt0;
@@ -298,11 +298,11 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && TN <= 9) ? 2 : 1)
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int row = row0 + rg * 4 + r;
-      if (row < a.n) {
+      if (row < a.row_end) {
         double v;
         if constexpr (sizeof(T) == 4) v = acc64[r][c];
         else v = static_cast<double>(acc[r][c]);
-        o[static_cast<long long>(col) * a.ldo + row] = a.scale * v;
+        o[static_cast<long long>(col) * a.ldo + (row - a.row_begin)] = a.scale * v;
       }
     }
   }

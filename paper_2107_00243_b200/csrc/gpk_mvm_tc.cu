@@ -50,7 +50,7 @@ cudaError_t launch_fused_kmvm_tc(int family, int dp, const float* X, const float
                                  const MvmArgs& a, int splits, cudaStream_t st) {
   const int npad = tc_npad(a.t);
   if (npad < 0) return cudaErrorInvalidValue;
-  dim3 g(a.n_pad / tc::BM, splits);
+  dim3 g((a.row_end - a.row_begin + tc::BM - 1) / tc::BM, splits);
   const int nc8 = npad / 8;
   switch (family) {
     case kRBF: return tc::launch_tc_fam<kRBF>(dp, nc8, X, vhi, vlo, out, a, g, st);

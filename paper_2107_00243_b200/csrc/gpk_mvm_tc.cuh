@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int row0 = blockIdx.x * BM;
+  const int row0 = a.row_begin + blockIdx.x * BM;
   const int jt0 = blockIdx.y * a.jtiles_per_split;
   const int jt1 = min(jt0 + a.jtiles_per_split, a.n_pad / BK);
   const int nt = jt1 - jt0;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (nt > 0) drain((nt - 1) / F);
     // epilogue: column-major fp64 output (or split-K partial)
-    if (row < a.n) {
+    if (row < a.row_end) {
       double* o = out + static_cast<long long>(blockIdx.y) * a.split_stride;
 #pragma unroll
       for (int h = 0; h < HC; ++h) {
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int col = c8 * 8 + e;
-          if (col < a.t) o[static_cast<long long>(col) * a.ldo + row] = a.scale * acc64[h * 8 + e];
+          if (col < a.t) o[static_cast<long long>(col) * a.ldo + (row - a.row_begin)] = a.scale * acc64[h * 8 + e];
         }
       }
     }

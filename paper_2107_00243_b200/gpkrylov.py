@@ -148,13 +148,43 @@ def noise_index(d):
     return d + 1
 
 
-class _Ctx:
-    """Owns one gpk_ctx (device state: data, packed operands, preconditioner, workspaces)."""
+class RankGroup:
+    """In-process group of `world` ranks (one host thread per rank) for the row-sharded path;
+    collectives are host-staged, so it runs on any number of devices (also one)."""
 
-    def __init__(self, device=0):
+    def __init__(self, world: int):
+        self.lib = capi.lib()
+        g = C.c_void_p()
+        _check(self.lib.gpk_group_create(int(world), C.byref(g)), None, "gpk_group_create failed")
+        self.g = g
+        self.world = int(world)
+
+    def __del__(self):
+        try:
+            if getattr(self, "g", None):
+                self.lib.gpk_group_destroy(self.g)
+                self.g = None
+        except Exception:
+            pass
+
+
+class _Ctx:
+    """Owns one gpk_ctx (device state: data, packed operands, preconditioner, workspaces).
+    shard=(RankGroup, rank) or ("nccl", rank, world, unique_id_bytes) makes it one rank of a
+    row-sharded evaluation."""
+
+    def __init__(self, device=0, shard=None):
         self.lib = capi.lib()
         h = C.c_void_p()
-        rc = self.lib.gpk_create(int(device), C.byref(h))
+        if shard is None:
+            rc = self.lib.gpk_create(int(device), C.byref(h))
+        elif isinstance(shard[0], RankGroup):
+            self.group = shard[0]  # keep the group alive
+            rc = self.lib.gpk_create_in_group(int(device), shard[0].g, int(shard[1]), C.byref(h))
+        else:
+            _, rank, world, uid = shard
+            buf = C.create_string_buffer(bytes(uid), 128)
+            rc = self.lib.gpk_create_sharded(int(device), int(rank), int(world), buf, C.byref(h))
         if rc != capi.GPK_OK:
             raise CudaError(f"gpk_create(device={device}) failed with status {rc}: no usable CUDA device")
         self.h = h
@@ -181,7 +211,7 @@ class KernelOperator:
     hyperparameters while keeping the attached preconditioner (the line-search
     situation of optimizer.hpp:437 vs :450-451)."""
 
-    def __init__(self, spec: KernelSpec, x, params: Hyperparameters, device: int = 0, precision="fp64"):
+    def __init__(self, spec: KernelSpec, x, params: Hyperparameters, device: int = 0, precision="fp64", shard=None):
         x = np.asfortranarray(np.asarray(x, dtype=np.float64))
         if x.ndim != 2 or x.shape[0] < 1:
             raise InputError("KernelOperator: empty dataset")
@@ -191,7 +221,7 @@ class KernelOperator:
         self._x = x
         self.params = params
         self.precision = precision
-        self.ctx = _Ctx(device)
+        self.ctx = _Ctx(device, shard)
         self.ctx.check(self.ctx.lib.gpk_set_data(self.ctx.h, _ptr(x), x.shape[0], x.shape[1], x.shape[0]))
         self._set_params(params)
         self.preconditioner = None
@@ -247,6 +277,12 @@ class KernelOperator:
         return self._mvm(which, v, precision)
 
     deriv_apply_matrix = deriv_apply
+
+    def shard_rows(self):
+        """This rank's [r0, r1) rows of the n-length arrays (the whole range when unsharded)."""
+        a, b = C.c_int64(), C.c_int64()
+        self.ctx.check(self.ctx.lib.gpk_shard_rows(self.ctx.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def kernel_diagonal(self):  # kernels.hpp:230-233
         return np.full(self.rows(), self.params.outputscale() ** 2)

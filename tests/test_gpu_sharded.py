@@ -1,0 +1,108 @@
+"""Row-sharded multi-rank path of the C++ driver, run as an in-process rank group
+(one host thread per rank) on one GPU: every collective is host-staged, no kernel
+waits on another.  Results must match the single-rank evaluation (the MVM rows
+bitwise; reductions differ only in their rank grouping)."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2107_00243_b200 as gk
+from paper_2107_00243_b200.gpkrylov import RankGroup
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(world, fn):
+    group = RankGroup(world)
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            out[r] = fn(group, r)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    return out
+
+
+def problem(orc, n=1000, d=3):
+    x = orc.random_matrix(n, d, 501)
+    y = np.sin(2 * x[:, 0]) + 0.1 * orc.random_matrix(n, 1, 502)[:, 0]
+    hp = gk.Hyperparameters.from_raw(d, 1.1, 0.8, 0.05)
+    return x, y, hp
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_mvm_rows_bitwise(orc, world):
+    x, y, hp = problem(orc, n=1100)
+    v = orc.random_matrix(1100, 9, 503)
+    ref = {p: gk.KernelOperator(gk.KernelSpec("matern32"), x, hp).apply(v, precision=p)
+           for p in ("fp64", "fp32", "tf32x3")}
+
+    def fn(group, r):
+        op = gk.KernelOperator(gk.KernelSpec("matern32"), x, hp, shard=(group, r))
+        r0, r1 = op.shard_rows()
+        res = {}
+        for p in ("fp64", "fp32", "tf32x3"):
+            res[p] = op.apply(v, precision=p)[r0:r1]
+        return r0, r1, res
+
+    rows = run_ranks(world, fn)
+    assert rows[0][0] == 0 and rows[-1][1] == 1100
+    for r0, r1, res in rows:
+        for p in res:
+            assert np.array_equal(res[p], ref[p][r0:r1]), p
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("precision,backward", [("fp64", "faithful"), ("fp64", "fused"), ("tf32x3", "fused")])
+def test_sharded_evaluate_matches_single_rank(orc, world, precision, backward):
+    x, y, hp = problem(orc)
+    n = x.shape[0]
+    z = gk.make_probes(n, 6, gk.mix_seed(17, 1))
+    cfg = gk.MllConfig(gk.CgConfig(400, 1e-8, False, precision, 2), True, backward)
+    op1 = gk.KernelOperator(gk.KernelSpec("rbf"), x, hp)
+    pc1 = gk.pivoted_cholesky_with_derivatives(op1, 12)
+    want = gk.evaluate_mll(y, op1, pc1, z, cfg)
+
+    def fn(group, r):
+        op = gk.KernelOperator(gk.KernelSpec("rbf"), x, hp, shard=(group, r))
+        pc = gk.pivoted_cholesky_with_derivatives(op, 12)
+        return gk.evaluate_mll(y, op, pc, z, cfg)
+
+    res = run_ranks(world, fn)
+    for r in res:  # every rank reports the same global result
+        assert r.value == res[0].value
+        assert np.array_equal(r.gradient, res[0].gradient)
+    got = res[0]
+    tol = 1e-9 if precision == "fp64" else 1e-6
+    assert got.value == pytest.approx(want.value, rel=tol)
+    assert got.logdet == pytest.approx(want.logdet, rel=tol)
+    np.testing.assert_allclose(got.gradient, want.gradient, rtol=100 * tol, atol=1e-9)
+    assert abs(got.total_cg_iterations - want.total_cg_iterations) <= 2 * 7
+
+
+def test_sharded_identity_and_mbcg(orc):
+    x, y, hp = problem(orc, n=700, d=2)
+    b = orc.random_matrix(700, 4, 505)
+    op1 = gk.KernelOperator(gk.KernelSpec("matern52"), x, hp)
+    ref = gk.batched_pcg(op1, b, gk.IdentityPreconditioner(op1), gk.CgConfig(500, 1e-9, False, "fp64", 0))
+
+    def fn(group, r):
+        op = gk.KernelOperator(gk.KernelSpec("matern52"), x, hp, shard=(group, r))
+        res = gk.batched_pcg(op, b, gk.IdentityPreconditioner(op), gk.CgConfig(500, 1e-9, False, "fp64", 0))
+        return op.shard_rows(), res
+
+    out = run_ranks(2, fn)
+    for (r0, r1), res in out:
+        for c in range(4):
+            assert abs(res[c].iterations_used - ref[c].iterations_used) <= max(1, ref[c].iterations_used // 10)
+            np.testing.assert_allclose(res[c].solution[r0:r1], ref[c].solution[r0:r1], rtol=1e-6, atol=1e-9)
