@@ -114,8 +114,9 @@ def run_ours(args, rank_env):
     w = workloads.config(args.workload, rank=args.rank)
     x, y = workloads.generate(w)
     n, d, l = w.n, w.d, w.probes
-    # replicas (N > 1): each rank evaluates with its own probe batch (optimizer step rank+1)
-    seed = int(lib.gpk_mix_seed(workloads.PROBE_SEED, 1 + rank))
+    # replicas (N > 1): each rank evaluates with its own probe batch (optimizer step rank+1);
+    # sharded: all ranks share the one evaluation's probes
+    seed = int(lib.gpk_mix_seed(workloads.PROBE_SEED, 1 + (rank if args.mode == "replicas" else 0)))
     z = np.empty((n, l), order="F")
     assert lib.gpk_make_probes(n, l, C.c_uint64(seed), z.ctypes.data_as(C.POINTER(C.c_double))) == 0
     log_o, log_ls, log_noise = w.log_params
@@ -129,7 +130,21 @@ def run_ours(args, rank_env):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2 (126 MB)
 
     ctx = C.c_void_p()
-    assert lib.gpk_create(local, C.byref(ctx)) == 0, "gpk_create failed"
+    if world > 1 and args.mode == "sharded":
+        # one evaluation row-sharded over all ranks: NCCL communicator inside the library
+        import torch.distributed as dist
+
+        uid = [None]
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            assert lib.gpk_nccl_unique_id(buf) == 0
+            uid[0] = buf.raw
+        dist.broadcast_object_list(uid, src=0)
+        ub = C.create_string_buffer(uid[0], 128)
+        rc = lib.gpk_create_sharded(local, rank, world, ub, C.byref(ctx))
+        assert rc == 0, f"gpk_create_sharded failed ({rc})"
+    else:
+        assert lib.gpk_create(local, C.byref(ctx)) == 0, "gpk_create failed"
     stream = torch.cuda.ExternalStream(lib.gpk_stream(ctx), device=dev)
     prec = {"fp64": capi.GPK_PREC_FP64, "fp32": capi.GPK_PREC_FP32, "tf32x3": capi.GPK_PREC_TF32X3}[args.precision]
     cfg = capi.gpk_mll_cfg(capi.gpk_cg_cfg(w.max_iters, w.rel_tol, 0, prec, args.refine), 1, 1,
@@ -288,6 +303,8 @@ def main():
     ap.add_argument("--refine", type=int, default=2)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
+                    help="N>1: one row-sharded evaluation over N GPUs (NCCL) or N independent replicas")
     ap.add_argument("--cpu-iters", type=int, default=None, help="CG iterations for the CPU extrapolation")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -302,7 +319,8 @@ def main():
               "n": w.n, "d": w.d, "probes": w.probes, "precond_rank": w.rank, "precision": args.precision,
               "backward": args.backward, "l2": "flushed between timed steps (256 MB write)",
               "step": "set_data + set_params + pivoted_cholesky(+deriv factors) + evaluate_mll(value+grad)",
-              "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"}
+              "parallelism": (f"row-sharded x{world} (NCCL)" if args.mode == "sharded" else f"replicas x{world}")
+              if world > 1 else "1 GPU"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -337,8 +355,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         per_step, e2e = float(t[0]), float(t[1])
     # replicas: N independent evaluations per step -> whole-job seconds per evaluation
-    value = per_step / world
-    e2e_value = e2e / world
+    # sharded: one evaluation across all GPUs (strong scaling); replicas: N evaluations per step
+    div = world if args.mode == "replicas" else 1
+    value = per_step / div
+    e2e_value = e2e / div
     mvm = r["mvm"]
     fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     achieved = (mvm["flops"] / mvm["launches"]) / (mvm["ms"] / mvm["launches"] / 1e3) / 1e12 if mvm["launches"] else 0
@@ -375,7 +395,7 @@ def main():
                                   "share_of_step": (dcp["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "weak" if (world == 1 or args.mode == "replicas") else "strong", "vs_baseline": None,
             "dtype": {"fp64": "f64", "fp32": "f32 entries+contraction / f64 CG state",
                       "tf32x3": "f32 entries, 3xTF32 tensor-core contraction / f64 CG state"}[args.precision],
             "data": "synthetic (seeded stand-in for the BASELINE config; UCI data unavailable offline)",

@@ -87,7 +87,8 @@ def test_sharded_evaluate_matches_single_rank(orc, world, precision, backward):
     assert got.value == pytest.approx(want.value, rel=tol)
     assert got.logdet == pytest.approx(want.logdet, rel=tol)
     np.testing.assert_allclose(got.gradient, want.gradient, rtol=100 * tol, atol=1e-9)
-    assert abs(got.total_cg_iterations - want.total_cg_iterations) <= 2 * 7
+    # +-1 iteration per column from the regrouped reductions (up to 31 solves in faithful mode)
+    assert abs(got.total_cg_iterations - want.total_cg_iterations) <= max(14, want.total_cg_iterations // 100)
 
 
 def test_sharded_identity_and_mbcg(orc):
