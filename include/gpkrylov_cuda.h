@@ -46,6 +46,17 @@ typedef enum { GPK_PREC_FP64 = 0, GPK_PREC_FP32 = 1, GPK_PREC_TF32X3 = 2 } gpk_p
  * cores in split precision (a_hi b_hi + a_hi b_lo + a_lo b_hi, tf32 parts), fp32
  * accumulation in TMEM over 128 entries and fp64 across; derivative MVMs use FP32. */
 
+/* Kernel-entry strategy of the tensor-core (GPK_PREC_TF32X3) value MVM.
+ * DIRECT: fp32 direct-difference squared distances on the CUDA cores (any family).
+ * GRAM: expanded distances |x_i|^2 + |x_j|^2 - 2 x_i.x_j (the reference's own
+ *   column formula, kernels.hpp:235-243) with the cross term on the tensor cores
+ *   (3xTF32) from mean-centred coordinates; near pairs (s <= (|x_i|^2+|x_j|^2)/16,
+ *   where cancellation would dominate) recomputed by direct differences;
+ *   RBF / Matern-3/2 / Matern-5/2, d <= 32.
+ * AUTO (default): GRAM when eligible, d >= 6 and max |x~|^2 of the centred
+ *   pre-scaled coordinates <= 320, else DIRECT. */
+typedef enum { GPK_MVM_AUTO = 0, GPK_MVM_DIRECT = 1, GPK_MVM_GRAM = 2 } gpk_mvm_variant;
+
 /* krylov.hpp:15-24 CgConfig (+ GPU fields). */
 typedef struct {
   int max_iters;        /* >= 1 */
@@ -166,6 +177,11 @@ gpk_status gpk_evaluate_mll_device(gpk_ctx* ctx, const double* dy, const double*
 /* ---- probes (trace_estimation.hpp:27-36, common.hpp:93-98) --------------- */
 gpk_status gpk_make_probes(int64_t n, int count, uint64_t seed, double* out /* n x count col-major */);
 uint64_t gpk_mix_seed(uint64_t seed, uint64_t salt);
+
+/* Select the tensor-core MVM variant (takes effect at the next call). */
+gpk_status gpk_set_mvm_variant(gpk_ctx* ctx, int variant);
+/* The variant the current data/params use (DIRECT or GRAM) and max |x~|^2 of the centred coordinates. */
+gpk_status gpk_get_mvm_variant(gpk_ctx* ctx, int* variant, double* max_sqnorm);
 
 /* Number of this library's kernels launched on ctx since creation. */
 long long gpk_launch_count(const gpk_ctx* ctx);

@@ -11,12 +11,13 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libgpkrylov_cuda.so")
+LIB_PATH = os.environ.get("GPK_LIB_PATH") or os.path.join(_HERE, "lib", "libgpkrylov_cuda.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "gpkrylov_cuda.h")
 
 GPK_OK, GPK_INPUT_ERROR, GPK_NUMERICAL_ERROR, GPK_SOLVER_ERROR, GPK_CUDA_ERROR, GPK_NCCL_ERROR = range(6)
 GPK_RBF, GPK_MATERN12, GPK_MATERN32, GPK_MATERN52, GPK_RATQUAD = range(5)
 GPK_PREC_FP64, GPK_PREC_FP32, GPK_PREC_TF32X3 = 0, 1, 2
+GPK_MVM_AUTO, GPK_MVM_DIRECT, GPK_MVM_GRAM = 0, 1, 2
 
 
 class gpk_cg_cfg(C.Structure):
@@ -72,6 +73,8 @@ SIGNATURES = {
                                           C.POINTER(gpk_mll_result)]),
     "gpk_make_probes": (C.c_int, [C.c_int64, C.c_int, C.c_uint64, _D]),
     "gpk_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "gpk_set_mvm_variant": (C.c_int, [_V, C.c_int]),
+    "gpk_get_mvm_variant": (C.c_int, [_V, _I, _D]),
     "gpk_launch_count": (C.c_longlong, [_V]),
     "gpk_stream": (_V, [_V]),
     "gpk_profile_enable": (C.c_int, [_V, C.c_int]),

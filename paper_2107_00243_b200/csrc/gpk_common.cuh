@@ -39,6 +39,21 @@ GPK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// As mbar_wait, but a thread whose phase is not complete is suspended (woken by
+// the phase completion, hint 1 ms) instead of spinning: keeps the single-thread
+// TMA / MMA issuers from stealing issue slots from the math warps.
+GPK_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 // Bulk global -> shared copy; bytes multiple of 16, both addresses 16B aligned.
 GPK_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile(

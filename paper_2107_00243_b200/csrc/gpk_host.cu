@@ -414,6 +414,16 @@ struct gpk_ctx {
     const int v = e ? std::atoi(e) : 2;
     return v >= 1 && v <= 8 ? v : 2;
   }();
+  // Gram-variant tensor-core MVM (gpk_mvm_tcg.cuh): packed centred coordinates + norms
+  int mvm_variant = [] {  // GPK_MVM_AUTO / DIRECT / GRAM (env GPK_MVM_VARIANT, default auto)
+    const char* e = std::getenv("GPK_MVM_VARIANT");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 0 && v <= 2 ? v : 0;
+  }();
+  bool gram_ok = false;   // the value MVMs of the tf32x3 path use the Gram kernel
+  float gram_maxnorm = 0.0f;
+  DBuf<float> Xgh, Xgl, Xgn;
+  DBuf<double> Xgmu;
   DBuf<double> w_v64, w_f64;
   DBuf<gpk::SlotState> w_ss[2];
   DBuf<int> w_map;
@@ -528,8 +538,28 @@ struct gpk_ctx {
     check_launch(gpk::launch_pack_x(X.p, n, n, d, n_pad, ls_dev.p, gpk::prescale_c(family), dp, X32.p, dp, X64s.p,
                                     sx.p, sq.p, st),
                  1, "pack_x");
+    gram_ok = false;
+    // Gram variant: RBF / Matern-3/2 / Matern-5/2, d <= 32, and centred pre-scaled
+    // coordinates small enough that the expanded-distance cancellation stays at the
+    // fp32 level (max |x~|^2 <= kGramMaxNorm; see gpk_mvm_tcg.cuh).
+    if (mvm_variant != GPK_MVM_DIRECT && family != gpk::kMatern12 && d <= 32) {
+      Xgh.ensure(static_cast<size_t>(n_pad) * 32);
+      Xgl.ensure(static_cast<size_t>(n_pad) * 32);
+      Xgn.ensure(n_pad);
+      Xgmu.ensure(d);
+      check_launch(gpk::launch_gram_pack(X.p, n, n, d, n_pad, ls_dev.p, gpk::prescale_c(family), Xgmu.p, Xgh.p, Xgl.p,
+                                         Xgn.p, st),
+                   2, "gram_pack");
+      std::vector<float> nr(n);
+      d2h(nr.data(), Xgn.p, sizeof(float) * n);
+      gram_maxnorm = 0.0f;
+      for (float v : nr) gram_maxnorm = std::max(gram_maxnorm, v);
+      gram_ok = mvm_variant == GPK_MVM_GRAM || (gram_maxnorm <= kGramMaxNorm && d >= kGramMinDim);
+    }
     packed = true;
   }
+  static constexpr float kGramMaxNorm = 320.0f;
+  static constexpr int kGramMinDim = 6;  // below, direct differences cost about as much as the Gram path
 
   // split-K factor: a function of n only (so a column's summation order never
   // depends on t), chosen so the grid fills whole waves of 2 x 148 CTA slots
@@ -588,22 +618,25 @@ struct gpk_ctx {
         a.jtiles_per_split = per;
         a.scale = o2;
         a.flush = tc_flush;
+        a.dp = dp;
         a.row_begin = r0;
         a.row_end = r1;
         const int cf[] = {2, 3, 6, 9};
         const double fl = static_cast<double>(nl) * n * (2.0 * tc + 3.0 * d + cf[family]);
         auto ev = prof_begin(0);
+        auto launch = [&](double* o, int sp) {
+          return gram_ok ? gpk::launch_fused_kmvm_tcg(family, d, Xgh.p, Xgl.p, Xgn.p, X32.p, w_vhi.p, w_vlo.p, o, a, sp, st)
+                         : gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, o, a, sp, st);
+        };
         if (splits == 1) {
           a.ldo = ldo;
-          check_launch(gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, out + c0 * ldo, a, 1, st), 1,
-                       "fused_kmvm_tc");
+          check_launch(launch(out + c0 * ldo, 1), 1, "fused_kmvm_tc");
           prof_end(0, ev, fl, static_cast<double>(nl) * n);
         } else {
           a.ldo = ldp;
           a.split_stride = static_cast<long long>(tc) * ldp;
           w_y.ensure(static_cast<size_t>(splits) * tc * ldp);
-          check_launch(gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, w_y.p, a, splits, st), 1,
-                       "fused_kmvm_tc");
+          check_launch(launch(w_y.p, splits), 1, "fused_kmvm_tc");
           prof_end(0, ev, fl, static_cast<double>(nl) * n);
           check_launch(
               gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, nl, ldp, out + c0 * ldo, ldo, st), 1,
@@ -1489,6 +1522,21 @@ void gpk_destroy(gpk_ctx* ctx) {
 const char* gpk_last_error(const gpk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 long long gpk_launch_count(const gpk_ctx* ctx) { return ctx ? ctx->launches : 0; }
 void* gpk_stream(const gpk_ctx* ctx) { return ctx ? static_cast<void*>(ctx->st) : nullptr; }
+
+gpk_status gpk_set_mvm_variant(gpk_ctx* ctx, int variant) {
+  return guard(ctx, [&] {
+    require(variant >= GPK_MVM_AUTO && variant <= GPK_MVM_GRAM, "gpk_set_mvm_variant: unknown variant");
+    ctx->mvm_variant = variant;
+    ctx->packed = false;
+  });
+}
+gpk_status gpk_get_mvm_variant(gpk_ctx* ctx, int* variant, double* max_sqnorm) {
+  return guard(ctx, [&] {
+    ctx->require_ready();
+    if (variant) *variant = ctx->gram_ok ? GPK_MVM_GRAM : GPK_MVM_DIRECT;
+    if (max_sqnorm) *max_sqnorm = ctx->gram_maxnorm;
+  });
+}
 
 gpk_status gpk_profile_enable(gpk_ctx* ctx, int on) {
   return guard(ctx, [&] { ctx->prof_on = on != 0; });

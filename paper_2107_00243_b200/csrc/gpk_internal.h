@@ -20,6 +20,7 @@ struct MvmArgs {
   int flush;                 // tcgen05 path: j-tiles per TMEM accumulation group (fp64 drain period)
   int row_begin;             // first output row of this rank's shard (multiple of 128)
   int row_end;               // one past the last output row; outputs are stored at row - row_begin
+  int dp;                    // padded coordinate count of the packed fp32 rows (Gram guard path)
 };
 
 // Packed-operand geometry for a given column count.
@@ -56,6 +57,16 @@ cudaError_t launch_pack_v_tc(const double* V, long long ldv, int t, int n, int n
                              float* vlo, cudaStream_t st);
 cudaError_t launch_fused_kmvm_tc(int family, int dp, const float* X, const float* vhi, const float* vlo, double* out,
                                  const MvmArgs& a, int splits, cudaStream_t st);
+
+// Gram variant (both contractions on tcgen05): squared distances from the expanded
+// form with the cross term in 3xTF32.  Packs X / l - mean, pre-scaled, as tf32 hi/lo
+// 32x32 swizzled tiles (xh, xl: n_pad x 32 floats) and fp32 norms xn (n_pad); mu: d
+// doubles of scratch.  RBF / Matern-3/2 / Matern-5/2, d <= 32.
+cudaError_t launch_gram_pack(const double* X, long long ldx, int n, int d, int n_pad, const double* ls,
+                             double prescale, double* mu, float* xh, float* xl, float* xn, cudaStream_t st);
+cudaError_t launch_fused_kmvm_tcg(int family, int d, const float* xh, const float* xl, const float* xn,
+                                  const float* x32, const float* vhi, const float* vlo, double* out, const MvmArgs& a, int splits,
+                                  cudaStream_t st);
 
 // Reference-formula kernel column (kernels.hpp:235-243) / derivative column (:252-267), fp64.
 // which < 0: K[:, p];  which == 0: outputscale;  1..d: lengthscale which-1.

@@ -72,21 +72,12 @@ GPK_DEV float to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-// paired fp32 (sm_100 FADD2 / FFMA2): two lanes of work per issue slot
-typedef unsigned long long f32x2;
-GPK_DEV f32x2 f2_sub(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-GPK_DEV f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-GPK_DEV float f2_hsum(f32x2 a) {
-  return __uint_as_float(static_cast<uint32_t>(a)) + __uint_as_float(static_cast<uint32_t>(a >> 32));
-}
+// paired fp32 (sm_100 FADD2 / FFMA2): two lanes of work per issue slot.  The
+// intrinsics are required: inline-asm f32x2 on 64-bit registers is split by
+// ptxas into scalar FADD/FFMA.
+GPK_DEV float2 f2_sub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+GPK_DEV float2 f2_fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+GPK_DEV float f2_hsum(float2 a) { return a.x + a.y; }
 // round-to-nearest (ties away) to tf32 with integer ALU ops instead of the
 // quarter-rate conversion unit (finite inputs)
 GPK_DEV float to_tf32_alu(float x) {
@@ -188,8 +179,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int it = 0; it < nt; ++it) {
         const int s = it % S;
         const uint32_t par = ((it / S) & 1) ^ 1;
-        mbar_wait(&x_empty[s], par);
-        mbar_wait(&v_empty[s], par);
+        mbar_wait_sleep(&x_empty[s], par);
+        mbar_wait_sleep(&v_empty[s], par);
         const long long jt = jt0 + it;
         mbar_arrive_expect_tx(&xv_full[s], XTILE + 2 * VTILE);
         bulk_g2s(sbase + (sX - base) + s * XTILE, X + jt * BK * DP, XTILE, &xv_full[s]);
@@ -204,9 +195,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int it = 0; it < nt; ++it) {
         const int s = it % S, as = it % AS;
         const int g = it / F, buf = g & 1;
-        if (it % F == 0) mbar_wait(&acc_empty[buf], ((g >> 1) & 1) ^ 1);
-        mbar_wait(&a_full[as], (it / AS) & 1);
-        mbar_wait(&xv_full[s], (it / S) & 1);
+        if (it % F == 0) mbar_wait_sleep(&acc_empty[buf], ((g >> 1) & 1) ^ 1);
+        mbar_wait_sleep(&a_full[as], (it / AS) & 1);
+        mbar_wait_sleep(&xv_full[s], (it / S) & 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * NPAD;
         const uint32_t ahi = sA + (as * 2 + 0) * ATILE, alo = sA + (as * 2 + 1) * ATILE;
@@ -233,12 +224,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = pw >> 2;             // quarter: j-range and column-chunk subset
     const int r = lg * 32 + lane;      // row within the tile == TMEM lane
     const int row = row0 + r;
-    f32x2 xr[DP / 2];  // this row's coordinates, packed in pairs
+    float2 xr[DP / 2];  // this row's coordinates, packed in pairs
 #pragma unroll
     for (int k = 0; k < DP / 4; ++k) {
-      const ulonglong2 v = reinterpret_cast<const ulonglong2*>(X + static_cast<long long>(row) * DP)[k];
-      xr[2 * k] = v.x;
-      xr[2 * k + 1] = v.y;
+      const float4 v = reinterpret_cast<const float4*>(X + static_cast<long long>(row) * DP)[k];
+      xr[2 * k] = make_float2(v.x, v.y);
+      xr[2 * k + 1] = make_float2(v.z, v.w);
     }
     double acc64[HC * 8];
 #pragma unroll
@@ -246,7 +237,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // column chunks drained by this thread: c8 = q, q + RPT, ...
     auto drain = [&](int g) {
       const int buf = g & 1;
-      mbar_wait(&acc_full[buf], (g >> 1) & 1);
+      mbar_wait_sleep(&acc_full[buf], (g >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int h = 0; h < HC; ++h) {
@@ -265,8 +256,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     };
     for (int it = 0; it < nt; ++it) {
       const int s = it % S, as = it % AS;
-      mbar_wait(&xv_full[s], (it / S) & 1);
-      mbar_wait(&a_empty[as], ((it / AS) & 1) ^ 1);
+      mbar_wait_sleep(&xv_full[s], (it / S) & 1);
+      mbar_wait_sleep(&a_empty[as], ((it / AS) & 1) ^ 1);
       const float* xs = Xs + s * (BK * DP);
       const uint32_t ahi = sA + (as * 2 + 0) * ATILE, alo = sA + (as * 2 + 1) * ATILE;
 #pragma unroll
@@ -275,12 +266,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = q * JPT + c4 * 4 + u;
-          const ulonglong2* xj = reinterpret_cast<const ulonglong2*>(xs + j * DP);
-          f32x2 a0 = 0ull, a1 = 0ull;  // four partial sums of squared differences
+          const float4* xj = reinterpret_cast<const float4*>(xs + j * DP);
+          float2 a0 = make_float2(0.f, 0.f), a1 = a0;  // four partial sums of squared differences
 #pragma unroll
           for (int k = 0; k < DP / 4; ++k) {
-            const ulonglong2 v = xj[k];
-            const f32x2 d0 = f2_sub(xr[2 * k], v.x), d1 = f2_sub(xr[2 * k + 1], v.y);
+            const float4 v = xj[k];
+            const float2 d0 = f2_sub(xr[2 * k], make_float2(v.x, v.y));
+            const float2 d1 = f2_sub(xr[2 * k + 1], make_float2(v.z, v.w));
             a0 = f2_fma(d0, d0, a0);
             a1 = f2_fma(d1, d1, a1);
           }

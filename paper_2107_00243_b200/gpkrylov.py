@@ -238,6 +238,19 @@ class KernelOperator:
         self._set_params(params)
         return self
 
+    MVM_VARIANTS = {"auto": 0, "direct": 1, "gram": 2}
+
+    def set_mvm_variant(self, variant: str):
+        """Kernel-entry strategy of the tensor-core MVM (gpk_set_mvm_variant): "auto", "direct", "gram"."""
+        self.ctx.check(self.ctx.lib.gpk_set_mvm_variant(self.ctx.h, self.MVM_VARIANTS[variant]))
+        return self
+
+    def mvm_variant(self):
+        """(variant in use: "direct" | "gram", max squared norm of the centred pre-scaled coordinates)."""
+        v, m = C.c_int(), C.c_double()
+        self.ctx.check(self.ctx.lib.gpk_get_mvm_variant(self.ctx.h, C.byref(v), C.byref(m)))
+        return ("direct", "direct", "gram")[v.value], m.value
+
     def rows(self):
         return self._x.shape[0]
 

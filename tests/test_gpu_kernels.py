@@ -50,6 +50,43 @@ def test_mvm_fp32_matches_oracle(orc, fam, n, d, t, precision):
         assert rel(got[:, c], want[:, c]) < (5e-6 if precision == "fp32" else 1e-5)
 
 
+@pytest.mark.parametrize("fam", ["rbf", "matern32", "matern52"])
+@pytest.mark.parametrize("n,d,t", [(1000, 3, 9), (2051, 9, 51), (700, 18, 65), (300, 32, 130), (129, 1, 1),
+                                   (4100, 11, 8)])
+@pytest.mark.parametrize("variant", ["direct", "gram"])
+def test_mvm_tc_variants_match_oracle(orc, fam, n, d, t, variant):
+    # both kernel-entry strategies of the tensor-core MVM: fp32 direct differences, and
+    # the expanded form with the cross term on the tensor cores (gpk_mvm_tcg.cuh)
+    x = orc.random_matrix(n, d, 300 + n)
+    p = orc.Params(d, 1.0, 0.8 * math.sqrt(d), 0.01)
+    v = orc.random_matrix(n, t, 11)
+    want = orc.kernel_apply(orc.FAMILIES[fam], x, p, v)
+    op = op_for(orc, fam, x, p).set_mvm_variant(variant)
+    got = op.apply(v, precision="tf32x3")
+    assert op.mvm_variant()[0] == variant
+    assert rel(got, want) < 3e-6
+    for c in range(t):
+        assert rel(got[:, c], want[:, c]) < 1e-5
+
+
+def test_mvm_variant_auto_selection(orc):
+    # auto: Gram for moderate coordinate norms, direct differences for large ones and Matern-1/2
+    x = orc.random_matrix(2000, 18, 41)
+    small = op_for(orc, "matern32", x, orc.Params(18, 1.0, 2.0, 0.01))
+    assert small.mvm_variant()[0] == "gram"
+    big = op_for(orc, "matern32", 100.0 * x, orc.Params(18, 1.0, 2.0, 0.01))
+    assert big.mvm_variant()[0] == "direct"
+    m12 = op_for(orc, "matern12", x, orc.Params(18, 1.0, 2.0, 0.01)).set_mvm_variant("gram")
+    assert m12.mvm_variant()[0] == "direct"
+    # clustered near-duplicate points (C4-like): Gram stays accurate near s = 0 where forced
+    xc = np.repeat(orc.random_matrix(64, 3, 42), 20, axis=0) + 1e-3 * orc.random_matrix(1280, 3, 43)
+    p = orc.Params(3, 1.0, 0.3, 0.01)
+    v = orc.random_matrix(1280, 5, 44)
+    want = orc.kernel_apply(orc.FAMILIES["matern52"], xc, p, v)
+    op = op_for(orc, "matern52", xc, p).set_mvm_variant("gram")
+    assert rel(op.apply(v, precision="tf32x3"), want) < 3e-6
+
+
 @pytest.mark.parametrize("fam", FAMS)
 @pytest.mark.parametrize("precision,tol", [("fp64", 1e-11), ("fp32", 5e-6)])
 def test_deriv_mvm_matches_oracle(orc, fam, precision, tol):

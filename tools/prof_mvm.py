@@ -1,4 +1,4 @@
-"""Standalone fused-MVM driver for ncu / timing: python tools/prof_mvm.py [n d t family precision reps]."""
+"""Standalone fused-MVM driver for ncu / timing: python tools/prof_mvm.py [n d t family precision reps variant]."""
 import os
 import sys
 import time
@@ -18,12 +18,16 @@ rng = np.random.default_rng(0)
 x = rng.standard_normal((n, d))
 v = rng.standard_normal((n, t))
 op = gk.KernelOperator(gk.KernelSpec(fam), x, gk.Hyperparameters.from_raw(d, 1.0, 2.0, 0.01))
+if len(sys.argv) > 7:
+    op.set_mvm_variant(sys.argv[7])  # auto | direct | gram
 lib = op.ctx.lib
 import ctypes as C
+for r in range(2):  # warm-up: module load, workspace allocation
+    op.apply(v, precision=prec)
 lib.gpk_profile_enable(op.ctx.h, 1)
 for r in range(reps):
     op.apply(v, precision=prec)
 ms, cnt, fl, en = C.c_double(), C.c_longlong(), C.c_double(), C.c_double()
 lib.gpk_profile_read(op.ctx.h, 0, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en))
-print(f"n={n} d={d} t={t} {fam} {prec}: {ms.value/cnt.value:.3f} ms/launch, {fl.value/ms.value*1e3/1e12:.2f} TFLOP/s "
+print(f"[{op.mvm_variant()[0]}] n={n} d={d} t={t} {fam} {prec}: {ms.value/cnt.value:.3f} ms/launch, {fl.value/ms.value*1e3/1e12:.2f} TFLOP/s "
       f"({en.value/ms.value*1e3/1e9:.1f} G entries/s) over {cnt.value} launches")
