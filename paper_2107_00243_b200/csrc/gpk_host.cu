@@ -424,6 +424,9 @@ struct gpk_ctx {
   float gram_maxnorm = 0.0f;
   DBuf<float> Xgh, Xgl, Xgn;
   DBuf<double> Xgmu;
+  DBuf<uint16_t> w_h16hi, w_h16lo;  // fp16 V tiles of the Gram variant
+  DBuf<float> w_vsig;
+  DBuf<double> w_colscale;
   DBuf<double> w_v64, w_f64;
   DBuf<gpk::SlotState> w_ss[2];
   DBuf<int> w_map;
@@ -604,43 +607,61 @@ struct gpk_ctx {
     const int per = (ntiles + splits - 1) / splits;
     const long long ldp = (nl + 127) / 128 * 128;  // split-K partial leading dimension (local rows)
     if (!fp64 && use_tc && which < 0) {  // tcgen05 path (value mode)
-      for (int c0 = 0; c0 < t; c0 += 128) {
-        const int tc = std::min(128, t - c0);
-        const int npad = gpk::tc_npad(tc);
-        w_vhi.ensure(static_cast<size_t>(n_pad) * npad);
-        w_vlo.ensure(static_cast<size_t>(n_pad) * npad);
-        check_launch(gpk::launch_pack_v_tc(V + c0 * ldv, ldv, tc, n, n_pad, npad, w_vhi.p, w_vlo.p, st), 1,
-                     "pack_v_tc");
+      const int cmax = gram_ok ? 96 : 128;
+      for (int c0 = 0; c0 < t; c0 += cmax) {
+        const int tc = std::min(cmax, t - c0);
         gpk::MvmArgs a{};
         a.n = n;
         a.n_pad = n_pad;
         a.t = tc;
-        a.jtiles_per_split = per;
         a.scale = o2;
-        a.flush = tc_flush;
         a.dp = dp;
         a.row_begin = r0;
         a.row_end = r1;
+        int sp = splits;
+        if (gram_ok) {  // Gram variant: 64-wide j-tiles, fp16 V with per-column scales
+          const int npad = gpk::tcg_npad(tc);
+          w_h16hi.ensure(static_cast<size_t>(n_pad) * npad);
+          w_h16lo.ensure(static_cast<size_t>(n_pad) * npad);
+          w_vsig.ensure(tc);
+          w_colscale.ensure(tc);
+          check_launch(gpk::launch_pack_v_f16(V + c0 * ldv, ldv, tc, n, n_pad, npad, o2, w_vsig.p, w_colscale.p,
+                                              w_h16hi.p, w_h16lo.p, st),
+                       2, "pack_v_f16");
+          const int nt64 = n_pad / 64;
+          const int per64 = (nt64 + splits - 1) / splits;
+          sp = (nt64 + per64 - 1) / per64;
+          a.jtiles_per_split = per64;
+          a.flush = tc_flush;  // 64-wide tiles: 128 entries per fp32 TMEM accumulation at the default 2
+        } else {
+          const int npad = gpk::tc_npad(tc);
+          w_vhi.ensure(static_cast<size_t>(n_pad) * npad);
+          w_vlo.ensure(static_cast<size_t>(n_pad) * npad);
+          check_launch(gpk::launch_pack_v_tc(V + c0 * ldv, ldv, tc, n, n_pad, npad, w_vhi.p, w_vlo.p, st), 1,
+                       "pack_v_tc");
+          a.jtiles_per_split = per;
+          a.flush = tc_flush;
+        }
         const int cf[] = {2, 3, 6, 9};
         const double fl = static_cast<double>(nl) * n * (2.0 * tc + 3.0 * d + cf[family]);
         auto ev = prof_begin(0);
-        auto launch = [&](double* o, int sp) {
-          return gram_ok ? gpk::launch_fused_kmvm_tcg(family, d, Xgh.p, Xgl.p, Xgn.p, X32.p, w_vhi.p, w_vlo.p, o, a, sp, st)
-                         : gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, o, a, sp, st);
+        auto launch = [&](double* o, int nsp) {
+          return gram_ok ? gpk::launch_fused_kmvm_tcg(family, d, Xgh.p, Xgl.p, Xgn.p, X32.p, w_h16hi.p, w_h16lo.p,
+                                                      w_colscale.p, o, a, nsp, st)
+                         : gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, o, a, nsp, st);
         };
-        if (splits == 1) {
+        if (sp == 1) {
           a.ldo = ldo;
           check_launch(launch(out + c0 * ldo, 1), 1, "fused_kmvm_tc");
           prof_end(0, ev, fl, static_cast<double>(nl) * n);
         } else {
           a.ldo = ldp;
           a.split_stride = static_cast<long long>(tc) * ldp;
-          w_y.ensure(static_cast<size_t>(splits) * tc * ldp);
-          check_launch(launch(w_y.p, splits), 1, "fused_kmvm_tc");
+          w_y.ensure(static_cast<size_t>(sp) * tc * ldp);
+          check_launch(launch(w_y.p, sp), 1, "fused_kmvm_tc");
           prof_end(0, ev, fl, static_cast<double>(nl) * n);
-          check_launch(
-              gpk::launch_reduce_splits(w_y.p, splits, a.split_stride, tc, nl, ldp, out + c0 * ldo, ldo, st), 1,
-              "reduce_splits");
+          check_launch(gpk::launch_reduce_splits(w_y.p, sp, a.split_stride, tc, nl, ldp, out + c0 * ldo, ldo, st),
+                       1, "reduce_splits");
         }
         entries += static_cast<long long>(nl) * n;
         flops += static_cast<long long>(fl);

@@ -67,6 +67,22 @@ GPK_DEV float kval32(float s) {
     return fmaf(rr, fmaf(rr, 1.0f / 3.0f, 1.0f), 1.0f) * e;
   }
 }
+// C * kval32(s) with the constant folded into the shape polynomial (RBF: into the
+// ex2 argument when C is a power of two, passed as log2 C).
+template <int FAM, int LOG2C>
+GPK_DEV float kval32_scaled(float s) {
+  constexpr float C = static_cast<float>(1 << LOG2C);
+  if constexpr (FAM == kRBF) {
+    return ex2_approx(static_cast<float>(LOG2C) - s);
+  } else {
+    const float r = sqrt_approx(s);
+    const float e = ex2_approx(-r);
+    if constexpr (FAM == kMatern12) return C * e;
+    if constexpr (FAM == kMatern32) return fmaf(r, C * kLn2, C) * e;
+    const float rr = r * kLn2;  // Matern52
+    return fmaf(rr, fmaf(rr, C / 3.0f, C), C) * e;
+  }
+}
 // shape_ds (kernels.hpp:115-134) in pre-scaled units.
 template <int FAM>
 GPK_DEV float kds32(float s) {

@@ -7,8 +7,8 @@ namespace gpk {
 namespace tcg {
 template <int FAM>
 cudaError_t launch_tcg_fam(int ks, int nc8, const float* Xh, const float* Xl, const float* Xn, const float* X32,
-                           const float* Vhi,
-                           const float* Vlo, double* out, const MvmArgs& a, dim3 g, cudaStream_t st);
+                           const __half* Vhi, const __half* Vlo, const double* colscale, double* out,
+                           const MvmArgs& a, dim3 g, cudaStream_t st);
 }
 
 // mu[k] = mean_i X[i, k] / l_k (fixed-order block reduction, one block per coordinate)
@@ -59,18 +59,81 @@ cudaError_t launch_gram_pack(const double* X, long long ldx, int n, int d, int n
   return cudaGetLastError();
 }
 
+int tcg_npad(int t) {
+  static const int set[] = {1, 2, 4, 6, 7, 8, 9, 10, 12};
+  const int need = (t + 7) / 8;
+  for (int v : set)
+    if (v >= need) return 8 * v;
+  return -1;
+}
+
+// per column c < t: sigma_c = 2^(14 - e), max |V[:, c]| = m 2^e (m in [0.5, 1)), so
+// |V sigma| < 2^14 and both fp16 halves stay in range; colscale_c = scale / (2^10 sigma_c)
+__global__ void vscale_kernel(const double* __restrict__ V, long long ldv, int n, double scale,
+                              float* __restrict__ sig, double* __restrict__ colscale) {
+  __shared__ double red[256];
+  const int c = blockIdx.x;
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(V[c * ldv + i]));
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int e = 0;
+    if (red[0] > 0.0) frexp(red[0], &e);
+    const double sg = ldexp(1.0, 14 - e);
+    sig[c] = static_cast<float>(sg);
+    colscale[c] = scale / (1024.0 * sg);
+  }
+}
+
+// V (fp64, column-major) -> per 64-row j-tile, NPAD x 64 fp16 hi / lo tiles of V sigma
+// in the 128B-swizzled K-major UMMA layout.
+__global__ void pack_v_f16_kernel(const double* __restrict__ V, long long ldv, int t, int n, int n_pad, int npad,
+                                  const float* __restrict__ sig, __half* __restrict__ vhi,
+                                  __half* __restrict__ vlo) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long total = static_cast<long long>(n_pad) * npad;
+  if (idx >= total) return;
+  const int j = static_cast<int>(idx & 63);
+  const long long rest = idx >> 6;
+  const int c = static_cast<int>(rest % npad);
+  const long long jt = rest / npad;
+  const long long i = jt * 64 + j;
+  const float v = (c < t && i < n) ? static_cast<float>(V[c * ldv + i] * sig[c]) : 0.0f;
+  const __half hi = __float2half_rn(v);
+  const __half lo = __float2half_rn(v - __half2float(hi));
+  const long long off = jt * npad * 64 + (c >> 3) * 512 + (c & 7) * 64 + (((j >> 3) ^ (c & 7)) << 3) + (j & 7);
+  vhi[off] = hi;
+  vlo[off] = lo;
+}
+
+cudaError_t launch_pack_v_f16(const double* V, long long ldv, int t, int n, int n_pad, int npad, double scale,
+                              float* sig, double* colscale, void* vhi, void* vlo, cudaStream_t st) {
+  vscale_kernel<<<t, 256, 0, st>>>(V, ldv, n, scale, sig, colscale);
+  const long long total = static_cast<long long>(n_pad) * npad;
+  pack_v_f16_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+      V, ldv, t, n, n_pad, npad, sig, static_cast<__half*>(vhi), static_cast<__half*>(vlo));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fused_kmvm_tcg(int family, int d, const float* xh, const float* xl, const float* xn,
-                                  const float* x32, const float* vhi, const float* vlo, double* out, const MvmArgs& a, int splits,
-                                  cudaStream_t st) {
-  const int npad = tc_npad(a.t);
+                                  const float* x32, const void* vhi, const void* vlo, const double* colscale,
+                                  double* out, const MvmArgs& a, int splits, cudaStream_t st) {
+  const int npad = tcg_npad(a.t);
   if (npad < 0 || d < 1 || d > 32) return cudaErrorInvalidValue;
   const int ks = (d + 7) / 8;
-  dim3 g((a.row_end - a.row_begin + tc::BM - 1) / tc::BM, splits);
+  dim3 g((a.row_end - a.row_begin + tcg::BM - 1) / tcg::BM, splits);
   const int nc8 = npad / 8;
+  const __half* h = static_cast<const __half*>(vhi);
+  const __half* l = static_cast<const __half*>(vlo);
   switch (family) {
-    case kRBF: return tcg::launch_tcg_fam<kRBF>(ks, nc8, xh, xl, xn, x32, vhi, vlo, out, a, g, st);
-    case kMatern32: return tcg::launch_tcg_fam<kMatern32>(ks, nc8, xh, xl, xn, x32, vhi, vlo, out, a, g, st);
-    case kMatern52: return tcg::launch_tcg_fam<kMatern52>(ks, nc8, xh, xl, xn, x32, vhi, vlo, out, a, g, st);
+    case kRBF: return tcg::launch_tcg_fam<kRBF>(ks, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
+    case kMatern32: return tcg::launch_tcg_fam<kMatern32>(ks, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
+    case kMatern52: return tcg::launch_tcg_fam<kMatern52>(ks, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
   }
   return cudaErrorInvalidValue;  // Matern-1/2 stays on the direct-difference kernels
 }
