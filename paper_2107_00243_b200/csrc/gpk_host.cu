@@ -425,7 +425,7 @@ struct gpk_ctx {
   DBuf<float> Xgh, Xgl, Xgn;
   DBuf<double> Xgmu;
   DBuf<uint16_t> w_h16hi, w_h16lo;  // fp16 V tiles of the Gram variant
-  DBuf<float> w_vsig;
+  DBuf<unsigned long long> w_vmax;
   DBuf<double> w_colscale;
   DBuf<double> w_v64, w_f64;
   DBuf<gpk::SlotState> w_ss[2];
@@ -623,9 +623,9 @@ struct gpk_ctx {
           const int npad = gpk::tcg_npad(tc);
           w_h16hi.ensure(static_cast<size_t>(n_pad) * npad);
           w_h16lo.ensure(static_cast<size_t>(n_pad) * npad);
-          w_vsig.ensure(tc);
+          w_vmax.ensure(tc);
           w_colscale.ensure(tc);
-          check_launch(gpk::launch_pack_v_f16(V + c0 * ldv, ldv, tc, n, n_pad, npad, o2, w_vsig.p, w_colscale.p,
+          check_launch(gpk::launch_pack_v_f16(V + c0 * ldv, ldv, tc, n, n_pad, npad, o2, w_vmax.p, w_colscale.p,
                                               w_h16hi.p, w_h16lo.p, st),
                        2, "pack_v_f16");
           const int nt64 = n_pad / 64;
@@ -734,8 +734,8 @@ struct gpk_ctx {
     w_T.ensure(static_cast<size_t>(t) * ldn);
     check_launch(gpk::launch_g1(L.p + r0, n, k, R, ldn, t, nl, w_g1.p, w_W.p, k, st), 2, "g1");
     allreduce_sum(w_W.p, static_cast<long long>(k) * t);
-    check_launch(gpk::launch_g2(C.p + r0, n, k, w_W.p, k, t, nl, w_T.p, ldn, st), 1, "g2");
-    check_launch(gpk::launch_woodbury_finish(R, w_T.p, pnoise, nl, ldn, t, Z, st), 1, "woodbury");
+    check_launch(gpk::launch_woodbury_apply(C.p + r0, n, k, w_W.p, k, R, ldn, pnoise, t, nl, Z, ldn, st), 1,
+                 "woodbury");
   }
 
   // per-column dots a.b over all rows (host result, fixed-order reduction, rank-ordered sum)
@@ -991,6 +991,8 @@ struct gpk_ctx {
         }
       }
       *max_ratio = mr;
+      if (std::getenv("GPK_DEBUG_REFINE"))
+        std::fprintf(stderr, "[refine] pass %d: t=%d bad=%zu max_ratio=%.3e\n", pass, t, bad.size(), mr);
       if (bad.empty() || pass == passes) break;
       ++used;
       // correction solve K E = R[:, bad] with absolute target rel_tol * norm0

@@ -279,92 +279,111 @@ cudaError_t launch_woodbury_finish(const double* R, const double* T, double sig2
 }
 
 // ---------------------------------------------------------------------------
-// Skinny fp64 GEMMs for the Woodbury solve, Gram matrix and trace terms.
+// Skinny fp64 GEMMs for the Woodbury solve, Gram matrix and trace terms, on the
+// fp64 tensor cores (DMMA 8x8x4, mma.sync .f64):
 //   G1: W[s][kk] = sum_i A[kk][i] * B[s][i]     (A^T B, A: [ka][lda], B: [tb][ldb])
-//       per 4096-row chunk partials, then a fixed-order chunk reduction.
-//   G2: T[s][i]  = sum_kk A[kk][i] * W[s][kk]   (A W,  sequential kk order)
+//       per row-chunk partials (chunk = f(n) only), then a fixed-order chunk reduction.
+//   G2: T[s][i]  = sum_kk A[kk][i] * W[s][kk]   (A W), optionally fused with the
+//       Woodbury finish Z = R / s2 - T / s2.
+// Each warp owns one 8-row m-tile and eight 8-column n-tiles (64 columns) and walks
+// K in steps of 4 in a fixed order, so every output column is computed from its own
+// column of B / W only (the batched == independent contract) and runs are bitwise
+// reproducible.  Fragments come straight from global memory (L2-resident operands;
+// every 32-byte sector fully used).
 // ---------------------------------------------------------------------------
-constexpr int kG1T = 64;   // output tile 64 (ka) x 64 (tb), 4 x 4 per thread
-constexpr int kG1R = 16;   // rows per shared-memory sub-tile
+GPK_DEV void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
 
-// rows per chunk: a function of n only (~256 chunks), multiple of kG1R
+// rows per G1 chunk: a function of n only (~128 chunks), multiple of 16
 static int g1_chunk(int n) {
-  int ch = (n + 255) / 256;
-  ch = (ch + kG1R - 1) / kG1R * kG1R;
-  return ch < 128 ? 128 : ch;
+  int ch = (n + 127) / 128;
+  ch = (ch + 15) / 16 * 16;
+  return ch < 64 ? 64 : ch;
 }
 
 __global__ void __launch_bounds__(256) g1_kernel(const double* __restrict__ A, long long lda, int ka,
                                                  const double* __restrict__ B, long long ldb, int tb, int n, int ch,
                                                  double* __restrict__ part) {
-  __shared__ double As[kG1R][kG1T + 2];
-  __shared__ double Bs[kG1R][kG1T + 2];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = blockIdx.y * 8 + w;
+  if (mt * 8 >= ka) return;  // warp-uniform; no block-level synchronisation below
   const int chunk = blockIdx.x;
-  const int k0 = blockIdx.y * kG1T;
-  const int s0 = blockIdx.z * kG1T;
-  const int tx = threadIdx.x & 15;  // 4 consecutive kk
-  const int ty = threadIdx.x >> 4;  // 4 consecutive slots
-  double acc[4][4];
+  const int n0 = blockIdx.z * 64;
+  const int r = lane & 3, m = lane >> 2;
+  const int kk = mt * 8 + m;
+  const bool aval = kk < ka;
+  const double* acol = A + static_cast<long long>(aval ? kk : 0) * lda;
+  const double* bcol[8];
+  bool bval[8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int j = 0; j < 8; ++j) {
+    const int sj = n0 + 8 * j + m;
+    bval[j] = sj < tb;
+    bcol[j] = B + static_cast<long long>(bval[j] ? sj : 0) * ldb;
+  }
+  double acc[8][2];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int i0 = chunk * ch;
   const int i1 = min(n, i0 + ch);
-  for (int ib = i0; ib < i1; ib += kG1R) {
-    for (int e = threadIdx.x; e < kG1R * kG1T; e += blockDim.x) {
-      const int r = e % kG1R, c = e / kG1R;  // 16 consecutive rows of one column per half-warp
-      const int i = ib + r;
-      As[r][c] = (i < i1 && k0 + c < ka) ? A[static_cast<long long>(k0 + c) * lda + i] : 0.0;
-      Bs[r][c] = (i < i1 && s0 + c < tb) ? B[static_cast<long long>(s0 + c) * ldb + i] : 0.0;
+  for (int ib = i0; ib < i1; ib += 16) {  // 4 k-steps per round: loads first, then the DMMAs
+    double av[4], bv[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int row = ib + 4 * u + r;
+      const bool rv = row < i1;
+      av[u] = (aval && rv) ? acol[row] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bv[u][j] = (bval[j] && rv) ? bcol[j][row] : 0.0;
     }
-    __syncthreads();
-#pragma unroll 4
-    for (int r = 0; r < kG1R; ++r) {
-      double av[4], bv[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        av[q] = As[r][tx * 4 + q];
-        bv[q] = Bs[r][ty * 4 + q];
-      }
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-    }
-    __syncthreads();
+      for (int j = 0; j < 8; ++j) dmma884(acc[j], av[u], bv[u][j]);
   }
+  const int kko = mt * 8 + m;  // C fragment: row m, columns 2 r + e
+  if (kko < ka) {
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int kk = k0 + tx * 4 + a;
-    if (kk >= ka) continue;
+    for (int j = 0; j < 8; ++j)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int s = s0 + ty * 4 + b;
-      if (s < tb) part[(static_cast<long long>(chunk) * tb + s) * ka + kk] = acc[a][b];
-    }
+      for (int e = 0; e < 2; ++e) {
+        const int s = n0 + 8 * j + 2 * r + e;
+        if (s < tb) part[(static_cast<long long>(chunk) * tb + s) * ka + kko] = acc[j][e];
+      }
   }
 }
 
+// W[s][kk] = sum over chunks in fixed order: 4 threads per output (strided chunk
+// subsets, 8-deep batched loads), combined in fixed order through shared memory.
 __global__ void g1_reduce_kernel(const double* __restrict__ part, int nch, int ka, int tb, double* __restrict__ W,
                                  long long ldw) {
-  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= static_cast<long long>(ka) * tb) return;
-  const int s = static_cast<int>(idx / ka), kk = static_cast<int>(idx % ka);
+  __shared__ double red[4][64];
+  const int q = threadIdx.x >> 6, o = threadIdx.x & 63;
+  const long long idx = blockIdx.x * 64LL + o;
+  const long long tot = static_cast<long long>(ka) * tb;
   double acc = 0.0;
-  const double* p = part + static_cast<long long>(s) * ka + kk;
-  const long long stride = static_cast<long long>(tb) * ka;
-  // fixed chunk order; loads batched 8 deep (their addresses do not depend on the sum)
-  int c = 0;
-  for (; c + 8 <= nch; c += 8) {
-    double v[8];
+  if (idx < tot) {
+    const double* p = part + idx;
+    const long long stride = tot;
+    int c = q;
+    for (; c + 28 < nch; c += 32) {
+      double v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = p[(c + q) * stride];
+      for (int u = 0; u < 8; ++u) v[u] = p[(c + 4 * u) * stride];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc += v[q];
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; c < nch; c += 4) acc += p[c * stride];
   }
-  for (; c < nch; ++c) acc += p[c * stride];
-  W[s * ldw + kk] = acc;
+  red[q][o] = acc;
+  __syncthreads();
+  if (q == 0 && idx < tot) {
+    const int s = static_cast<int>(idx / ka), kk = static_cast<int>(idx % ka);
+    W[s * ldw + kk] = ((red[0][o] + red[1][o]) + red[2][o]) + red[3][o];
+  }
 }
 
 size_t g1_workspace(int n, int ka, int tb) {
@@ -377,52 +396,79 @@ cudaError_t launch_g1(const double* A, long long lda, int ka, const double* B, l
   if (ka <= 0 || tb <= 0) return cudaSuccess;
   const int ch = g1_chunk(n);
   const int nch = (n + ch - 1) / ch;
-  dim3 g(nch, (ka + kG1T - 1) / kG1T, (tb + kG1T - 1) / kG1T);
+  dim3 g(nch, (ka + 63) / 64, (tb + 63) / 64);
   g1_kernel<<<g, 256, 0, st>>>(A, lda, ka, B, ldb, tb, n, ch, part);
   const long long tot = static_cast<long long>(ka) * tb;
-  g1_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(part, nch, ka, tb, W, ldw);
+  g1_reduce_kernel<<<static_cast<unsigned>((tot + 63) / 64), 256, 0, st>>>(part, nch, ka, tb, W, ldw);
   return cudaGetLastError();
 }
 
-// G2: one thread per row, 16 slots per thread; W staged through shared memory.
-constexpr int kG2S = 16;
-constexpr int kG2K = 64;
-__global__ void g2_kernel(const double* __restrict__ A, long long lda, int ka, const double* __restrict__ W,
-                          long long ldw, int tb, int n, double* __restrict__ T, long long ldt) {
-  __shared__ double Ws[kG2K][kG2S];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int s0 = blockIdx.y * kG2S;
-  double acc[kG2S];
+// G2 (+ Woodbury finish): warp = 8 rows x 64 columns, K = ka in steps of 4 (fixed order).
+__global__ void __launch_bounds__(256) g2_kernel(const double* __restrict__ A, long long lda, int ka,
+                                                 const double* __restrict__ W, long long ldw, int tb, int n,
+                                                 double* __restrict__ T, long long ldt, const double* __restrict__ R,
+                                                 long long ldr, double sig2) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = (blockIdx.x * 8 + w) * 8;
+  if (i0 >= n) return;  // warp-uniform
+  const int n0 = blockIdx.y * 64;
+  const int r = lane & 3, m = lane >> 2;
+  const int row = i0 + m;
+  const bool rowv = row < n;
+  const double* arow = A + (rowv ? row : 0);
+  const double* wcol[8];
+  bool wval[8];
 #pragma unroll
-  for (int q = 0; q < kG2S; ++q) acc[q] = 0.0;
-  for (int k0 = 0; k0 < ka; k0 += kG2K) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kG2K * kG2S; e += blockDim.x) {
-      const int kk = e / kG2S, q = e % kG2S;
-      Ws[kk][q] = (k0 + kk < ka && s0 + q < tb) ? W[static_cast<long long>(s0 + q) * ldw + k0 + kk] : 0.0;
-    }
-    __syncthreads();
-    if (i < n) {
-      const int kmax = min(kG2K, ka - k0);
-      for (int kk = 0; kk < kmax; ++kk) {
-        const double av = A[static_cast<long long>(k0 + kk) * lda + i];
-#pragma unroll
-        for (int q = 0; q < kG2S; ++q) acc[q] += av * Ws[kk][q];
-      }
-    }
+  for (int j = 0; j < 8; ++j) {
+    const int sj = n0 + 8 * j + m;
+    wval[j] = sj < tb;
+    wcol[j] = W + static_cast<long long>(wval[j] ? sj : 0) * ldw;
   }
-  if (i < n) {
+  double acc[8][2];
 #pragma unroll
-    for (int q = 0; q < kG2S; ++q)
-      if (s0 + q < tb) T[static_cast<long long>(s0 + q) * ldt + i] = acc[q];
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int kb = 0; kb < ka; kb += 16) {
+    double av[4], bv[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int kr = kb + 4 * u + r;
+      const bool kv = kr < ka;
+      av[u] = (kv && rowv) ? arow[static_cast<long long>(kr) * lda] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bv[u][j] = (kv && wval[j]) ? wcol[j][kr] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dmma884(acc[j], av[u], bv[u][j]);
   }
+  if (!rowv) return;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int s = n0 + 8 * j + 2 * r + e;
+      if (s >= tb) continue;
+      const long long o = static_cast<long long>(s) * ldt + row;
+      if (R) T[o] = R[static_cast<long long>(s) * ldr + row] / sig2 - acc[j][e] / sig2;  // preconditioners.hpp:114-118
+      else T[o] = acc[j][e];
+    }
 }
 
 cudaError_t launch_g2(const double* A, long long lda, int ka, const double* W, long long ldw, int tb, int n,
                       double* T, long long ldt, cudaStream_t st) {
   if (tb <= 0) return cudaSuccess;
-  dim3 g((n + 127) / 128, (tb + kG2S - 1) / kG2S);
-  g2_kernel<<<g, 128, 0, st>>>(A, lda, ka, W, ldw, tb, n, T, ldt);
+  dim3 g((n + 63) / 64, (tb + 63) / 64);
+  g2_kernel<<<g, 256, 0, st>>>(A, lda, ka, W, ldw, tb, n, T, ldt, nullptr, 0, 1.0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_woodbury_apply(const double* C, long long ldc, int ka, const double* W, long long ldw,
+                                  const double* R, long long ldr, double sig2, int tb, int n, double* Z,
+                                  long long ldz, cudaStream_t st) {
+  if (tb <= 0) return cudaSuccess;
+  dim3 g((n + 63) / 64, (tb + 63) / 64);
+  g2_kernel<<<g, 256, 0, st>>>(C, ldc, ka, W, ldw, tb, n, Z, ldz, R, ldr, sig2);
   return cudaGetLastError();
 }
 

@@ -42,6 +42,10 @@ cudaError_t launch_g1(const double* A, long long lda, int ka, const double* B, l
                       double* part, double* W, long long ldw, cudaStream_t st);
 cudaError_t launch_g2(const double* A, long long lda, int ka, const double* W, long long ldw, int tb, int n,
                       double* T, long long ldt, cudaStream_t st);
+// Z = R / s2 - (C W) / s2 (G2 fused with the Woodbury finish, preconditioners.hpp:114-118)
+cudaError_t launch_woodbury_apply(const double* C, long long ldc, int ka, const double* W, long long ldw,
+                                  const double* R, long long ldr, double sig2, int tb, int n, double* Z,
+                                  long long ldz, cudaStream_t st);
 
 int pchol_blocks(int n);
 struct PivotState {

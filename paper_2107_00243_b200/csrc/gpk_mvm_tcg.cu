@@ -1,6 +1,8 @@
 // Front end of the Gram-variant tensor-core MVM (gpk_mvm_tcg.cuh): packing of
 // the centred, pre-scaled coordinates into tf32 hi/lo 128B-swizzled K-major
 // tiles plus their fp32 squared norms, and dispatch.
+#include <algorithm>
+
 #include "gpk_mvm_tcg.cuh"
 
 namespace gpk {
@@ -68,32 +70,30 @@ int tcg_npad(int t) {
 }
 
 // per column c < t: sigma_c = 2^(14 - e), max |V[:, c]| = m 2^e (m in [0.5, 1)), so
-// |V sigma| < 2^14 and both fp16 halves stay in range; colscale_c = scale / (2^10 sigma_c)
-__global__ void vscale_kernel(const double* __restrict__ V, long long ldv, int n, double scale,
-                              float* __restrict__ sig, double* __restrict__ colscale) {
-  __shared__ double red[256];
-  const int c = blockIdx.x;
+// |V sigma| < 2^14 and both fp16 halves stay in range; colscale_c = scale / (2^10 sigma_c).
+// Column maxima: 2-D grid of row chunks, integer atomicMax on the (non-negative) fp64 bit
+// patterns (order-independent, so deterministic); the pack kernel derives sigma from them.
+__global__ void vmax_kernel(const double* __restrict__ V, long long ldv, int n, unsigned long long* __restrict__ vmax) {
+  const int c = blockIdx.y;
   double m = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(V[c * ldv + i]));
-  red[threadIdx.x] = m;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    int e = 0;
-    if (red[0] > 0.0) frexp(red[0], &e);
-    const double sg = ldexp(1.0, 14 - e);
-    sig[c] = static_cast<float>(sg);
-    colscale[c] = scale / (1024.0 * sg);
-  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    m = fmax(m, fabs(V[c * ldv + i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(vmax + c, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+GPK_DEV double sigma_of(unsigned long long bits) {
+  const double m = __longlong_as_double(static_cast<long long>(bits));
+  int e = 0;
+  if (m > 0.0) frexp(m, &e);
+  return ldexp(1.0, 14 - e);
 }
 
 // V (fp64, column-major) -> per 64-row j-tile, NPAD x 64 fp16 hi / lo tiles of V sigma
 // in the 128B-swizzled K-major UMMA layout.
 __global__ void pack_v_f16_kernel(const double* __restrict__ V, long long ldv, int t, int n, int n_pad, int npad,
-                                  const float* __restrict__ sig, __half* __restrict__ vhi,
+                                  const unsigned long long* __restrict__ vmax, double scale,
+                                  double* __restrict__ colscale, __half* __restrict__ vhi,
                                   __half* __restrict__ vlo) {
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long total = static_cast<long long>(n_pad) * npad;
@@ -103,7 +103,9 @@ __global__ void pack_v_f16_kernel(const double* __restrict__ V, long long ldv, i
   const int c = static_cast<int>(rest % npad);
   const long long jt = rest / npad;
   const long long i = jt * 64 + j;
-  const float v = (c < t && i < n) ? static_cast<float>(V[c * ldv + i] * sig[c]) : 0.0f;
+  const double sg = c < t ? sigma_of(vmax[c]) : 1.0;
+  if (jt == 0 && j == 0 && c < t) colscale[c] = scale / (1024.0 * sg);
+  const float v = (c < t && i < n) ? static_cast<float>(V[c * ldv + i] * sg) : 0.0f;
   const __half hi = __float2half_rn(v);
   const __half lo = __float2half_rn(v - __half2float(hi));
   const long long off = jt * npad * 64 + (c >> 3) * 512 + (c & 7) * 64 + (((j >> 3) ^ (c & 7)) << 3) + (j & 7);
@@ -112,11 +114,15 @@ __global__ void pack_v_f16_kernel(const double* __restrict__ V, long long ldv, i
 }
 
 cudaError_t launch_pack_v_f16(const double* V, long long ldv, int t, int n, int n_pad, int npad, double scale,
-                              float* sig, double* colscale, void* vhi, void* vlo, cudaStream_t st) {
-  vscale_kernel<<<t, 256, 0, st>>>(V, ldv, n, scale, sig, colscale);
+                              void* vmax, double* colscale, void* vhi, void* vlo, cudaStream_t st) {
+  unsigned long long* vm = static_cast<unsigned long long*>(vmax);
+  cudaError_t e = cudaMemsetAsync(vm, 0, sizeof(unsigned long long) * t, st);
+  if (e != cudaSuccess) return e;
+  const int bx = std::min(16, (n + 1023) / 1024);
+  vmax_kernel<<<dim3(bx, t), 256, 0, st>>>(V, ldv, n, vm);
   const long long total = static_cast<long long>(n_pad) * npad;
   pack_v_f16_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-      V, ldv, t, n, n_pad, npad, sig, static_cast<__half*>(vhi), static_cast<__half*>(vlo));
+      V, ldv, t, n, n_pad, npad, vm, scale, colscale, static_cast<__half*>(vhi), static_cast<__half*>(vlo));
   return cudaGetLastError();
 }
 
