@@ -960,7 +960,11 @@ struct gpk_ctx {
   }
 
   // FP32 defect correction: audit the fp64 preconditioned true residual of
-  // every converged column and correct the ones above tolerance.
+  // every converged column and correct the ones above tolerance.  The fp64
+  // residual R = B - K_hat X is formed ONCE (fp64 fused MVM); after a correction
+  // X += E it is updated as R -= K_hat E with the solve's own (reduced-precision)
+  // operator: E is the small defect, so that product's relative error (<= ~5e-7)
+  // perturbs R by ~5e-7 |R|, far below the tolerance being certified.
   int refine(const double* B, long long ldb, int t, double* Xd, long long ldx, const CgOut& cg, int max_iters,
              double rel_tol, int passes, double* max_ratio) {
     w_tmp.ensure(static_cast<size_t>(t) * ldn);
@@ -968,14 +972,16 @@ struct gpk_ctx {
     w_B.ensure(static_cast<size_t>(t) * ldn);
     int used = 0;
     *max_ratio = 0.0;
-    for (int pass = 0; pass <= passes; ++pass) {
-      // R = B - (K X + s2 X)  in fp64
-      w_kx.ensure(static_cast<size_t>(t) * ldn);
-      apply_kernel(Xd, ldx, t, w_kx.p, ldn, true, -1);
-      check_launch(gpk::launch_gather_cols(Xd, ldx, nullptr, 1.0, nl, t, w_tmp2.p, ldn, st), 1, "copy");
+    // R = B - (K X + s2 X)  in fp64
+    w_kx.ensure(static_cast<size_t>(t) * ldn);
+    apply_kernel(Xd, ldx, t, w_kx.p, ldn, true, -1);
+    check_launch(gpk::launch_gather_cols(Xd, ldx, nullptr, 1.0, nl, t, w_tmp2.p, ldn, st), 1, "copy");
+    {
       dim3 g((nl + 255) / 256, t);
       residual_kernel<<<g, 256, 0, st>>>(B, ldb, w_kx.p, w_tmp2.p, noise, nl, ldn, w_B.p);
       check_launch(cudaGetLastError(), 1, "residual");
+    }
+    for (int pass = 0; pass <= passes; ++pass) {
       psolve(w_B.p, t, w_tmp.p);
       const std::vector<double> zz = col_dots(w_tmp.p, w_tmp.p, t, ldn);
       std::vector<int> bad;
@@ -997,9 +1003,10 @@ struct gpk_ctx {
       ++used;
       // correction solve K E = R[:, bad] with absolute target rel_tol * norm0
       const int nb = static_cast<int>(bad.size());
-      DBuf<double> Rb, Eb;
+      DBuf<double> Rb, Eb, KE;
       Rb.ensure(static_cast<size_t>(nb) * ldn);
       Eb.ensure(static_cast<size_t>(nb) * ldn);
+      KE.ensure(static_cast<size_t>(nb) * ldn);
       w_map.ensure(nb);
       h2d(w_map.p, bad.data(), sizeof(int) * nb);
       check_launch(gpk::launch_gather_cols(w_B.p, ldn, w_map.p, 1.0, nl, nb, Rb.p, ldn, st), 1, "gather");
@@ -1014,6 +1021,14 @@ struct gpk_ctx {
       check_launch(gpk::launch_gather_cols(Xd, ldx, w_map.p, 1.0, nl, nb, w_tmp2.p, ldn, st), 1, "gather");
       check_launch(gpk::launch_axpby(w_tmp2.p, Eb.p, 1.0, 1.0, nl, nb, ldn, st), 1, "axpy");
       check_launch(gpk::launch_scatter_cols(w_tmp2.p, ldn, w_map.p, nl, nb, Xd, ldx, st), 1, "scatter");
+      // R[:, bad] -= K E + s2 E  (reduced-precision product of the small correction)
+      apply_kernel(Eb.p, ldn, nb, KE.p, ldn, false, -1);
+      {
+        dim3 g((nl + 255) / 256, nb);
+        residual_kernel<<<g, 256, 0, st>>>(Rb.p, ldn, KE.p, Eb.p, noise, nl, ldn, w_tmp2.p);
+        check_launch(cudaGetLastError(), 1, "residual");
+      }
+      check_launch(gpk::launch_scatter_cols(w_tmp2.p, ldn, w_map.p, nl, nb, w_B.p, ldn, st), 1, "scatter");
       sync();
     }
     return used;
