@@ -55,6 +55,8 @@ constexpr int SG = 4;                     // X_j / V_j stages
 constexpr int AS = 2;                     // kernel-tile stages (TMEM)
 constexpr int MAX_NPAD = 96;
 constexpr uint32_t XG_TILE = BK * 32 * 4;  // 64 rows x 32 tf32 coordinates (hi or lo), 8 KB
+constexpr uint32_t XJ_TILE = BK * 32 * 4;  // 64 fp32 coordinate rows (dp <= 32 each), guard path
+constexpr uint32_t XI_BLOCK = BM * 32 * 4; // the CTA's 128 fp32 coordinate rows
 constexpr uint32_t T_GRAM = 0, T_AX = 128, T_AT = 192, T_ACC = 320;
 constexpr int kEntryLog2 = 10;             // entries scaled by 2^10: fp16 hi/lo stay normal
 constexpr float kGuard = 1.0f / 16.0f;     // cancellation guard (see the producer loop)
@@ -110,22 +112,6 @@ GPK_DEV uint32_t elect_one() {
   asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n}\n" : "=r"(pred));
   return pred;
 }
-// fp32 direct-difference squared distance of packed rows i, j (the guard path; kept
-// out of line so the rare branch does not cost registers in the main loop)
-static __device__ __noinline__ float direct_sqdist(const float* __restrict__ X32, int dp, int i, int j) {
-  const float4* xi = reinterpret_cast<const float4*>(X32 + static_cast<long long>(i) * dp);
-  const float4* xj = reinterpret_cast<const float4*>(X32 + static_cast<long long>(j) * dp);
-  float acc = 0.0f;
-  for (int k = 0; k < dp / 4; ++k) {
-    const float4 p = xi[k], q = xj[k];
-    const float d0 = p.x - q.x, d1 = p.y - q.y, d2 = p.z - q.z, d3 = p.w - q.w;
-    acc = fmaf(d0, d0, acc);
-    acc = fmaf(d1, d1, acc);
-    acc = fmaf(d2, d2, acc);
-    acc = fmaf(d3, d3, acc);
-  }
-  return acc;
-}
 GPK_DEV uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
 template <int FAM, int KS, int NC8>
@@ -149,7 +135,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t sV = sBx + SG * 2 * XG_TILE;
   const uint32_t sN = sV + SG * 2 * VTILE;
   const float* Ns = reinterpret_cast<const float*>(sbase + (sN - base));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (sN - base) + SG * BK * 4);
+  // fp32 coordinates for the cancellation guard: the j-tile rows per stage and the CTA's rows
+  const uint32_t sXJ = sN + SG * BK * 4;
+  const uint32_t sXI = sXJ + SG * XJ_TILE;
+  const float* XJs = reinterpret_cast<const float*>(sbase + (sXJ - base));
+  const float* XIs = reinterpret_cast<const float*>(sbase + (sXI - base));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (sXI - base) + XI_BLOCK);
   uint64_t* xv_full = bars;
   uint64_t* xv_empty = bars + SG;
   uint64_t* a_full = bars + 2 * SG;
@@ -159,7 +150,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* acc_full = g_full + 4;
   uint64_t* acc_empty = g_full + 6;
   uint64_t* ax_ready = g_full + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g_full + 9);
+  uint64_t* xi_full = g_full + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g_full + 10);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -186,6 +178,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&acc_empty[s], NPW);
     }
     mbar_init(ax_ready, NPW);
+    mbar_init(xi_full, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -201,12 +194,19 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer (converged warp, elected lane) ----------------
+    const uint32_t xjb = static_cast<uint32_t>(BK * a.dp * 4);
+    if (nt > 0 && elect_one()) {
+      mbar_arrive_expect_tx(xi_full, BM * a.dp * 4);
+      bulk_g2s(sbase + (sXI - base), X32 + static_cast<long long>(row0) * a.dp, BM * a.dp * 4, xi_full);
+    }
+    __syncwarp();
     for (int it = 0; it < nt; ++it) {
       const int s = it % SG;
       mbar_wait_sleep(&xv_empty[s], ((it / SG) & 1) ^ 1);
       if (elect_one()) {
         const long long jt = jt0 + it;
-        mbar_arrive_expect_tx(&xv_full[s], 2 * XG_TILE + BK * 4 + 2 * VTILE);
+        mbar_arrive_expect_tx(&xv_full[s], 2 * XG_TILE + BK * 4 + 2 * VTILE + xjb);
+        bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
         bulk_g2s(sbase + (sBx - base) + (s * 2 + 0) * XG_TILE, Xh + jt * (BK * 32), XG_TILE, &xv_full[s]);
         bulk_g2s(sbase + (sBx - base) + (s * 2 + 1) * XG_TILE, Xl + jt * (BK * 32), XG_TILE, &xv_full[s]);
         bulk_g2s(sbase + (sN - base) + s * BK * 4, Xn + jt * BK, BK * 4, &xv_full[s]);
@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     double acc64[HC * 8];
 #pragma unroll
     for (int e = 0; e < HC * 8; ++e) acc64[e] = 0.0;
+    if (nt > 0) mbar_wait_sleep(xi_full, 0);  // the CTA's fp32 rows (guard path)
     auto drain = [&](int g) {
       const int buf = g & 1;
       mbar_wait_sleep(&acc_full[buf], (g >> 1) & 1);
@@ -364,9 +365,24 @@ __global__ void __launch_bounds__(THREADS, 1)
         // coordinates, so the expanded form only serves pairs whose relative error in s
         // stays at the fp32 level.  Rare for the spread-out data auto mode selects.
         if (__any_sync(0xffffffffu, fminf(gmin.x, gmin.y) <= 0.0f)) {
+          // the whole warp evaluates the 8 direct distances (no divergence), from shared memory
+          const float4* xi4 = reinterpret_cast<const float4*>(XIs + r * a.dp);
+          const float4* xj4 = reinterpret_cast<const float4*>(XJs + s * (XJ_TILE / 4) + (q * JPT + hf8 * 8) * a.dp);
+          const int d4 = a.dp >> 2;
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (sv[u] <= kGuard * (nsj[u] + ni)) sv[u] = direct_sqdist(X32, a.dp, row, jb + hf8 * 8 + u);
+          for (int u = 0; u < 8; ++u) {
+            float acc = 0.0f;
+#pragma unroll 1
+            for (int k = 0; k < d4; ++k) {
+              const float4 p = xi4[k], qv = xj4[u * d4 + k];
+              const float d0 = p.x - qv.x, d1 = p.y - qv.y, d2 = p.z - qv.z, d3 = p.w - qv.w;
+              acc = fmaf(d0, d0, acc);
+              acc = fmaf(d1, d1, acc);
+              acc = fmaf(d2, d2, acc);
+              acc = fmaf(d3, d3, acc);
+            }
+            if (sv[u] <= kGuard * (nsj[u] + ni)) sv[u] = acc;
+          }
         }
         uint32_t eh[4], el[4];
 #pragma unroll
@@ -416,7 +432,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 template <int NC8>
 constexpr size_t tcg_smem_bytes() {
-  return 1024 + SG * 2 * XG_TILE + SG * 2 * (8 * NC8 * BK * 2) + SG * BK * 4 + (2 * SG + 2 * AS + 9) * 8 + 16;
+  return 1024 + SG * 2 * XG_TILE + SG * 2 * (8 * NC8 * BK * 2) + SG * BK * 4 + SG * XJ_TILE + XI_BLOCK +
+         (2 * SG + 2 * AS + 10) * 8 + 16;
 }
 
 template <int FAM, int KS, int NC8>
