@@ -588,6 +588,27 @@ struct gpk_ctx {
     return (ntiles + per - 1) / per;
   }
 
+  // split-K factor of the Gram tensor-core MVM (one 576-thread CTA per SM, 64-wide
+  // j-tiles): minimise waves x (tiles per CTA + per-CTA start-up, ~8 tiles); a
+  // function of n (and the shard's rows) only
+  int splits_for_tcg() const {
+    const int rb = (nl + 127) / 128;
+    const int nt64 = n_pad / 64;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int s = 1; s <= std::min(32, nt64); ++s) {
+      const int per = (nt64 + s - 1) / s;
+      const int se = (nt64 + per - 1) / per;
+      const double waves = std::ceil(static_cast<double>(rb) * se / 148.0);
+      const double cost = waves * (per + 8.0) + (se > 1 ? 0.02 * se * rb / 148.0 * per : 0.0);
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        best = se;
+      }
+    }
+    return best;
+  }
+
   // out[:, c] = op(V[:, c]) for c < t.  which < 0: K (noise-free, scaled o^2);
   // which == 0: dK/do; 1..d: dK/dl_j; d+1: identity (noise derivative).
   // V, out: this rank's rows (nl) of t columns; the direction block is all-gathered
@@ -629,7 +650,8 @@ struct gpk_ctx {
                                               w_h16hi.p, w_h16lo.p, st),
                        2, "pack_v_f16");
           const int nt64 = n_pad / 64;
-          const int per64 = (nt64 + splits - 1) / splits;
+          const int sg = splits_for_tcg();
+          const int per64 = (nt64 + sg - 1) / sg;
           sp = (nt64 + per64 - 1) / per64;
           a.jtiles_per_split = per64;
           a.flush = tc_flush;  // 64-wide tiles: 128 entries per fp32 TMEM accumulation at the default 2

@@ -490,7 +490,15 @@ __global__ void pchol_step_kernel(double* __restrict__ L, long long ldl, int s, 
   long long bi = 0x7fffffffffffffffLL;
   if (i < n) {
     double g = 0.0;
-    for (int c = 0; c < s; ++c) g = __dadd_rn(g, __dmul_rn(L[static_cast<long long>(c) * ldl + i], lp[c]));
+    int c = 0;
+    for (; c + 8 <= s; c += 8) {  // loads batched ahead of the (sequential, reference-order) sum
+      double v8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v8[u] = L[static_cast<long long>(c + u) * ldl + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) g = __dadd_rn(g, __dmul_rn(v8[u], lp[c + u]));
+    }
+    for (; c < s; ++c) g = __dadd_rn(g, __dmul_rn(L[static_cast<long long>(c) * ldl + i], lp[c]));
     const double v = __ddiv_rn(__dsub_rn(col[i], g), root);
     L[static_cast<long long>(s) * ldl + i] = v;
     const double dn = __dsub_rn(dg[i], __dmul_rn(v, v));
@@ -581,7 +589,8 @@ __global__ void argmax_blocks_kernel(const double* __restrict__ v, int n, double
   }
 }
 
-int pchol_blocks(int n) { return (n + kVT - 1) / kVT; }
+constexpr int kPB = 128;  // threads per pivoted-Cholesky step block (more CTAs per step)
+int pchol_blocks(int n) { return (n + kPB - 1) / kPB; }
 
 // ---------------------------------------------------------------------------
 // Device-resident pivot state: the whole factorisation is enqueued without host
@@ -606,7 +615,15 @@ __global__ void pchol_step_dev_kernel(double* __restrict__ L, long long ldl, int
   long long bi = 0x7fffffffffffffffLL;
   if (i < n) {
     double g = 0.0;
-    for (int c = 0; c < s; ++c) g = __dadd_rn(g, __dmul_rn(L[static_cast<long long>(c) * ldl + i], lp[c]));
+    int c = 0;
+    for (; c + 8 <= s; c += 8) {  // loads batched ahead of the (sequential, reference-order) sum
+      double v8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v8[u] = L[static_cast<long long>(c + u) * ldl + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) g = __dadd_rn(g, __dmul_rn(v8[u], lp[c + u]));
+    }
+    for (; c < s; ++c) g = __dadd_rn(g, __dmul_rn(L[static_cast<long long>(c) * ldl + i], lp[c]));
     const double v = __ddiv_rn(__dsub_rn(col[i], g), root);
     L[static_cast<long long>(s) * ldl + i] = v;
     const double dn = __dsub_rn(dg[i], __dmul_rn(v, v));
@@ -689,7 +706,7 @@ cudaError_t launch_pchol_dev(int family, const double* sx, const double* sq, int
   for (int s = 0; s < rank; ++s) {
     launch_pchol_column_dev(family, sx, sq, n, d, o2, ps, col, st);
     const size_t sm = sizeof(double) * static_cast<size_t>(s > 0 ? s : 1);
-    pchol_step_dev_kernel<<<nb, kVT, sm, st>>>(L, n, s, col, dg, n, ps, bval, bidx);
+    pchol_step_dev_kernel<<<nb, kPB, sm, st>>>(L, n, s, col, dg, n, ps, bval, bidx);
     pchol_next_kernel<<<1, kVT, 0, st>>>(bval, bidx, nb, s, kmax, diag_tol, ps, pivots);
   }
   return cudaGetLastError();
@@ -698,7 +715,7 @@ cudaError_t launch_pchol_dev(int family, const double* sx, const double* sq, int
 cudaError_t launch_argmax(const double* v, int n, double* bval, long long* bidx, double* out_val,
                           long long* out_idx, cudaStream_t st) {
   const int nb = pchol_blocks(n);
-  argmax_blocks_kernel<<<nb, kVT, 0, st>>>(v, n, bval, bidx);
+  argmax_blocks_kernel<<<nb, kPB, 0, st>>>(v, n, bval, bidx);
   argmax_finalize_kernel<<<1, kVT, 0, st>>>(bval, bidx, nb, out_val, out_idx);
   return cudaGetLastError();
 }
@@ -708,7 +725,7 @@ cudaError_t launch_pchol_step(double* L, long long ldl, int s, long long p, doub
                               cudaStream_t st) {
   const int nb = pchol_blocks(n);
   const size_t sm = sizeof(double) * static_cast<size_t>(s > 0 ? s : 1);
-  pchol_step_kernel<<<nb, kVT, sm, st>>>(L, ldl, s, p, root, col, dg, n, bval, bidx);
+  pchol_step_kernel<<<nb, kPB, sm, st>>>(L, ldl, s, p, root, col, dg, n, bval, bidx);
   argmax_finalize_kernel<<<1, kVT, 0, st>>>(bval, bidx, nb, out_val, out_idx);
   return cudaGetLastError();
 }
@@ -772,7 +789,12 @@ __global__ void dl_inblock_kernel(const double* __restrict__ L, long long ldl, d
     for (int c = 0; c < q; ++c) g2 = __dadd_rn(g2, __dmul_rn(L[static_cast<long long>(s0 + c) * ldl + i], dlp[c]));
     return __dsub_rn(__dsub_rn(dcw[i], g1), g2);
   };
-  if (threadIdx.x == 0) dd_sh = dc_at(p);
+  if (threadIdx.x == 0) {  // row p's value from the staged pivot rows (same operation order)
+    double g1 = 0.0, g2 = 0.0;
+    for (int c = 0; c < q; ++c) g1 = __dadd_rn(g1, __dmul_rn(dlp[c], lp[c]));
+    for (int c = 0; c < q; ++c) g2 = __dadd_rn(g2, __dmul_rn(lp[c], dlp[c]));
+    dd_sh = __dsub_rn(__dsub_rn(dcw[p], g1), g2);
+  }
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -787,7 +809,7 @@ __global__ void dl_inblock_kernel(const double* __restrict__ L, long long ldl, d
 cudaError_t launch_dl_inblock(const double* L, long long ldl, double* dL, long long wstride, int nw, int s0, int q,
                               long long p, const double* DC, long long dcw_stride, int n, cudaStream_t st) {
   dim3 g(pchol_blocks(n), nw);
-  dl_inblock_kernel<<<g, kVT, 0, st>>>(L, ldl, dL, wstride, s0, q, p, DC, dcw_stride, n);
+  dl_inblock_kernel<<<g, kPB, 0, st>>>(L, ldl, dL, wstride, s0, q, p, DC, dcw_stride, n);
   return cudaGetLastError();
 }
 
@@ -816,7 +838,7 @@ cudaError_t launch_dl_step(const double* L, long long ldl, double* dL, long long
                            const double* dcol, long long dcol_stride, int n, cudaStream_t st) {
   dim3 g(pchol_blocks(n), nw);
   const size_t sm = sizeof(double) * static_cast<size_t>(2 * (s > 0 ? s : 1));
-  dl_step_kernel<<<g, kVT, sm, st>>>(L, ldl, dL, wstride, s, p, dcol, dcol_stride, n);
+  dl_step_kernel<<<g, kPB, sm, st>>>(L, ldl, dL, wstride, s, p, dcol, dcol_stride, n);
   return cudaGetLastError();
 }
 

@@ -229,37 +229,36 @@ __global__ void pchol_column_dev_kernel(int f, const double* __restrict__ sx, co
 
 cudaError_t launch_pchol_column_dev(int f, const double* sx, const double* sq, int n, int d, double o2,
                                     const PivotState* ps, double* out, cudaStream_t st) {
-  pchol_column_dev_kernel<<<(n + 255) / 256, 256, 0, st>>>(f, sx, sq, n, d, o2, ps, out);
+  pchol_column_dev_kernel<<<(n + 63) / 64, 64, 0, st>>>(f, sx, sq, n, d, o2, ps, out);
   return cudaGetLastError();
 }
 
-// all derivative columns of pivot p at once (blockIdx.y = parameter w = 0..nw-1)
+// all derivative columns of pivot p at once: one thread per row evaluates the
+// distance and both shape values once and writes the nw = d + 1 columns
 __global__ void kernel_deriv_columns_kernel(int f, const double* __restrict__ sx, const double* __restrict__ x,
-                                            const double* __restrict__ sq, int n, int d, long long p,
+                                            const double* __restrict__ sq, int n, int d, long long p, int nw,
                                             const double* __restrict__ facs, double o2, double* __restrict__ out) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const int w = blockIdx.y;
   if (r >= n) return;
   double g = 0.0;
   for (int k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(sx[static_cast<long long>(k) * n + r], sx[k * n + p]));
   double s = __dsub_rn(__dadd_rn(sq[r], sq[p]), __dmul_rn(2.0, g));
   s = s > 0.0 ? s : 0.0;
-  double v;
-  if (w == 0) {
-    v = __dmul_rn(facs[0], __dmul_rn(o2, ref_shape(f, s)));
-  } else {
-    const int j = w - 1;
-    const double dx = __dsub_rn(x[static_cast<long long>(j) * n + r], x[static_cast<long long>(j) * n + p]);
-    v = __dmul_rn(facs[w], __dmul_rn(ref_shape_ds(f, s), __dmul_rn(dx, dx)));
+  out[r] = __dmul_rn(facs[0], __dmul_rn(o2, ref_shape(f, s)));
+  if (nw > 1) {
+    const double ds = ref_shape_ds(f, s);
+    for (int w = 1; w < nw; ++w) {
+      const int j = w - 1;
+      const double dx = __dsub_rn(x[static_cast<long long>(j) * n + r], x[static_cast<long long>(j) * n + p]);
+      out[static_cast<long long>(w) * n + r] = __dmul_rn(facs[w], __dmul_rn(ds, __dmul_rn(dx, dx)));
+    }
   }
-  out[static_cast<long long>(w) * n + r] = v;
 }
 
 cudaError_t launch_kernel_deriv_columns(int family, const double* sx, const double* x, const double* sq, int n, int d,
                                         long long p, int nw, const double* facs, double o2, double* out,
                                         cudaStream_t st) {
-  dim3 g((n + 255) / 256, nw);
-  kernel_deriv_columns_kernel<<<g, 256, 0, st>>>(family, sx, x, sq, n, d, p, facs, o2, out);
+  kernel_deriv_columns_kernel<<<(n + 127) / 128, 128, 0, st>>>(family, sx, x, sq, n, d, p, nw, facs, o2, out);
   return cudaGetLastError();
 }
 
