@@ -216,6 +216,9 @@ def run_ours(args, rank_env):
     check(lib.gpk_profile_read(ctx, 1, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en)))
     dc = {"ms": ms.value, "launches": cnt.value, "flops": fl.value}
     check(lib.gpk_profile_enable(ctx, 0))
+    var, maxnorm = C.c_int(), C.c_double()
+    check(lib.gpk_get_mvm_variant(ctx, C.byref(var), C.byref(maxnorm)))
+    mvm_variant = {1: "direct", 2: "gram"}.get(var.value, "direct")
     telemetry = {"value": res.value, "gradient": grad.tolist(), "logdet": res.logdet,
                  "solve_iterations": res.solve_iterations, "total_cg_iterations": res.total_cg_iterations,
                  "forward_cg_iterations_mean": float(np.mean(fi)), "refine_passes": res.refine_passes,
@@ -235,6 +238,7 @@ def run_ours(args, rank_env):
     h2d = X_h.numel() * 8 + y_h.numel() * 8 + Z_h.numel() * 8
     d2h = 8 * (d + 2) + 8 * l + 4 * l + 8 * 8
     return dict(times=times, e2e_times=e2e_times, launches=launches, mvm=mvm, dc=dc, clocks=clk.summary(),
+                mvm_variant=mvm_variant,
                 telemetry=telemetry, sweep=sweep, h2d=h2d, d2h=d2h, w=w)
 
 
@@ -360,34 +364,58 @@ def main():
     value = per_step / div
     e2e_value = e2e / div
     mvm = r["mvm"]
-    fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
     achieved = (mvm["flops"] / mvm["launches"]) / (mvm["ms"] / mvm["launches"] / 1e3) / 1e12 if mvm["launches"] else 0
     clk = r["clocks"]
     tc = args.precision == "tf32x3"
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak if fp32_peak else None, "traffic": None,
-                "kernel": ("fused_kmvm_tc_kernel (tcgen05 3xTF32 contraction, entries on CUDA cores)" if tc
-                           else "fused_kmvm_kernel (SIMT fp32)"),
-                "peak_source": f"north-star roofline: FP32 CUDA-core peak = 148 SM x 128 FMA/clk x 2 x sm_max_mhz "
-                               f"({peaks_src} MEASURED_PEAKS.json sm_max_mhz); achieved = algorithmic flops "
-                               f"n^2 (2t + 3d + c_fam) per launch / CUDA-event launch time",
-                "flops_per_launch": mvm["flops"] / max(mvm["launches"], 1),
-                "avg_launch_ms": mvm["ms"] / max(mvm["launches"], 1), "launches_per_step":
-                    mvm["launches"] / max(args.steps, 1),
-                "share_of_step": (mvm["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
-    if clk.get("sm_mhz"):
+    gram = tc and r["mvm_variant"] == "gram"
+    t_cols = w.probes + 1
+    npad = 8 * ((t_cols + 7) // 8)
+    ks = (w.d + 7) // 8
+    common = {"flops_per_launch": mvm["flops"] / max(mvm["launches"], 1),
+              "avg_launch_ms": mvm["ms"] / max(mvm["launches"], 1),
+              "launches_per_step": mvm["launches"] / max(args.steps, 1),
+              "share_of_step": (mvm["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
+    entries_per_s = w.n * w.n * mvm["launches"] / (mvm["ms"] / 1e3) if mvm["launches"] else 0.0
+    if tc:
+        # both contractions run on the 5th-gen tensor cores: the roofline is the measured dense
+        # tensor peak (MEASURED_PEAKS.json bf16, the f16 kind's rate); achieved = ALGORITHMIC flops
+        tpeak = float(peaks.get("bf16_tflops", 1656.1))
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
+                    "frac": achieved / tpeak, "traffic": None,
+                    "kernel": ("fused_kmvm_tcg_kernel (Gram distances 3xTF32 + 3xF16 contraction on tcgen05, "
+                               "kernel shape on the SFU)" if gram else
+                               "fused_kmvm_tc_kernel (3xTF32 contraction on tcgen05, entries on CUDA cores)"),
+                    "peak_source": f"{peaks_src} MEASURED_PEAKS.json bf16_tflops (dense, burst); achieved = "
+                                   f"algorithmic flops n^2 (2t + 3d + c_fam) per launch / CUDA-event launch time",
+                    **common}
+        if gram:
+            # hardware tensor work actually issued per entry: Gram 3 x 2 x 8 KS (tf32, half rate) and the
+            # contraction 3 x 2 x NPAD (f16)
+            hw_f16_equiv = 2 * (3 * 2 * 8 * ks) + 3 * 2 * npad
+            roofline["tensor_issued"] = {"f16_equiv_flops_per_entry": hw_f16_equiv,
+                                         "achieved": entries_per_s * hw_f16_equiv / 1e12,
+                                         "frac": entries_per_s * hw_f16_equiv / 1e12 / tpeak}
+            # the binding unit: the SFU evaluates the kernel shape (2 MUFU per entry; RBF 1) at 16/clk/SM
+            mufu = 1 if w.family == 0 else 2
+            sfu_peak = 148 * 16 * mhz * 1e6 / mufu
+            roofline["sfu_bound"] = {"mufu_per_entry": mufu, "peak_entries_per_s": sfu_peak,
+                                     "entries_per_s": entries_per_s, "frac": entries_per_s / sfu_peak}
+    else:
+        fp32_peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+        roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp32_peak, "traffic": None, "kernel": "fused_kmvm_kernel (SIMT fp32)",
+                    "peak_source": "FP32 CUDA-core peak = 148 SM x 128 FMA/clk x 2 x sm_max_mhz", **common}
+    if clk.get("sm_mhz") and roofline["bound"] == "fp32":
         roofline["frac_at_inrun_clock"] = achieved / (148 * 128 * 2 * clk["sm_mhz"] * 1e6 / 1e12)
-    # the kernel's own bound: CUDA-core issue of the kernel-entry evaluation (the contraction runs
-    # on the tensor cores in tf32x3 mode): ~2*DP (difference + square-accumulate) + c_instr + split/store
-    dp = 4 if w.d <= 4 else 12 if w.d <= 12 else 20 if w.d <= 20 else 32
-    c_instr = {0: 2, 1: 4, 2: 5, 3: 7}[w.family] + (4 if tc else 0)
-    instr_per_entry = 2 * dp + 1 + c_instr + (0 if tc else 8 * ((w.probes + 1 + 7) // 8))
-    entry_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / instr_per_entry
-    if mvm["launches"]:
-        entries_per_s = w.n * w.n * mvm["launches"] / (mvm["ms"] / 1e3)
-        roofline["entries_per_s"] = entries_per_s
-        roofline["entry_issue_bound"] = {"instr_per_entry": instr_per_entry, "peak_entries_per_s": entry_peak,
-                                         "frac": entries_per_s / entry_peak}
+    roofline["entries_per_s"] = entries_per_s
+    # DRAM traffic per launch of this kernel from the committed ncu --set full capture (same config)
+    tfile = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "mvm_traffic.json")
+    if os.path.exists(tfile):
+        tr = json.load(open(tfile))
+        if tr.get("workload") == w.name and tr.get("variant") == r["mvm_variant"]:
+            roofline["traffic"] = tr["dram_bytes_per_launch"]
+            roofline["traffic_source"] = tr.get("source")
     dcp = r["dc"]
     if dcp["launches"]:
         roofline["deriv_pass"] = {"achieved": (dcp["flops"] / dcp["ms"] * 1e3) / 1e12, "unit": "TFLOP/s",
