@@ -119,6 +119,8 @@ typedef struct gpk_group gpk_group;
 gpk_status gpk_group_create(int world, gpk_group** out);
 void gpk_group_destroy(gpk_group* g);
 gpk_status gpk_create_in_group(int device, gpk_group* g, int rank, gpk_ctx** out);
+/* Total rows n and input dimension d of the data set on ctx (GPK_INPUT_ERROR before gpk_set_data). */
+gpk_status gpk_data_shape(const gpk_ctx* ctx, int64_t* n, int* d);
 /* This rank's rows after gpk_set_data. */
 gpk_status gpk_shard_rows(const gpk_ctx* ctx, int64_t* r0, int64_t* r1);
 
@@ -177,6 +179,85 @@ gpk_status gpk_evaluate_mll_device(gpk_ctx* ctx, const double* dy, const double*
 /* ---- probes (trace_estimation.hpp:27-36, common.hpp:93-98) --------------- */
 gpk_status gpk_make_probes(int64_t n, int count, uint64_t seed, double* out /* n x count col-major */);
 uint64_t gpk_mix_seed(uint64_t seed, uint64_t salt);
+
+/* ---- callers of the hot path ------------------------------ */
+/* mll_exact (gp_likelihood.hpp:124-146) on the device: dense fp64 K_hat, cuSOLVER Cholesky.
+ * gradient: d+2 log-space components (nullable: value only, the validation / test metric of
+ * optimizer.hpp:458-459 and experiments.hpp:377-380).  Unsharded contexts only. */
+gpk_status gpk_mll_exact(gpk_ctx* ctx, const double* y, double* value, double* gradient);
+/* out (na) = cross_kernel(spec, params, A, X) v (kernels.hpp:339-354); A is na x d column-major
+ * (ld lda), v has n entries.  fp64. */
+gpk_status gpk_cross_kernel_mvm(gpk_ctx* ctx, const double* A, int64_t na, int64_t lda, const double* v,
+                                double* out);
+/* Predictive mean of run_training_arm (experiments.hpp:403-414): alpha = pcg_solve(K_hat, y,
+ * attached preconditioner, cfg), mean = cross_kernel(A, X) alpha.  iters nullable. */
+gpk_status gpk_predict_mean(gpk_ctx* ctx, const double* y, const double* A, int64_t na, int64_t lda,
+                            const gpk_cg_cfg* cfg, double* mean, int* iters);
+
+/* optimizer.hpp:22-43 OptMethod / OptOptions */
+typedef enum { GPK_OPT_LBFGS = 0, GPK_OPT_ADAM = 1 } gpk_opt_method;
+typedef struct {
+  int method;              /* gpk_opt_method (default L-BFGS) */
+  int max_steps;           /* 20 */
+  int lbfgs_memory;        /* 10 */
+  double armijo_c1;        /* 1e-4 */
+  double wolfe_c2;         /* 0.9 */
+  double adam_lr;          /* 0.1 */
+  int early_stop_patience; /* 3 */
+  double grad_tol;         /* 1e-8 */
+  int max_line_search;     /* 20 */
+} gpk_opt_options;
+
+/* Why the minimizer stopped (MinimizeResult.message, optimizer.hpp:236-298). */
+typedef enum {
+  GPK_OPT_MAX_STEPS = 0,         /* "" (ran max_steps) */
+  GPK_OPT_GRAD_TOL = 1,          /* "gradient norm below tolerance" */
+  GPK_OPT_LINE_SEARCH_FAILED = 2,/* "line search failed after bounded bisection; step rejected" */
+  GPK_OPT_STOPPED = 3            /* "stopped by callback" (early stopping on the validation proxy) */
+} gpk_opt_stop;
+
+/* OptimizeResult (optimizer.hpp:356-361) + MinimizeResult (:205-211) + OptTrace (:45-72).
+ * Arrays are caller-allocated and nullable; step arrays hold max_steps rows. */
+typedef struct {
+  double* best_log_params;       /* d+2: best (o, l_1..l_d, sigma^2), log space */
+  double best_validation;        /* +inf without validation data */
+  double final_train_neg_mll_per_point;
+  double final_objective;        /* MinimizeResult.f */
+  int minimizer_steps;           /* MinimizeResult.steps */
+  int converged;
+  int stop_reason;               /* gpk_opt_stop */
+  int n_steps;                   /* OptTrace.steps.size() */
+  double* step_theta;            /* max_steps x np_opt, row per step; np_opt = ard ? d+2 : 3 */
+  double* step_objective;
+  double* step_validation;
+  double* step_wall_time;
+  double* step_length;
+  double* step_f_before;
+  double* step_dir_derivative_before;
+  double* step_dir_derivative_after;
+  int* step_accepted;
+  long long* step_evaluations;   /* model_evaluations_cumulative */
+  int eval_capacity;             /* rows of the eval_* arrays */
+  int n_evaluations;             /* OptTrace.evaluations.size() (rows beyond eval_capacity are dropped) */
+  int* eval_step;
+  double* eval_f;
+  double* eval_grad_norm;
+  long long total_cg_iterations; /* telemetry: CG iterations over every objective evaluation */
+  double seconds_total;
+} gpk_opt_result;
+
+/* optimize() (optimizer.hpp:404-505) on the device path: L-BFGS (strong-Wolfe line search) or
+ * Adam on the negative mLL in log space; at every step start the preconditioner is rebuilt at
+ * the current iterate (precond_rank < 0: IdentityPreconditioner; >= 0: pivoted Cholesky of that
+ * rank + derivative factors, experiments.hpp:30-68) and the probes are redrawn with
+ * mix_seed(seed, step); trial points of the line search reuse both.  Unevaluable iterates read
+ * as +inf.  train: context with the training X (gpk_set_data); validation: context with the
+ * validation X or NULL (no early stopping).  dense_limit: validation / final metrics use the
+ * dense mll_exact for sets of at most this size (the reference's Dense/MatrixFree switch). */
+gpk_status gpk_optimize(gpk_ctx* train, const double* y, gpk_ctx* validation, const double* y_val, int family,
+                        int ard, const double* init_log_params, int precond_rank, double diag_tol,
+                        int probe_count, const gpk_opt_options* opts, const gpk_mll_cfg* mll_cfg, uint64_t seed,
+                        int64_t dense_limit, gpk_opt_result* res);
 
 /* Select the tensor-core MVM variant (takes effect at the next call). */
 gpk_status gpk_set_mvm_variant(gpk_ctx* ctx, int variant);

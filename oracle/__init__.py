@@ -336,3 +336,103 @@ def dense_spd(a, want_log=False):
     ml = np.zeros((n, n), order="F") if want_log else None
     _check(lib().orc_dense_spd(_p(a), C.c_int64(n), C.byref(lc), C.byref(le), _p(ev), _p(ml)))
     return lc.value, le.value, ev, ml
+
+
+# ---------------------------------------------------------------------------
+# the callers of the hot path
+# ---------------------------------------------------------------------------
+def mll_exact_value(family, x, p: Params, y, alpha=1.0):
+    """mll_exact(...).value (gp_likelihood.hpp:124-146) without the O(n^3) gradient."""
+    x = _f(x)
+    n, d = x.shape
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    val = C.c_double()
+    _check(lib().orc_mll_exact_value(C.c_int(family), C.c_double(alpha), _p(x), C.c_int64(n), C.c_int(d),
+                                     C.c_double(p.log_o), _p(p.log_ls), C.c_double(p.log_noise), _p(y),
+                                     C.byref(val)))
+    return val.value
+
+
+def cross_kernel_mvm(family, a, b, p: Params, v, alpha=1.0):
+    """cross_kernel(spec, params, A, B) @ v (kernels.hpp:339-354)."""
+    a, b = _f(a), _f(b)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = np.empty(a.shape[0])
+    _check(lib().orc_cross_kernel_mvm(C.c_int(family), C.c_double(alpha), _p(a), C.c_int64(a.shape[0]), _p(b),
+                                      C.c_int64(b.shape[0]), C.c_int(a.shape[1]), C.c_double(p.log_o),
+                                      _p(p.log_ls), C.c_double(p.log_noise), _p(v), _p(out)))
+    return out
+
+
+def predict_mean(family, x, y, xs, p: Params, rank=-1, diag_tol=0.0, dense_limit=4096, max_iters=100,
+                 rel_tol=1e-6, alpha=1.0):
+    """run_training_arm's predictive mean (experiments.hpp:403-414). Returns (mean, cg iterations)."""
+    x, xs = _f(x), _f(xs)
+    n, d = x.shape
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    mean = np.empty(xs.shape[0])
+    it = C.c_int()
+    _check(lib().orc_predict_mean(C.c_int(family), C.c_double(alpha), _p(x), C.c_int64(n), C.c_int(d), _p(y),
+                                  _p(xs), C.c_int64(xs.shape[0]), C.c_double(p.log_o), _p(p.log_ls),
+                                  C.c_double(p.log_noise), C.c_int(rank), C.c_double(diag_tol),
+                                  C.c_int64(dense_limit), C.c_int(max_iters), C.c_double(rel_tol), _p(mean),
+                                  C.byref(it)))
+    return mean, it.value
+
+
+OPT_DEFAULTS = dict(method=0, max_steps=20, lbfgs_memory=10, armijo_c1=1e-4, wolfe_c2=0.9, adam_lr=0.1,
+                    early_stop_patience=3, grad_tol=1e-8, max_line_search=20)
+
+
+def optimize(family, x, y, xv, yv, p0: Params, ard=True, rank=0, diag_tol=0.0, probe_count=8, max_iters=100,
+             rel_tol=1e-6, share_probes=True, seed=17, dense_limit=4096, alpha=1.0, **opts):
+    """optimize() (optimizer.hpp:404-505) with the pivoted-Cholesky builder (rank >= 0) or the
+    identity (rank < 0), per-step probe rotation mix_seed(seed, step) and early stopping."""
+    o = dict(OPT_DEFAULTS, **opts)
+    x = _f(x)
+    n, d = x.shape
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    nv = 0 if xv is None else int(np.shape(xv)[0])
+    xvf = _f(xv) if nv else None
+    yvf = np.ascontiguousarray(yv, dtype=np.float64) if nv else None
+    theta0 = np.concatenate([[p0.log_o], p0.log_ls, [p0.log_noise]])
+    optv = np.array([o["method"], o["max_steps"], o["lbfgs_memory"], o["armijo_c1"], o["wolfe_c2"], o["adam_lr"],
+                     o["early_stop_patience"], o["grad_tol"], o["max_line_search"]], dtype=np.float64)
+    ms = int(o["max_steps"])
+    npo = d + 2 if ard else 3
+    cap = ms * (int(o["max_line_search"]) + 1)
+    best = np.zeros(d + 2)
+    sc = np.zeros(8)
+    rows = np.zeros((ms, 8))
+    th = np.zeros((ms, npo))
+    ev = np.zeros((cap, 3))
+    _check(lib().orc_optimize(C.c_int(family), C.c_double(alpha), _p(x), C.c_int64(n), C.c_int(d), _p(y), _p(xvf),
+                              C.c_int64(nv), _p(yvf), C.c_int(int(ard)), _p(theta0), C.c_int(rank),
+                              C.c_double(diag_tol), C.c_int(probe_count), _p(optv), C.c_int(max_iters),
+                              C.c_double(rel_tol), C.c_int(int(share_probes)), C.c_uint64(seed),
+                              C.c_int64(dense_limit), _p(best), _p(sc), _p(rows), _p(th), _p(ev), C.c_int(cap)))
+    ns, ne = int(sc[5]), int(sc[6])
+    return dict(best=best, best_validation=sc[0], final_train_neg_mll_per_point=sc[1], final_objective=sc[2],
+                converged=bool(sc[3]), stop_reason=int(sc[4]), minimizer_steps=int(sc[7]),
+                steps=[dict(theta=th[s].copy(), objective=rows[s, 0], validation_metric=rows[s, 1],
+                            step_length=rows[s, 2], f_before=rows[s, 3], dir_derivative_before=rows[s, 4],
+                            dir_derivative_after=rows[s, 5], accepted=bool(rows[s, 6]),
+                            model_evaluations_cumulative=int(rows[s, 7])) for s in range(ns)],
+                evaluations=[dict(step=int(ev[e, 0]), f=ev[e, 1], grad_norm=ev[e, 2]) for e in range(min(ne, cap))])
+
+
+def minimize_quadratic(xstar, x0, method=0, max_steps=20, lbfgs_memory=10, armijo_c1=1e-4, wolfe_c2=0.9,
+                       adam_lr=0.1, grad_tol=1e-8, max_line_search=20):
+    """the optimizer.hpp minimizers on f = 0.5 |x - x*|^2 (GP bypassed)."""
+    xstar = np.ascontiguousarray(xstar, dtype=np.float64)
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    m = xstar.size
+    opt = np.array([max_steps, lbfgs_memory, armijo_c1, wolfe_c2, adam_lr, grad_tol, max_line_search], float)
+    traj = np.zeros((max_steps + 1, m))
+    certs = np.zeros((max_steps, 4))
+    sc = np.zeros(3)
+    _check(lib().orc_minimize_quadratic(C.c_int(method), C.c_int(m), _p(xstar), _p(x0), _p(opt), _p(traj),
+                                        _p(certs), _p(sc)))
+    ns = int(sc[0])
+    return dict(trajectory=traj[: ns + 1].copy(), certificates=certs[:ns].copy(), steps=ns, evaluations=int(sc[1]),
+                reason=int(sc[2]))

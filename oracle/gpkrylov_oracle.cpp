@@ -20,7 +20,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <chrono>
 #include <cstring>
+#include <deque>
 #include <functional>
 #include <limits>
 #include <memory>
@@ -1100,6 +1102,388 @@ inline ExactMll mll_exact(const Vec& y, const Mat& x, int family, double alpha, 
   return out;
 }
 
+
+// :124-146 without the gradient (the validation / test metric of optimizer.hpp:458-459,
+// experiments.hpp:377-380 only read .value).
+inline double mll_exact_value(const Vec& y, const Mat& x, int family, double alpha, const Hyper& p) {
+  KernelOperator k(family, alpha, x, p, Dense);
+  const Index n = k.rows();
+  require(static_cast<Index>(y.size()) == n, "mll_exact: label length does not match data");
+  Mat llt = k.dense_hat();
+  if (!cholesky(llt)) throw numerical_error("mll_exact: Cholesky factorization failed; consider a larger noise variance");
+  Vec a = y;
+  chol_solve(llt, a.data());
+  double ld = 0.0;
+  for (Index i = 0; i < n; ++i) ld += std::log(llt(i, i));
+  return -0.5 * (dot(y.data(), a.data(), n) + 2.0 * ld + static_cast<double>(n) * std::log(2.0 * M_PI));
+}
+
+// kernels.hpp:339-354 — cross_kernel(spec, params, A, B) * v.
+inline Vec cross_kernel_mvm(int family, double alpha, const Hyper& p, const Mat& a, const Mat& b, const Vec& v) {
+  p.validate();
+  require(a.cols == b.cols && a.cols == p.dim(), "cross_kernel: dimension mismatch");
+  const Index d = a.cols;
+  auto scaled = [&](const Mat& m, Mat& s, Vec& sq) {
+    s = Mat(m.rows, d);
+    sq.assign(static_cast<size_t>(m.rows), 0.0);
+    for (Index j = 0; j < d; ++j) {
+      const double l = std::exp(p.log_ls[static_cast<size_t>(j)]);
+      for (Index i = 0; i < m.rows; ++i) s(i, j) = m(i, j) / l;
+    }
+    for (Index i = 0; i < m.rows; ++i)
+      for (Index j = 0; j < d; ++j) sq[static_cast<size_t>(i)] += s(i, j) * s(i, j);
+  };
+  Mat sa, sb;
+  Vec qa, qb;
+  scaled(a, sa, qa);
+  scaled(b, sb, qb);
+  const double o2 = std::pow(p.outputscale(), 2);
+  Vec out(static_cast<size_t>(a.rows), 0.0);
+  for (Index i = 0; i < a.rows; ++i) {
+    double acc = 0.0;
+    for (Index j = 0; j < b.rows; ++j) {
+      double g = 0.0;
+      for (Index c = 0; c < d; ++c) g += sa(i, c) * sb(j, c);
+      const double s = std::max(-2.0 * g + qa[static_cast<size_t>(i)] + qb[static_cast<size_t>(j)], 0.0);
+      acc += o2 * shape(family, alpha, s) * v[static_cast<size_t>(j)];
+    }
+    out[static_cast<size_t>(i)] = acc;
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// optimizer.hpp — the caller of the hot path.
+// ---------------------------------------------------------------------------
+struct OptOptions {  // optimizer.hpp:24-43
+  int method = 0;  // 0 L-BFGS, 1 Adam
+  int max_steps = 20, lbfgs_memory = 10;
+  double c1 = 1e-4, c2 = 0.9, adam_lr = 0.1;
+  int patience = 3;
+  double grad_tol = 1e-8;
+  int max_line_search = 20;
+  void validate() const {
+    require(max_steps >= 1, "OptOptions: max_steps must be >= 1");
+    require(c1 > 0.0 && c1 < c2 && c2 < 1.0, "OptOptions: need 0 < c1 < c2 < 1");
+    require(lbfgs_memory >= 1, "OptOptions: lbfgs_memory must be >= 1");
+    require(patience >= 1, "OptOptions: early_stop_patience must be >= 1");
+  }
+};
+struct OptStep {  // StepRecord, optimizer.hpp:52-66
+  Vec theta;
+  double objective = 0.0, validation = 0.0, wall = 0.0, step_length = 0.0, f_before = 0.0, dd_before = 0.0,
+         dd_after = 0.0;
+  long evals = 0;
+  bool accepted = true;
+};
+struct OptEval { int step; double f, gnorm; };  // EvalRecord, :45-50
+struct OptLog { std::vector<OptStep> steps; std::vector<OptEval> evals; };
+struct FG { double f = 0.0; Vec g; };
+using ObjFn = std::function<double(const Vec&, Vec&)>;
+struct StepHooks {  // MinimizerHooks, :196-202
+  std::function<void(int, const Vec&)> begin;
+  std::function<bool(int, const Vec&, double)> after;
+};
+struct MinOut { Vec x; double f = std::numeric_limits<double>::quiet_NaN(); int steps = 0; bool converged = false; int reason = 0; };
+
+inline double vnorm(const Vec& v) { return std::sqrt(dot(v.data(), v.data(), static_cast<Index>(v.size()))); }
+inline double vdot(const Vec& a, const Vec& b) { return dot(a.data(), b.data(), static_cast<Index>(a.size())); }
+inline Vec axpy(const Vec& x, double a, const Vec& p) {
+  Vec r(x.size());
+  for (size_t i = 0; i < x.size(); ++i) r[i] = x[i] + a * p[i];
+  return r;
+}
+
+// CountingObjective (:76-90): every evaluation is logged with its step.
+inline FG counted(const ObjFn& obj, OptLog& log, const Vec& x, int step) {
+  FG e;
+  e.g.assign(x.size(), 0.0);
+  e.f = obj(x, e.g);
+  log.evals.push_back({step, e.f, vnorm(e.g)});
+  return e;
+}
+
+// :100-180 — strong-Wolfe search: doubling bracket phase, then bisection zoom.
+inline bool wolfe_search(const ObjFn& obj, OptLog& log, const Vec& x, const Vec& p, const FG& start, double c1,
+                         double c2, int max_evals, int step, double* alpha_out, FG* at) {
+  const double f0 = start.f, g0 = vdot(start.g, p);
+  if (!(g0 < 0.0)) return false;
+  int used = 0;
+  auto trial = [&](double a) { ++used; return counted(obj, log, axpy(x, a, p), step); };
+  auto too_high = [&](double a, double f) { return f > f0 + c1 * a * g0; };
+  auto curvature = [&](const FG& e) { return std::abs(vdot(e.g, p)) <= c2 * std::abs(g0); };
+  double lo = 0.0, hi = 0.0, flo = f0;
+  double a = 1.0, a_prev = 0.0, f_prev = f0;
+  bool have_bracket = false;
+  while (used < max_evals) {
+    FG e = trial(a);
+    const double ga = vdot(e.g, p);
+    if (too_high(a, e.f) || (a_prev > 0.0 && e.f >= f_prev)) {
+      lo = a_prev; flo = f_prev; hi = a; have_bracket = true;
+      break;
+    }
+    if (curvature(e)) { *alpha_out = a; *at = std::move(e); return true; }
+    if (ga >= 0.0) {
+      lo = a; flo = e.f; hi = a_prev; have_bracket = true;
+      break;
+    }
+    a_prev = a;
+    f_prev = e.f;
+    a = std::min(2.0 * a, 1e6);
+  }
+  if (!have_bracket) return false;
+  while (used < max_evals) {
+    const double m = 0.5 * (lo + hi);
+    FG e = trial(m);
+    if (too_high(m, e.f) || e.f >= flo) {
+      hi = m;
+    } else {
+      if (curvature(e)) { *alpha_out = m; *at = std::move(e); return true; }
+      if (vdot(e.g, p) * (hi - lo) >= 0.0) hi = lo;
+      lo = m;
+      flo = e.f;
+    }
+    if (std::abs(hi - lo) < 1e-16) break;
+  }
+  return false;
+}
+
+using Clock = std::chrono::steady_clock;
+
+// :215-301 — L-BFGS (two-loop recursion), objective re-sampled at every step start.
+inline MinOut lbfgs(const ObjFn& obj, const Vec& x0, const OptOptions& o, OptLog& log, const StepHooks& h) {
+  o.validate();
+  MinOut r;
+  r.x = x0;
+  std::deque<std::pair<Vec, Vec>> mem;
+  const auto t0 = Clock::now();
+  auto secs = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+  for (int step = 1; step <= o.max_steps; ++step) {
+    if (h.begin) h.begin(step, r.x);
+    FG cur = counted(obj, log, r.x, step);
+    r.f = cur.f;
+    if (vnorm(cur.g) <= o.grad_tol) { r.converged = true; r.reason = 1; break; }
+    Vec q = cur.g;
+    std::vector<double> coef(mem.size());
+    for (int i = static_cast<int>(mem.size()) - 1; i >= 0; --i) {
+      const Vec& s = mem[static_cast<size_t>(i)].first;
+      const Vec& yv = mem[static_cast<size_t>(i)].second;
+      const double rho = 1.0 / vdot(yv, s);
+      coef[static_cast<size_t>(i)] = rho * vdot(s, q);
+      q = axpy(q, -coef[static_cast<size_t>(i)], yv);
+    }
+    if (!mem.empty()) {
+      const double gam = vdot(mem.back().first, mem.back().second) / vdot(mem.back().second, mem.back().second);
+      for (double& v : q) v *= gam;
+    }
+    for (size_t i = 0; i < mem.size(); ++i) {
+      const double rho = 1.0 / vdot(mem[i].second, mem[i].first);
+      const double b = rho * vdot(mem[i].second, q);
+      q = axpy(q, coef[i] - b, mem[i].first);
+    }
+    Vec p(q.size());
+    for (size_t i = 0; i < q.size(); ++i) p[i] = -q[i];
+    if (vdot(p, cur.g) >= 0.0) {
+      mem.clear();
+      for (size_t i = 0; i < q.size(); ++i) p[i] = -cur.g[i];
+    }
+    double alpha = 0.0;
+    FG at;
+    const bool ok = wolfe_search(obj, log, r.x, p, cur, o.c1, o.c2, o.max_line_search, step, &alpha, &at);
+    OptStep rec;
+    rec.f_before = cur.f;
+    rec.dd_before = vdot(cur.g, p);
+    rec.evals = static_cast<long>(log.evals.size());
+    rec.wall = secs();
+    if (!ok) {
+      rec.theta = r.x;
+      rec.objective = cur.f;
+      rec.accepted = false;
+      log.steps.push_back(rec);
+      r.reason = 2;
+      break;
+    }
+    Vec s(p.size()), yv(p.size());
+    for (size_t i = 0; i < p.size(); ++i) {
+      s[i] = alpha * p[i];
+      yv[i] = at.g[i] - cur.g[i];
+    }
+    if (vdot(s, yv) > 1e-12 * vnorm(s) * vnorm(yv)) {
+      mem.emplace_back(s, yv);
+      if (static_cast<int>(mem.size()) > o.lbfgs_memory) mem.pop_front();
+    }
+    for (size_t i = 0; i < s.size(); ++i) r.x[i] += s[i];
+    r.f = at.f;
+    r.steps = step;
+    rec.theta = r.x;
+    rec.objective = at.f;
+    rec.step_length = alpha;
+    rec.dd_after = vdot(at.g, p);
+    rec.evals = static_cast<long>(log.evals.size());
+    rec.wall = secs();
+    log.steps.push_back(rec);
+    if (h.after && !h.after(step, r.x, r.f)) { r.reason = 3; break; }
+  }
+  return r;
+}
+
+// :305-350 — Adam (beta1 0.9, beta2 0.999, eps 1e-8).
+inline MinOut adam(const ObjFn& obj, const Vec& x0, const OptOptions& o, OptLog& log, const StepHooks& h) {
+  o.validate();
+  MinOut r;
+  r.x = x0;
+  Vec m(x0.size(), 0.0), v(x0.size(), 0.0);
+  const auto t0 = Clock::now();
+  for (int step = 1; step <= o.max_steps; ++step) {
+    if (h.begin) h.begin(step, r.x);
+    FG cur = counted(obj, log, r.x, step);
+    r.f = cur.f;
+    if (vnorm(cur.g) <= o.grad_tol) { r.converged = true; r.reason = 1; break; }
+    const double bc1 = 1.0 - std::pow(0.9, step), bc2 = 1.0 - std::pow(0.999, step);
+    for (size_t i = 0; i < x0.size(); ++i) {
+      m[i] = 0.9 * m[i] + (1.0 - 0.9) * cur.g[i];
+      v[i] = 0.999 * v[i] + (1.0 - 0.999) * (cur.g[i] * cur.g[i]);
+      r.x[i] -= (o.adam_lr / bc1) * (m[i] / (std::sqrt(v[i] / bc2) + 1e-8));
+    }
+    r.steps = step;
+    OptStep rec;
+    rec.theta = r.x;
+    rec.objective = cur.f;
+    rec.f_before = cur.f;
+    rec.step_length = o.adam_lr;
+    rec.evals = static_cast<long>(log.evals.size());
+    rec.wall = std::chrono::duration<double>(Clock::now() - t0).count();
+    log.steps.push_back(rec);
+    if (h.after && !h.after(step, r.x, r.f)) { r.reason = 3; break; }
+  }
+  return r;
+}
+
+// :373-400 — tied (isotropic) lengthscale packing and gradient collapse.
+inline Hyper theta_to_hyper(const Vec& x, int d, bool ard) {
+  Hyper p;
+  if (ard) {
+    require(x.size() >= 3, "Hyperparameters: log vector needs at least 3 entries");
+    p.log_o = x[0];
+    p.log_ls.assign(x.begin() + 1, x.end() - 1);
+    p.log_noise = x.back();
+  } else {
+    p.log_o = x[0];
+    p.log_ls.assign(static_cast<size_t>(d), x[1]);
+    p.log_noise = x[2];
+  }
+  return p;
+}
+inline Vec hyper_to_theta(const Hyper& p, bool ard) {
+  if (!ard) return {p.log_o, p.log_ls[0], p.log_noise};
+  Vec x{p.log_o};
+  x.insert(x.end(), p.log_ls.begin(), p.log_ls.end());
+  x.push_back(p.log_noise);
+  return x;
+}
+inline Vec collapse(const Vec& g, int d, bool ard) {
+  if (ard) return g;
+  double s = 0.0;
+  for (int j = 0; j < d; ++j) s += g[static_cast<size_t>(1 + j)];
+  return {g[0], s, g[static_cast<size_t>(d + 1)]};
+}
+
+struct OptimizeOut {  // OptimizeResult, :356-361
+  Hyper best;
+  OptLog log;
+  double best_validation = std::numeric_limits<double>::infinity();
+  double final_train = 0.0;
+  MinOut min;
+};
+
+// :404-505 — optimize(): per-step preconditioner rebuild (rank < 0: identity, else
+// pivoted Cholesky + derivative factors, experiments.hpp:30-68) and probe rotation,
+// +inf on unevaluable iterates, early stopping on the validation proxy.
+inline OptimizeOut optimize(int family, double alpha, const Mat& xt, const Vec& yt, const Mat& xv, const Vec& yv,
+                            bool ard, const Hyper& init, int rank, double diag_tol, int probe_count,
+                            const OptOptions& o, const MllConfig& mcfg, std::uint64_t seed, Index dense_limit) {
+  o.validate();
+  init.validate();
+  require(xt.rows >= 1, "optimize: empty training set");
+  require(init.dim() == xt.cols, "optimize: hyperparameter dimension mismatch");
+  const int d = static_cast<int>(xt.cols);
+  const Index n = xt.rows;
+  const int mode = n <= dense_limit ? Dense : MatrixFree;
+  std::unique_ptr<MllPrecond> precond;
+  Mat probes;
+  std::uint64_t probe_seed = 0;
+  ObjFn objective = [&](const Vec& x, Vec& g) -> double {
+    try {
+      const Hyper p = theta_to_hyper(x, d, ard);
+      p.validate();
+      if (rank == -2) {
+        const ExactMll ex = mll_exact(yt, xt, family, alpha, p);
+        const Vec cg = collapse(ex.gradient, d, ard);
+        for (size_t i = 0; i < g.size(); ++i) g[i] = -cg[i];
+        return -ex.value;
+      }
+      KernelOperator op(family, alpha, xt, p, mode);
+      const MllEvaluation e = evaluate_mll(yt, op, *precond, probes, probe_seed, mcfg, true);
+      const Vec cg = collapse(e.gradient, d, ard);
+      for (size_t i = 0; i < g.size(); ++i) g[i] = -cg[i];
+      return -e.value;
+    } catch (const input_error&) {
+    } catch (const numerical_error&) {
+    }
+    std::fill(g.begin(), g.end(), 0.0);
+    return std::numeric_limits<double>::infinity();
+  };
+  StepHooks h;
+  h.begin = [&](int step, const Vec& x) {
+    const Hyper p = theta_to_hyper(x, d, ard);
+    KernelOperator op(family, alpha, xt, p, mode);
+    if (rank == -2) {  // dense-oracle run: the objective is mll_exact itself
+      precond.reset();
+    } else if (rank < 0) {
+      precond = std::make_unique<IdentityPrecond>();
+    } else {
+      KernelAccessor acc{n, [&op] { return op.kernel_diagonal(); }, [&op](Index i) { return op.kernel_column(i); }};
+      auto pc = std::make_unique<DiagPlusLowRank>(pivoted_cholesky(acc, rank, diag_tol, p.noise()));
+      pc->attach_derivatives(pivoted_cholesky_deriv_factors(op, *pc), d + 1);
+      precond = std::move(pc);
+    }
+    probe_seed = mix_seed(seed, static_cast<std::uint64_t>(step));
+    probes = make_probes(n, probe_count, probe_seed);
+  };
+  OptimizeOut out;
+  out.best = init;
+  int since_best = 0;
+  const bool early = xv.rows > 0;
+  auto validation = [&](const Hyper& p) -> double {
+    if (xv.rows == 0) return 0.0;
+    if (xv.rows <= dense_limit) return -mll_exact_value(yv, xv, family, alpha, p) / static_cast<double>(xv.rows);
+    KernelOperator vop(family, alpha, xv, p, MatrixFree);
+    const std::uint64_t vs = mix_seed(seed, 0x7a11ULL);
+    const Mat vz = make_probes(xv.rows, probe_count, vs);
+    IdentityPrecond ident;
+    return -evaluate_mll(yv, vop, ident, vz, vs, mcfg, false).value / static_cast<double>(xv.rows);
+  };
+  h.after = [&](int, const Vec& x, double) {
+    const Hyper p = theta_to_hyper(x, d, ard);
+    const double vm = validation(p);
+    out.log.steps.back().validation = vm;
+    if (!early) { out.best = p; return true; }
+    if (vm < out.best_validation) {
+      out.best_validation = vm;
+      out.best = p;
+      since_best = 0;
+    } else if (++since_best >= o.patience) {
+      return false;
+    }
+    return true;
+  };
+  const Vec x0 = hyper_to_theta(init, ard);
+  out.min = o.method == 0 ? lbfgs(objective, x0, o, out.log, h) : adam(objective, x0, o, out.log, h);
+  if (!early && out.log.steps.empty()) out.best = init;
+  out.final_train = n <= dense_limit ? -mll_exact_value(yt, xt, family, alpha, out.best) / static_cast<double>(n)
+                                     : out.min.f / static_cast<double>(n);
+  return out;
+}
 }  // namespace orc
 
 // ============================================================================
@@ -1469,4 +1853,159 @@ int orc_dense_spd(const double* a, std::int64_t n, double* logdet_chol, double* 
   });
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// the hot path's callers — optimize() (optimizer.hpp:404-505),
+// the validation / test metric (mll_exact value, gp_likelihood.hpp:124-146) and
+// the predictive mean of run_training_arm (experiments.hpp:403-414).
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int orc_mll_exact_value(int family, double alpha, const double* x, std::int64_t n, int d, double log_o,
+                        const double* log_ls, double log_noise, const double* y, double* value) {
+  return guard([&] {
+    *value = orc::mll_exact_value(orc::Vec(y, y + n), to_mat(x, n, d), family, alpha,
+                                  to_hyper(log_o, log_ls, d, log_noise));
+  });
+}
+
+// out (na) = cross_kernel(A, B) * v  (kernels.hpp:339-354)
+int orc_cross_kernel_mvm(int family, double alpha, const double* a, std::int64_t na, const double* b,
+                         std::int64_t nb, int d, double log_o, const double* log_ls, double log_noise,
+                         const double* v, double* out) {
+  return guard([&] {
+    const orc::Vec r = orc::cross_kernel_mvm(family, alpha, to_hyper(log_o, log_ls, d, log_noise), to_mat(a, na, d),
+                                             to_mat(b, nb, d), orc::Vec(v, v + nb));
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// Predictive mean of run_training_arm (experiments.hpp:403-414): the preconditioner
+// is rebuilt at the given hyperparameters (rank < 0: identity), alpha = pcg_solve(K_hat, y),
+// mean = cross_kernel(test, train) alpha.  iters: CG iterations of the solve.
+int orc_predict_mean(int family, double alpha, const double* x, std::int64_t n, int d, const double* y,
+                     const double* xs, std::int64_t ns, double log_o, const double* log_ls, double log_noise,
+                     int rank, double diag_tol, std::int64_t dense_limit, int max_iters, double rel_tol, double* mean,
+                     int* iters) {
+  return guard([&] {
+    const orc::Hyper h = to_hyper(log_o, log_ls, d, log_noise);
+    orc::KernelOperator op(family, alpha, to_mat(x, n, d), h, n <= dense_limit ? orc::Dense : orc::MatrixFree);
+    std::unique_ptr<orc::MllPrecond> prec;
+    if (rank < 0) {
+      prec = std::make_unique<orc::IdentityPrecond>();
+    } else {
+      orc::KernelAccessor acc{n, [&op] { return op.kernel_diagonal(); }, [&op](orc::Index i) { return op.kernel_column(i); }};
+      prec = std::make_unique<orc::DiagPlusLowRank>(orc::pivoted_cholesky(acc, rank, diag_tol, h.noise()));
+    }
+    const orc::CgResult r = orc::pcg_solve(op, orc::Vec(y, y + n), *prec, orc::CgConfig{max_iters, rel_tol, false});
+    *iters = r.iterations_used;
+    const orc::Vec m = orc::cross_kernel_mvm(family, alpha, h, to_mat(xs, ns, d), to_mat(x, n, d), r.solution);
+    std::memcpy(mean, m.data(), sizeof(double) * m.size());
+  });
+}
+
+// optimize() (optimizer.hpp:404-505).  theta0: d+2 log parameters (o, l_1..l_d, sigma^2);
+// opt[9] = {method, max_steps, lbfgs_memory, c1, c2, adam_lr, patience, grad_tol, max_line_search};
+// scalars[8] = {best_validation, final_train_neg_mll_per_point, final_f, converged, reason,
+//               n_steps, n_evaluations, minimizer_steps};  best: d+2;
+// step_rows: max_steps x 8 row-major {objective, validation, step_length, f_before, dd_before,
+//            dd_after, accepted, evaluations_cumulative}; step_theta: max_steps x np_opt;
+// eval_rows: eval_cap x 3 {step, f, grad_norm}.
+int orc_optimize(int family, double alpha, const double* xt, std::int64_t n, int d, const double* yt,
+                 const double* xv, std::int64_t nv, const double* yv, int ard, const double* theta0, int rank,
+                 double diag_tol, int probe_count, const double* opt, int max_iters, double rel_tol, int share_probes,
+                 std::uint64_t seed, std::int64_t dense_limit, double* best, double* scalars, double* step_rows,
+                 double* step_theta, double* eval_rows, int eval_cap) {
+  return guard([&] {
+    orc::OptOptions o;
+    o.method = static_cast<int>(opt[0]);
+    o.max_steps = static_cast<int>(opt[1]);
+    o.lbfgs_memory = static_cast<int>(opt[2]);
+    o.c1 = opt[3];
+    o.c2 = opt[4];
+    o.adam_lr = opt[5];
+    o.patience = static_cast<int>(opt[6]);
+    o.grad_tol = opt[7];
+    o.max_line_search = static_cast<int>(opt[8]);
+    orc::MllConfig mc;
+    mc.solver = orc::CgConfig{max_iters, rel_tol, false};
+    mc.share_probes = share_probes != 0;
+    const orc::Hyper init = to_hyper(theta0[0], theta0 + 1, d, theta0[d + 1]);
+    const orc::Mat xvm = nv > 0 ? to_mat(xv, nv, d) : orc::Mat(0, d);
+    const orc::Vec yvv = nv > 0 ? orc::Vec(yv, yv + nv) : orc::Vec();
+    const orc::OptimizeOut r = orc::optimize(family, alpha, to_mat(xt, n, d), orc::Vec(yt, yt + n), xvm, yvv, ard != 0,
+                                             init, rank, diag_tol, probe_count, o, mc, seed, dense_limit);
+    best[0] = r.best.log_o;
+    for (int j = 0; j < d; ++j) best[1 + j] = r.best.log_ls[static_cast<size_t>(j)];
+    best[d + 1] = r.best.log_noise;
+    scalars[0] = r.best_validation;
+    scalars[1] = r.final_train;
+    scalars[2] = r.min.f;
+    scalars[3] = r.min.converged ? 1.0 : 0.0;
+    scalars[4] = r.min.reason;
+    scalars[5] = static_cast<double>(r.log.steps.size());
+    scalars[6] = static_cast<double>(r.log.evals.size());
+    scalars[7] = r.min.steps;
+    const int npo = ard ? d + 2 : 3;
+    for (size_t s = 0; s < r.log.steps.size() && static_cast<int>(s) < o.max_steps; ++s) {
+      const orc::OptStep& st = r.log.steps[s];
+      double* row = step_rows + 8 * s;
+      row[0] = st.objective; row[1] = st.validation; row[2] = st.step_length; row[3] = st.f_before;
+      row[4] = st.dd_before; row[5] = st.dd_after; row[6] = st.accepted ? 1.0 : 0.0;
+      row[7] = static_cast<double>(st.evals);
+      for (int j = 0; j < npo; ++j) step_theta[s * npo + j] = st.theta[static_cast<size_t>(j)];
+    }
+    for (size_t e = 0; e < r.log.evals.size() && static_cast<int>(e) < eval_cap; ++e) {
+      eval_rows[3 * e] = r.log.evals[e].step;
+      eval_rows[3 * e + 1] = r.log.evals[e].f;
+      eval_rows[3 * e + 2] = r.log.evals[e].gnorm;
+    }
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+// SPEC.md:451/:467 "oracle mode bypassing GP": the minimizers of optimizer.hpp:215-350 on
+// f(x) = 0.5 |x - x*|^2 (+ the Armijo / curvature certificates of every accepted step).
+// traj: (max_steps + 1) x m row-major iterates (x0 first); certs: max_steps x 4 row-major
+// {f_before, f_after, dd_before, dd_after}; scalars[3] = {steps, evaluations, reason}.
+int orc_minimize_quadratic(int method, int m, const double* xstar, const double* x0, const double* opt,
+                           double* traj, double* certs, double* scalars) {
+  return guard([&] {
+    orc::OptOptions o;
+    o.method = method;
+    o.max_steps = static_cast<int>(opt[0]);
+    o.lbfgs_memory = static_cast<int>(opt[1]);
+    o.c1 = opt[2];
+    o.c2 = opt[3];
+    o.adam_lr = opt[4];
+    o.grad_tol = opt[5];
+    o.max_line_search = static_cast<int>(opt[6]);
+    const orc::Vec xs(xstar, xstar + m);
+    orc::ObjFn f = [&](const orc::Vec& x, orc::Vec& g) {
+      double v = 0.0;
+      for (int i = 0; i < m; ++i) {
+        g[static_cast<size_t>(i)] = x[static_cast<size_t>(i)] - xs[static_cast<size_t>(i)];
+        v += 0.5 * g[static_cast<size_t>(i)] * g[static_cast<size_t>(i)];
+      }
+      return v;
+    };
+    orc::OptLog log;
+    const orc::Vec x0v(x0, x0 + m);
+    const orc::MinOut r = method == 0 ? orc::lbfgs(f, x0v, o, log, {}) : orc::adam(f, x0v, o, log, {});
+    for (int i = 0; i < m; ++i) traj[i] = x0[i];
+    for (size_t s = 0; s < log.steps.size(); ++s) {
+      for (int i = 0; i < m; ++i) traj[(s + 1) * m + i] = log.steps[s].theta[static_cast<size_t>(i)];
+      certs[4 * s] = log.steps[s].f_before;
+      certs[4 * s + 1] = log.steps[s].objective;
+      certs[4 * s + 2] = log.steps[s].dd_before;
+      certs[4 * s + 3] = log.steps[s].dd_after;
+    }
+    scalars[0] = static_cast<double>(log.steps.size());
+    scalars[1] = static_cast<double>(log.evals.size());
+    scalars[2] = r.reason;
+  });
+}
 }  // extern "C"

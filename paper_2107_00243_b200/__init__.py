@@ -11,5 +11,9 @@ from .gpkrylov import (  # noqa: F401
     batched_pcg, evaluate_mll, evaluate_mll_device, make_probes, mix_seed, mll_estimate, mll_gradient, pcg_solve,
     pivoted_cholesky, pivoted_cholesky_deriv_factors, pivoted_cholesky_with_derivatives,
 )
+from .gpkrylov import (  # noqa: F401  SURVEY §8(f): the callers of the hot path
+    Dataset, ExactMll, IdentityBuilder, OptimizeResult, OptOptions, PivotedCholeskyBuilder, count_model_evaluations,
+    cross_kernel_mvm, mll_exact, optimize, predict_mean, run_training_arm,
+)
 
 __version__ = "0.1.0"

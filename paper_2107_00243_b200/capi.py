@@ -40,6 +40,30 @@ class gpk_mll_result(C.Structure):
                 ("kernel_entries", C.c_longlong), ("mvm_flops", C.c_longlong), ("gpu_launches", C.c_int)]
 
 
+class gpk_opt_options(C.Structure):
+    _fields_ = [("method", C.c_int), ("max_steps", C.c_int), ("lbfgs_memory", C.c_int), ("armijo_c1", C.c_double),
+                ("wolfe_c2", C.c_double), ("adam_lr", C.c_double), ("early_stop_patience", C.c_int),
+                ("grad_tol", C.c_double), ("max_line_search", C.c_int)]
+
+
+class gpk_opt_result(C.Structure):
+    _fields_ = [("best_log_params", C.POINTER(C.c_double)), ("best_validation", C.c_double),
+                ("final_train_neg_mll_per_point", C.c_double), ("final_objective", C.c_double),
+                ("minimizer_steps", C.c_int), ("converged", C.c_int), ("stop_reason", C.c_int),
+                ("n_steps", C.c_int), ("step_theta", C.POINTER(C.c_double)),
+                ("step_objective", C.POINTER(C.c_double)), ("step_validation", C.POINTER(C.c_double)),
+                ("step_wall_time", C.POINTER(C.c_double)), ("step_length", C.POINTER(C.c_double)),
+                ("step_f_before", C.POINTER(C.c_double)), ("step_dir_derivative_before", C.POINTER(C.c_double)),
+                ("step_dir_derivative_after", C.POINTER(C.c_double)), ("step_accepted", C.POINTER(C.c_int)),
+                ("step_evaluations", C.POINTER(C.c_longlong)), ("eval_capacity", C.c_int),
+                ("n_evaluations", C.c_int), ("eval_step", C.POINTER(C.c_int)), ("eval_f", C.POINTER(C.c_double)),
+                ("eval_grad_norm", C.POINTER(C.c_double)), ("total_cg_iterations", C.c_longlong),
+                ("seconds_total", C.c_double)]
+
+
+GPK_OPT_LBFGS, GPK_OPT_ADAM = 0, 1
+GPK_OPT_MAX_STEPS, GPK_OPT_GRAD_TOL, GPK_OPT_LINE_SEARCH_FAILED, GPK_OPT_STOPPED = range(4)
+
 _D = C.POINTER(C.c_double)
 _I = C.POINTER(C.c_int)
 _L = C.POINTER(C.c_int64)
@@ -86,6 +110,13 @@ SIGNATURES = {
     "gpk_group_destroy": (None, [_V]),
     "gpk_create_in_group": (C.c_int, [C.c_int, _V, C.c_int, C.POINTER(_V)]),
     "gpk_shard_rows": (C.c_int, [_V, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "gpk_data_shape": (C.c_int, [_V, C.POINTER(C.c_int64), _I]),
+    "gpk_mll_exact": (C.c_int, [_V, _D, _D, _D]),
+    "gpk_cross_kernel_mvm": (C.c_int, [_V, _D, C.c_int64, C.c_int64, _D, _D]),
+    "gpk_predict_mean": (C.c_int, [_V, _D, _D, C.c_int64, C.c_int64, C.POINTER(gpk_cg_cfg), _D, _I]),
+    "gpk_optimize": (C.c_int, [_V, _D, _V, _D, C.c_int, C.c_int, _D, C.c_int, C.c_double, C.c_int,
+                               C.POINTER(gpk_opt_options), C.POINTER(gpk_mll_cfg), C.c_uint64, C.c_int64,
+                               C.POINTER(gpk_opt_result)]),
 }
 
 

@@ -2087,6 +2087,182 @@ gpk_status gpk_evaluate_mll(gpk_ctx* ctx, const double* y, const double* Z, int6
   });
 }
 
+// ---- validation / test metric and predictive mean ------------------
+
+// mll_exact (gp_likelihood.hpp:124-146) on the device: dense K_hat in fp64 (the
+// reference's expanded distances), cuSOLVER Cholesky, log det from its diagonal;
+// the gradient from K_hat^{-1} (potri) contracted with each dense dK_w.
+gpk_status gpk_mll_exact(gpk_ctx* ctx, const double* y, double* value, double* gradient) {
+  return guard(ctx, [&] {
+    gpk_ctx* c = ctx;
+    c->require_ready();
+    require(c->world == 1, "mll_exact: not available on a row-sharded context");
+    require(value != nullptr, "mll_exact: null output");
+    const int n = c->n;
+    require(static_cast<double>(n) * n * 8.0 * (gradient ? 2.0 : 1.0) <= 96e9,
+            "mll_exact: n too large for a dense factorisation");
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(y[i])) fail(GPK_INPUT_ERROR, "KernelOperator: non-finite entries in input vector");
+    c->ensure_handles();
+    DBuf<double> K, a, work, part;
+    DBuf<int> info;
+    K.ensure(static_cast<size_t>(n) * n);
+    a.ensure(n);
+    part.ensure(n);
+    info.ensure(1);
+    c->check_launch(gpk::launch_dense_kernel(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, -1, c->o2, 1.0, K.p, n,
+                                             c->st),
+                    1, "dense_kernel");
+    add_diag_kernel<<<(n + 255) / 256, 256, 0, c->st>>>(K.p, n, c->noise);
+    c->check_launch(cudaGetLastError(), 1, "add_diag");
+    int lwork = 0;
+    CS(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, K.p, n, &lwork));
+    work.ensure(static_cast<size_t>(std::max(lwork, 1)));
+    CS(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, n, K.p, n, work.p, lwork, info.p));
+    int hinfo = 0;
+    c->d2h(&hinfo, info.p, sizeof(int));
+    if (hinfo != 0) fail(GPK_NUMERICAL_ERROR, "mll_exact: Cholesky factorization failed; consider a larger noise variance");
+    c->h2d(a.p, y, sizeof(double) * n);
+    CS(cusolverDnDpotrs(c->solver, CUBLAS_FILL_MODE_LOWER, n, 1, K.p, n, a.p, n, info.p));
+    std::vector<double> dg(n), ha(n);
+    CK(cudaMemcpy2DAsync(dg.data(), sizeof(double), K.p, (static_cast<size_t>(n) + 1) * sizeof(double),
+                         sizeof(double), n, cudaMemcpyDeviceToHost, c->st));
+    c->d2h(ha.data(), a.p, sizeof(double) * n);
+    double ld = 0.0, q = 0.0;
+    for (int i = 0; i < n; ++i) ld += std::log(dg[i]);
+    for (int i = 0; i < n; ++i) q += y[i] * ha[i];
+    *value = -0.5 * (q + 2.0 * ld + static_cast<double>(n) * std::log(2.0 * 3.14159265358979323846));
+    if (!gradient) return;
+    // K_hat^{-1} (lower triangle) in place of the factor
+    int lw2 = 0;
+    CS(cusolverDnDpotri_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, K.p, n, &lw2));
+    work.ensure(static_cast<size_t>(std::max(lw2, 1)));
+    CS(cusolverDnDpotri(c->solver, CUBLAS_FILL_MODE_LOWER, n, K.p, n, work.p, lw2, info.p));
+    DBuf<double> dK, dka;
+    dK.ensure(static_cast<size_t>(n) * n);
+    dka.ensure(n);
+    const double one = 1.0, zero = 0.0;
+    std::vector<double> hp(n), hk(n);
+    for (int w = 0; w < c->d + 2; ++w) {
+      double quad = 0.0, tr = 0.0, raw = c->noise;
+      if (w == c->d + 1) {  // dK_hat / dsigma^2 = I
+        for (int i = 0; i < n; ++i) quad += ha[i] * ha[i];
+        CK(cudaMemcpy2DAsync(hp.data(), sizeof(double), K.p, (static_cast<size_t>(n) + 1) * sizeof(double),
+                             sizeof(double), n, cudaMemcpyDeviceToHost, c->st));
+        c->sync();
+        for (int i = 0; i < n; ++i) tr += hp[i];
+      } else {
+        double fac = 2.0 / c->o;  // kernel_deriv_column scale factors (kernels.hpp:252-267)
+        raw = c->o;
+        if (w >= 1) {
+          const double lj = c->ls[w - 1];
+          fac = -2.0 * c->o2 / (lj * lj * lj);
+          raw = lj;
+        }
+        c->check_launch(gpk::launch_dense_kernel(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, w, c->o2, fac, dK.p,
+                                                 n, c->st),
+                        1, "dense_kernel");
+        CB(cublasDsymv(c->blas, CUBLAS_FILL_MODE_LOWER, n, &one, dK.p, n, a.p, 1, &zero, dka.p, 1));
+        c->check_launch(gpk::launch_sym_frob_partials(K.p, n, dK.p, n, n, part.p, c->st), 1, "sym_frob");
+        CK(cudaMemcpyAsync(hk.data(), dka.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->st));
+        c->d2h(hp.data(), part.p, sizeof(double) * n);
+        for (int i = 0; i < n; ++i) quad += ha[i] * hk[i];
+        for (int i = 0; i < n; ++i) tr += hp[i];
+      }
+      gradient[w] = 0.5 * (quad - tr) * raw;
+    }
+  });
+}
+
+// out = cross_kernel(A, X) v (kernels.hpp:339-354): A is na x d (test points), v has n entries.
+static void cross_common(gpk_ctx* c, const double* A, int64_t na, int64_t lda, const double* dv, double* out) {
+  const int d = c->d;
+  require(na >= 1 && lda >= na, "cross_kernel: dimension mismatch");
+  std::vector<double> sa(static_cast<size_t>(na) * d), qa(static_cast<size_t>(na), 0.0);
+  for (int j = 0; j < d; ++j)
+    for (int64_t i = 0; i < na; ++i) {
+      const double v = A[j * lda + i];
+      if (!std::isfinite(v)) fail(GPK_INPUT_ERROR, "cross_kernel: non-finite test inputs");
+      sa[j * na + i] = v / c->ls[j];
+    }
+  for (int64_t i = 0; i < na; ++i)
+    for (int j = 0; j < d; ++j) qa[i] += sa[j * na + i] * sa[j * na + i];
+  DBuf<double> dsa, dqa, dout;
+  dsa.ensure(sa.size());
+  dqa.ensure(qa.size());
+  dout.ensure(static_cast<size_t>(na));
+  c->h2d(dsa.p, sa.data(), sizeof(double) * sa.size());
+  c->h2d(dqa.p, qa.data(), sizeof(double) * qa.size());
+  c->check_launch(gpk::launch_cross_mvm(c->family, dsa.p, dqa.p, static_cast<int>(na), c->sx.p, c->sq.p, c->n, d,
+                                        c->o2, dv, dout.p, c->st),
+                  1, "cross_mvm");
+  c->d2h(out, dout.p, sizeof(double) * na);
+}
+
+gpk_status gpk_cross_kernel_mvm(gpk_ctx* ctx, const double* A, int64_t na, int64_t lda, const double* v,
+                                double* out) {
+  return guard(ctx, [&] {
+    gpk_ctx* c = ctx;
+    c->require_ready();
+    require(c->world == 1, "cross_kernel: not available on a row-sharded context");
+    for (int i = 0; i < c->n; ++i)
+      if (!std::isfinite(v[i])) fail(GPK_INPUT_ERROR, "KernelOperator: non-finite entries in input vector");
+    DBuf<double> dv;
+    dv.ensure(c->n);
+    c->h2d(dv.p, v, sizeof(double) * c->n);
+    cross_common(c, A, na, lda, dv.p, out);
+  });
+}
+
+// run_training_arm's predictive mean (experiments.hpp:403-414): alpha = pcg_solve(K_hat, y)
+// with the attached preconditioner (one mBCG column, fp64-certified in the reduced-precision
+// modes), then mean = cross_kernel(A, X) alpha.  iters: CG iterations of the solve (nullable).
+gpk_status gpk_predict_mean(gpk_ctx* ctx, const double* y, const double* A, int64_t na, int64_t lda,
+                            const gpk_cg_cfg* cfg, double* mean, int* iters) {
+  return guard(ctx, [&] {
+    gpk_ctx* c = ctx;
+    c->require_ready();
+    require(c->world == 1, "cross_kernel: not available on a row-sharded context");
+    require(cfg != nullptr, "gpk_predict_mean: null config");
+    require(c->pkind != 0, "gpkrylov_cuda: no preconditioner");
+    require(cfg->max_iters >= 1, "CgConfig: max_iters must be >= 1");
+    require(cfg->rel_tol > 0.0 && cfg->rel_tol < 1.0, "CgConfig: rel_tol must be in (0, 1)");
+    require(cfg->precision >= GPK_PREC_FP64 && cfg->precision <= GPK_PREC_TF32X3, "CgConfig: unknown precision");
+    for (int i = 0; i < c->n; ++i)
+      if (!std::isfinite(y[i])) fail(GPK_INPUT_ERROR, "KernelOperator: non-finite entries in input vector");
+    DBuf<double> db, dx;
+    db.ensure(c->ldn);
+    dx.ensure(c->ldn);
+    c->h2d(db.p, y, sizeof(double) * c->n);
+    const bool fp64 = cfg->precision == GPK_PREC_FP64;
+    c->use_tc = cfg->precision == GPK_PREC_TF32X3;
+    gpk_ctx::CgOut r;
+    try {
+      r = c->mbcg(db.p, c->ldn, 1, cfg->max_iters, cfg->rel_tol, fp64, dx.p, c->ldn, nullptr, nullptr, nullptr);
+    } catch (const GpkError& e) {
+      int col;
+      fail(GPK_SOLVER_ERROR, strip_col(e.msg, &col));
+    }
+    if (!fp64 && cfg->refine > 0) {
+      double mr;
+      c->refine(db.p, c->ldn, 1, dx.p, c->ldn, r, cfg->max_iters, cfg->rel_tol, cfg->refine, &mr);
+    }
+    if (iters) *iters = r.iters[0];
+    cross_common(c, A, na, lda, dx.p, mean);
+  });
+}
+
+gpk_status gpk_data_shape(const gpk_ctx* ctx, int64_t* n, int* d) {
+  if (!ctx || !ctx->have_data) return GPK_INPUT_ERROR;
+  if (n) *n = ctx->n;
+  if (d) *d = ctx->d;
+  return GPK_OK;
+}
+
+void gpk_set_error_internal(gpk_ctx* ctx, const char* msg) {
+  if (ctx) ctx->err = msg ? msg : "";
+}
+
 gpk_status gpk_make_probes(int64_t n, int count, uint64_t seed, double* out) {
   return guard(nullptr, [&] { make_probes_impl(n, count, seed, out); });
 }

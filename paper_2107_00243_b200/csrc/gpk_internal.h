@@ -75,6 +75,14 @@ cudaError_t launch_fused_kmvm_tcg(int family, int d, const float* xh, const floa
 
 // Reference-formula kernel column (kernels.hpp:235-243) / derivative column (:252-267), fp64.
 // which < 0: K[:, p];  which == 0: outputscale;  1..d: lengthscale which-1.
+// dense exact mLL pieces and the predictive mean's cross-kernel MVM (gpk_mvm.cu).
+cudaError_t launch_dense_kernel(int family, const double* sx, const double* x, const double* sq, int n, int d,
+                                int which, double o2, double fac, double* out, long long ldm, cudaStream_t st);
+cudaError_t launch_sym_frob_partials(const double* A, long long lda, const double* B, long long ldb, int n,
+                                     double* part, cudaStream_t st);
+cudaError_t launch_cross_mvm(int family, const double* sa, const double* qa, int na, const double* sb,
+                             const double* qb, int nb, int d, double o2, const double* v, double* out,
+                             cudaStream_t st);
 cudaError_t launch_kernel_column(int family, const double* sx, const double* x, const double* sq, int n, int d,
                                  long long p, int which, double o2, double fac, double* out, cudaStream_t st);
 

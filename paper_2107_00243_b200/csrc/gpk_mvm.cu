@@ -262,4 +262,120 @@ cudaError_t launch_kernel_deriv_columns(int family, const double* sx, const doub
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// dense exact mLL (validation / test metric, gp_likelihood.hpp:124-146)
+// and the predictive mean's cross-kernel MVM (kernels.hpp:339-354, experiments.hpp:410-412).
+// ---------------------------------------------------------------------------
+
+// Dense noise-free K (which < 0) or dK/dtheta_which (0..d) in fp64, column-major
+// [n][ldm]: entry (r, p) with the same operation order as kernel_column_kernel
+// (the reference's assemble_kernel_rows / kernel_column expanded distances).
+// Grid: x over rows (256 per block), y over columns.
+__global__ void dense_kernel_kernel(int f, const double* __restrict__ sx, const double* __restrict__ x,
+                                    const double* __restrict__ sq, int n, int d, int which, double o2, double fac,
+                                    double* __restrict__ out, long long ldm) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long p = blockIdx.y;
+  if (r >= n) return;
+  double g = 0.0;
+  for (int k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(sx[static_cast<long long>(k) * n + r], sx[k * n + p]));
+  double s = __dsub_rn(__dadd_rn(sq[r], sq[p]), __dmul_rn(2.0, g));
+  s = s > 0.0 ? s : 0.0;
+  double v;
+  if (which < 0) {
+    v = __dmul_rn(o2, ref_shape(f, s));
+  } else if (which == 0) {
+    v = __dmul_rn(fac, __dmul_rn(o2, ref_shape(f, s)));
+  } else {
+    const int j = which - 1;
+    const double dx = __dsub_rn(x[static_cast<long long>(j) * n + r], x[static_cast<long long>(j) * n + p]);
+    v = __dmul_rn(fac, __dmul_rn(ref_shape_ds(f, s), __dmul_rn(dx, dx)));
+  }
+  out[p * ldm + r] = v;
+}
+
+cudaError_t launch_dense_kernel(int family, const double* sx, const double* x, const double* sq, int n, int d,
+                                int which, double o2, double fac, double* out, long long ldm, cudaStream_t st) {
+  dim3 g((n + 255) / 256, n);
+  dense_kernel_kernel<<<g, 256, 0, st>>>(family, sx, x, sq, n, d, which, o2, fac, out, ldm);
+  return cudaGetLastError();
+}
+
+// Per-block partial sums of sum_{i,j} A_ij B_ij for symmetric A, B of which only the
+// LOWER triangles are valid (cuSOLVER potri / the assembled dK): diagonal once,
+// strictly-lower entries twice.  One block per column j (fixed order: deterministic).
+__global__ void sym_frob_partials_kernel(const double* __restrict__ A, long long lda, const double* __restrict__ B,
+                                         long long ldb, int n, double* __restrict__ part) {
+  const int j = blockIdx.x;
+  double acc = 0.0;
+  for (int i = j + threadIdx.x; i < n; i += blockDim.x) {
+    const double v = A[j * lda + i] * B[j * ldb + i];
+    acc += (i == j) ? v : 2.0 * v;
+  }
+  __shared__ double sh[256];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[j] = sh[0];
+}
+
+cudaError_t launch_sym_frob_partials(const double* A, long long lda, const double* B, long long ldb, int n,
+                                     double* part, cudaStream_t st) {
+  sym_frob_partials_kernel<<<n, 256, 0, st>>>(A, lda, B, ldb, n, part);
+  return cudaGetLastError();
+}
+
+// out[i] = sum_j o2 shape(max(-2 <sa_i, sb_j> + |sa_i|^2 + |sb_j|^2, 0)) v[j]
+// (cross_kernel(A, B) v, kernels.hpp:339-354) in fp64.  128 rows of A per block (one per
+// thread, coordinates in registers), 64-row tiles of B and v staged in shared memory.
+constexpr int kXR = 128, kXC = 64;
+__global__ void __launch_bounds__(kXR) cross_mvm_kernel(int f, const double* __restrict__ sa,
+                                                        const double* __restrict__ qa, int na,
+                                                        const double* __restrict__ sb,
+                                                        const double* __restrict__ qb, int nb, int d, double o2,
+                                                        const double* __restrict__ v, double* __restrict__ out) {
+  __shared__ double tb[32][kXC];
+  __shared__ double tq[kXC], tv[kXC];
+  const int i = blockIdx.x * kXR + threadIdx.x;
+  double a[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) a[k] = (k < d && i < na) ? sa[static_cast<long long>(k) * na + i] : 0.0;
+  const double qi = i < na ? qa[i] : 0.0;
+  double acc = 0.0;
+  for (int j0 = 0; j0 < nb; j0 += kXC) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < d * kXC; e += kXR) {
+      const int k = e / kXC, jj = e % kXC;
+      tb[k][jj] = j0 + jj < nb ? sb[static_cast<long long>(k) * nb + j0 + jj] : 0.0;
+    }
+    if (threadIdx.x < kXC) {
+      const int j = j0 + threadIdx.x;
+      tq[threadIdx.x] = j < nb ? qb[j] : 0.0;
+      tv[threadIdx.x] = j < nb ? v[j] : 0.0;
+    }
+    __syncthreads();
+    const int jn = min(kXC, nb - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      double g = 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (k < d) g = __dadd_rn(g, __dmul_rn(a[k], tb[k][jj]));
+      double s = __dadd_rn(__dadd_rn(__dmul_rn(-2.0, g), qi), tq[jj]);
+      s = s > 0.0 ? s : 0.0;
+      acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(o2, ref_shape(f, s)), tv[jj]));
+    }
+  }
+  if (i < na) out[i] = acc;
+}
+
+cudaError_t launch_cross_mvm(int family, const double* sa, const double* qa, int na, const double* sb,
+                             const double* qb, int nb, int d, double o2, const double* v, double* out,
+                             cudaStream_t st) {
+  cross_mvm_kernel<<<(na + kXR - 1) / kXR, kXR, 0, st>>>(family, sa, qa, na, sb, qb, nb, d, o2, v, out);
+  return cudaGetLastError();
+}
+
 }  // namespace gpk

@@ -648,3 +648,251 @@ def mll_estimate(y, k, prec, batch, solver: CgConfig):
 def mll_gradient(y, k, prec, batch, solver: CgConfig):
     """gp_likelihood.hpp:111-115"""
     return evaluate_mll(y, k, prec, batch, MllConfig(solver, True), with_gradient=True).gradient
+
+
+# ---------------------------------------------------------------------------
+# SURVEY §8(f): the callers of the hot path — dense exact mLL (validation / test
+# metric), cross-kernel predictive mean, and the optimize() step driver.
+# ---------------------------------------------------------------------------
+@dataclass
+class ExactMll:
+    """gp_likelihood.hpp:119-122"""
+    value: float
+    gradient: Optional[np.ndarray]
+
+
+def mll_exact(y, x, spec: KernelSpec, params: Hyperparameters, with_gradient: bool = True, device: int = 0):
+    """Dense exact mLL (+ log-space gradient) on the device (gp_likelihood.hpp:124-146)."""
+    op = KernelOperator(spec, x, params, device=device)
+    return op_mll_exact(op, y, with_gradient)
+
+
+def op_mll_exact(op: KernelOperator, y, with_gradient: bool = True):
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if y.ndim != 1 or y.shape[0] != op.rows():
+        raise InputError("mll_exact: label length does not match data")
+    v = C.c_double()
+    g = np.zeros(op.num_params()) if with_gradient else None
+    op.ctx.check(op.ctx.lib.gpk_mll_exact(op.ctx.h, _ptr(y), C.byref(v), _ptr(g)))
+    return ExactMll(v.value, g)
+
+
+def cross_kernel_mvm(op: KernelOperator, a, v):
+    """cross_kernel(spec, params, A, X) @ v (kernels.hpp:339-354), X = the operator's data."""
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2 or a.shape[1] != op.dim():
+        raise InputError("cross_kernel: dimension mismatch")
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if v.shape != (op.rows(),):
+        raise InputError("cross_kernel: dimension mismatch")
+    out = np.empty(a.shape[0])
+    op.ctx.check(op.ctx.lib.gpk_cross_kernel_mvm(op.ctx.h, _ptr(a), a.shape[0], a.shape[0], _ptr(v), _ptr(out)))
+    return out
+
+
+def predict_mean(op: KernelOperator, y, x_test, solver: CgConfig):
+    """run_training_arm's predictive mean (experiments.hpp:403-414) with the attached
+    preconditioner: returns (mean, CG iterations of the K_hat alpha = y solve)."""
+    if op.preconditioner is None:
+        raise InputError("predict_mean: no preconditioner attached")
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if y.shape != (op.rows(),):
+        raise InputError("pcg_solve: rhs length does not match operator")
+    a = np.asfortranarray(np.asarray(x_test, dtype=np.float64))
+    if a.ndim != 2 or a.shape[1] != op.dim():
+        raise InputError("cross_kernel: dimension mismatch")
+    out = np.empty(a.shape[0])
+    it = C.c_int()
+    cc = solver.c()
+    op.ctx.check(op.ctx.lib.gpk_predict_mean(op.ctx.h, _ptr(y), _ptr(a), a.shape[0], a.shape[0], C.byref(cc),
+                                             _ptr(out), C.byref(it)))
+    return out, it.value
+
+
+@dataclass
+class Dataset:
+    """dataset.hpp:18-26 (features n x d, targets n)."""
+    x: np.ndarray
+    y: np.ndarray
+
+    def size(self):
+        return 0 if self.x is None else int(np.shape(self.x)[0])
+
+
+@dataclass
+class OptOptions:
+    """optimizer.hpp:24-43"""
+    method: str = "lbfgs"  # "lbfgs" | "adam"
+    max_steps: int = 20
+    lbfgs_memory: int = 10
+    armijo_c1: float = 1e-4
+    wolfe_c2: float = 0.9
+    adam_lr: float = 0.1
+    early_stop_patience: int = 3
+    validation_fraction: float = 0.16
+    grad_tol: float = 1e-8
+    max_line_search: int = 20
+
+    def c(self):
+        m = {"lbfgs": capi.GPK_OPT_LBFGS, "adam": capi.GPK_OPT_ADAM}.get(self.method)
+        if m is None:
+            raise InputError("OptOptions: unknown method")
+        return capi.gpk_opt_options(m, int(self.max_steps), int(self.lbfgs_memory), float(self.armijo_c1),
+                                    float(self.wolfe_c2), float(self.adam_lr), int(self.early_stop_patience),
+                                    float(self.grad_tol), int(self.max_line_search))
+
+
+@dataclass
+class PivotedCholeskyBuilder:
+    """build_preconditioner's pivoted-Cholesky branch (experiments.hpp:30-68)."""
+    rank: int
+    diag_tol: float = 0.0
+
+
+@dataclass
+class IdentityBuilder:
+    """The baseline arm's builder (experiments.hpp:470-471): IdentityPreconditioner."""
+    rank: int = -1
+
+
+@dataclass
+class StepRecord:  # optimizer.hpp:52-66
+    theta: np.ndarray
+    objective: float
+    validation_metric: float
+    model_evaluations_cumulative: int
+    wall_time_s: float
+    accepted: bool
+    step_length: float
+    f_before: float
+    dir_derivative_before: float
+    dir_derivative_after: float
+
+
+@dataclass
+class EvalRecord:  # optimizer.hpp:45-50
+    step: int
+    f: float
+    grad_norm: float
+
+
+@dataclass
+class OptTrace:  # optimizer.hpp:68-72
+    steps: list
+    evaluations: list
+
+
+_STOP_MESSAGES = {capi.GPK_OPT_MAX_STEPS: "", capi.GPK_OPT_GRAD_TOL: "gradient norm below tolerance",
+                  capi.GPK_OPT_LINE_SEARCH_FAILED: "line search failed after bounded bisection; step rejected",
+                  capi.GPK_OPT_STOPPED: "stopped by callback"}
+
+
+@dataclass
+class OptimizeResult:
+    """optimizer.hpp:356-361 (+ the MinimizeResult fields and GPU telemetry)."""
+    best: Hyperparameters
+    trace: OptTrace
+    best_validation: float
+    final_train_neg_mll_per_point: float
+    final_objective: float
+    minimizer_steps: int
+    converged: bool
+    message: str
+    total_cg_iterations: int
+    seconds_total: float
+
+
+def count_model_evaluations(trace: OptTrace) -> int:
+    """optimizer.hpp:74"""
+    return len(trace.evaluations)
+
+
+def optimize(train: Dataset, validation: Optional[Dataset], spec: KernelSpec, init: Hyperparameters,
+             precond_builder, probe_count: int, opts: OptOptions, mll_cfg: MllConfig, seed: int,
+             dense_limit: int = 4096, device: int = 0) -> OptimizeResult:
+    """optimize() (optimizer.hpp:404-505) on the device path (gpk_optimize): L-BFGS / Adam on the
+    negative mLL in log space, preconditioner rebuilt and probes redrawn at every step start."""
+    x = np.asfortranarray(np.asarray(train.x, dtype=np.float64))
+    if x.ndim != 2 or x.shape[0] < 1:
+        raise InputError("optimize: empty training set")
+    if init.dim() != x.shape[1]:
+        raise InputError("optimize: hyperparameter dimension mismatch")
+    n, d = x.shape
+    ytr = np.ascontiguousarray(train.y, dtype=np.float64)
+    op = KernelOperator(spec, x, init, device=device)
+    vop = None
+    yv = None
+    if validation is not None and validation.size() > 0:
+        vop = KernelOperator(spec, validation.x, init, device=device)
+        yv = np.ascontiguousarray(validation.y, dtype=np.float64)
+    ard = bool(spec.ard)
+    npo = d + 2 if ard else 3
+    ms = int(opts.max_steps)
+    cap = ms * (int(opts.max_line_search) + 1)
+    best = np.zeros(d + 2)
+    th = np.zeros((ms, npo))
+    arr = {k: np.zeros(ms) for k in ("obj", "val", "wall", "len", "fb", "ddb", "dda")}
+    acc = np.zeros(ms, dtype=np.int32)
+    sev = np.zeros(ms, dtype=np.int64)
+    est = np.zeros(cap, dtype=np.int32)
+    ef = np.zeros(cap)
+    eg = np.zeros(cap)
+    r = capi.gpk_opt_result()
+    r.best_log_params = _ptr(best)
+    r.step_theta = _ptr(th)
+    r.step_objective, r.step_validation, r.step_wall_time = _ptr(arr["obj"]), _ptr(arr["val"]), _ptr(arr["wall"])
+    r.step_length, r.step_f_before = _ptr(arr["len"]), _ptr(arr["fb"])
+    r.step_dir_derivative_before, r.step_dir_derivative_after = _ptr(arr["ddb"]), _ptr(arr["dda"])
+    r.step_accepted = acc.ctypes.data_as(C.POINTER(C.c_int))
+    r.step_evaluations = sev.ctypes.data_as(C.POINTER(C.c_longlong))
+    r.eval_capacity = cap
+    r.eval_step = est.ctypes.data_as(C.POINTER(C.c_int))
+    r.eval_f, r.eval_grad_norm = _ptr(ef), _ptr(eg)
+    theta0 = np.ascontiguousarray(init.to_log_vector(), dtype=np.float64)
+    oc = opts.c()
+    mc = mll_cfg.c(True)
+    rank = int(getattr(precond_builder, "rank", -1))
+    diag_tol = float(getattr(precond_builder, "diag_tol", 0.0))
+    op.ctx.check(op.ctx.lib.gpk_optimize(op.ctx.h, _ptr(ytr), vop.ctx.h if vop else None, _ptr(yv), spec.code,
+                                         int(ard), _ptr(theta0), rank, diag_tol, int(probe_count), C.byref(oc),
+                                         C.byref(mc), C.c_uint64(seed), int(dense_limit), C.byref(r)))
+    steps = [StepRecord(th[s].copy(), arr["obj"][s], arr["val"][s], int(sev[s]), arr["wall"][s], bool(acc[s]),
+                        arr["len"][s], arr["fb"][s], arr["ddb"][s], arr["dda"][s]) for s in range(r.n_steps)]
+    evals = [EvalRecord(int(est[e]), float(ef[e]), float(eg[e])) for e in range(min(r.n_evaluations, cap))]
+    return OptimizeResult(Hyperparameters.from_log_vector(best), OptTrace(steps, evals), r.best_validation,
+                          r.final_train_neg_mll_per_point, r.final_objective, r.minimizer_steps, bool(r.converged),
+                          _STOP_MESSAGES.get(r.stop_reason, ""), int(r.total_cg_iterations), r.seconds_total)
+
+
+@dataclass
+class TrainingRow:
+    """experiments.hpp:360-372 (the per-arm row of run_training)."""
+    steps: int
+    model_evaluations: int
+    wall_time_s: float
+    train_neg_mll_per_point: float
+    test_neg_mll_per_point: float
+    test_rmse: float
+    final_params: Hyperparameters
+
+
+def run_training_arm(train: Dataset, validation: Optional[Dataset], test: Optional[Dataset], spec: KernelSpec,
+                     init: Hyperparameters, precond_builder, probe_count: int, opts: OptOptions,
+                     solver: CgConfig, seed: int, dense_limit: int = 4096, device: int = 0) -> TrainingRow:
+    """detail::run_training_arm (experiments.hpp:388-418): optimize, then the dense test metric and
+    the predictive-mean RMSE with the preconditioner rebuilt at the best hyperparameters."""
+    res = optimize(train, validation, spec, init, precond_builder, probe_count, opts, MllConfig(solver, True),
+                   seed, dense_limit, device)
+    test_nll, rmse = 0.0, 0.0
+    if test is not None and test.size() > 0:
+        test_nll = -mll_exact(test.y, test.x, spec, res.best, with_gradient=False, device=device).value / test.size()
+        op = KernelOperator(spec, train.x, res.best, device=device)
+        if int(getattr(precond_builder, "rank", -1)) < 0:
+            IdentityPreconditioner(op)
+        else:
+            pivoted_cholesky(op, precond_builder.rank, precond_builder.diag_tol)
+        mean, _ = predict_mean(op, train.y, test.x, solver)
+        rmse = float(np.sqrt(np.sum((mean - np.asarray(test.y)) ** 2) / test.size()))
+    return TrainingRow(len(res.trace.steps), count_model_evaluations(res.trace),
+                       res.trace.steps[-1].wall_time_s if res.trace.steps else 0.0,
+                       res.final_train_neg_mll_per_point, test_nll, rmse, res.best)
