@@ -404,6 +404,10 @@ struct gpk_ctx {
   DBuf<double> st_X[2], st_R[2], st_P[2], st_Z;
   DBuf<float> w_v32, w_f32, w_vhi, w_vlo;
   bool use_tc = false;  // GPK_PREC_TF32X3: value MVMs on the tcgen05 tensor cores
+  bool use_persistent_pchol = [] {  // env GPK_PCHOL_STEPS=1 selects the per-step kernels (A/B checks)
+    const char* e = std::getenv("GPK_PCHOL_STEPS");
+    return !(e && std::atoi(e) == 1);
+  }();
   int sync_every = [] {  // CG iterations between host round trips (env GPK_SYNC_EVERY, default 1:
     const char* e = std::getenv("GPK_SYNC_EVERY");  // measured no gain from lazier syncs at C2)
     const int v = e ? std::atoi(e) : 1;
@@ -1791,9 +1795,22 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
       h0.dp = kmax;
       h0.p = 0;
       c->h2d(ps.p, &h0, sizeof(h0));
-      c->check_launch(gpk::launch_pchol_dev(c->family, c->sx.p, c->sq.p, n, c->d, c->o2, c->L.p, rank, diag_tol, kmax,
-                                            col.p, dg.p, c->w_argval.p, c->w_argidx.p, ps.p, dpiv.p, c->st),
-                      3 * rank, "pivoted_cholesky");
+      // one cooperative launch for all steps (gpk_pchol.cu); the per-step kernels remain the
+      // fallback when the pivot row does not fit in shared memory or co-residency is unavailable
+      const size_t psm = sizeof(double) * static_cast<size_t>(rank);
+      const int pg = (psm <= 200 * 1024 && c->use_persistent_pchol) ? gpk::pchol_persistent_grid(n, psm) : 0;
+      if (pg > 0) {
+        c->w_argval.ensure(2 * static_cast<size_t>(pg) + 1);
+        c->w_argidx.ensure(2 * static_cast<size_t>(pg) + 1);
+        c->check_launch(gpk::launch_pchol_persistent(c->family, c->sx.p, c->sq.p, n, c->d, c->o2, c->L.p, rank,
+                                                     diag_tol, kmax, dg.p, c->w_argval.p, c->w_argidx.p, ps.p,
+                                                     dpiv.p, pg, c->st),
+                        1, "pivoted_cholesky");
+      } else {
+        c->check_launch(gpk::launch_pchol_dev(c->family, c->sx.p, c->sq.p, n, c->d, c->o2, c->L.p, rank, diag_tol,
+                                              kmax, col.p, dg.p, c->w_argval.p, c->w_argidx.p, ps.p, dpiv.p, c->st),
+                        3 * rank, "pivoted_cholesky");
+      }
       gpk::PivotState hs{};
       c->d2h(&hs, ps.p, sizeof(hs));
       step = hs.done;  // steps whose column was produced
@@ -1880,8 +1897,7 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
     c->have_dl = false;
     if (k > 0) {
       c->dL.ensure(static_cast<size_t>(nw) * n * k);
-      DBuf<double> dcol, facs;
-      dcol.ensure(static_cast<size_t>(nw) * n);
+      DBuf<double> facs;
       facs.ensure(nw);
       std::vector<double> hf(nw);
       for (int w = 0; w < nw; ++w) {  // kernels.hpp:262 (outputscale) and :270-272 (lengthscales)
@@ -1904,18 +1920,16 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
       dLp.ensure(static_cast<size_t>(nw) * k * kB);
       dpiv.ensure(k);
       c->h2d(dpiv.p, c->pivots.data(), sizeof(long long) * k);
+      DBuf<double> rep;
+      rep.ensure(gpk::dl_replay_workspace(nw));
       c->ensure_handles();
       for (int s0 = 0; s0 < k; s0 += kB) {
         const int bb = std::min(kB, k - s0);
-        // DC_w[:, q] = dK_w column of pivot s0+q
-        for (int q = 0; q < bb; ++q)
-          c->check_launch(gpk::launch_kernel_deriv_columns(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d,
-                                                           c->pivots[s0 + q], nw, facs.p, c->o2,
-                                                           dcol.p, c->st),
-                          1, "kernel_deriv_columns"),
-              c->check_launch(gpk::launch_gather_cols(dcol.p, n, nullptr, 1.0, n, nw, DC.p + static_cast<size_t>(q) * n,
-                                                      static_cast<long long>(n) * kB, c->st),
-                              1, "gather");
+        // DC_w[:, q] = dK_w column of pivot s0+q (all pivots of the block in one launch)
+        c->check_launch(gpk::launch_deriv_columns_block(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, dpiv.p + s0, bb,
+                                                        nw, facs.p, c->o2, DC.p, static_cast<long long>(n) * kB,
+                                                        c->st),
+                        1, "deriv_columns_block");
         if (s0 > 0) {
           // Lp[c][q] = L[piv_q, c], dLp_w[c][q] = dL_w[piv_q, c]   (s0 x bb, column-major)
           c->check_launch(gpk::launch_gather_pivot_rows(c->L.p, n, 0, 1, dpiv.p + s0, s0, bb, Lp.p, c->st), 1,
@@ -1931,10 +1945,10 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
                                        static_cast<long long>(n) * kB, nw));
           c->launches += 2;
         }
-        for (int q = 0; q < bb; ++q)
-          c->check_launch(gpk::launch_dl_inblock(c->L.p, n, c->dL.p, wstride, nw, s0, q, c->pivots[s0 + q], DC.p,
-                                                 static_cast<long long>(n) * kB, n, c->st),
-                          1, "dl_inblock");
+        // in-block recursion: one launch per block (every CTA replays the pivot rows' recursion)
+        c->check_launch(gpk::launch_dl_block(c->L.p, c->dL.p, wstride, nw, s0, bb, dpiv.p + s0, DC.p,
+                                             static_cast<long long>(n) * kB, n, rep.p, c->st),
+                        2, "dl_block");
       }
       // tr(P^{-1} dP_w) = 2 sum(C o dL_w)  (algebraically equal to preconditioners.hpp:138-145)
       const int nrb = gpk::num_chunks(n * k);

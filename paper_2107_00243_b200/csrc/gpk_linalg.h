@@ -59,6 +59,19 @@ struct PivotState {
 cudaError_t launch_pchol_dev(int family, const double* sx, const double* sq, int n, int d, double o2, double* L,
                              int rank, double diag_tol, double kmax, double* col, double* dg, double* bval,
                              long long* bidx, PivotState* ps, long long* pivots, cudaStream_t st);
+// gpk_pchol.cu: the whole pivoted Cholesky in one cooperative launch (grid = pchol_persistent_grid;
+// cval / cidx hold 2 * grid candidates), and the blocked derivative-factor kernels.
+int pchol_persistent_grid(int n, size_t smem);
+cudaError_t launch_pchol_persistent(int family, const double* sx, const double* sq, int n, int d, double o2,
+                                    double* L, int rank, double diag_tol, double kmax, double* dg, double* cval,
+                                    long long* cidx, PivotState* ps, long long* pivots, int grid, cudaStream_t st);
+cudaError_t launch_deriv_columns_block(int family, const double* sx, const double* x, const double* sq, int n, int d,
+                                       const long long* piv, int bb, int nw, const double* facs, double o2,
+                                       double* DC, long long dcw_stride, cudaStream_t st);
+size_t dl_replay_workspace(int nw);
+cudaError_t launch_dl_block(const double* L, double* dL, long long wstride, int nw, int s0, int bb,
+                            const long long* piv, const double* DC, long long dcw_stride, int n, double* rep,
+                            cudaStream_t st);
 cudaError_t launch_kernel_deriv_columns(int family, const double* sx, const double* x, const double* sq, int n, int d,
                                         long long p, int nw, const double* facs, double o2, double* out,
                                         cudaStream_t st);

@@ -4,6 +4,7 @@
 
 #include "gpk_linalg.h"
 #include "gpk_mvm.cuh"
+#include "gpk_ref_shape.cuh"
 
 namespace gpk {
 
@@ -152,38 +153,6 @@ cudaError_t launch_pack_v64(const double* V, long long ldv, const int* colmap, i
   pack_v_kernel<double><<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(V, ldv, colmap, t, n, n_pad,
                                                                                     sh.tn, sh.cgs, sh.vld, V64);
   return cudaGetLastError();
-}
-
-// kernels.hpp:235-243 (which < 0) and :252-267 (which >= 0), bit-faithful
-// operation order: s = (sq_r + sq_p) - 2 <sx_r, sx_p>, clamped; no FMA contraction.
-__device__ double ref_shape(int f, double s) {
-  switch (f) {
-    case kRBF: return exp(-0.5 * s);
-    case kMatern12: return exp(-sqrt(s));
-    case kMatern32: {
-      const double r = sqrt(__dmul_rn(3.0, s));
-      return __dmul_rn(__dadd_rn(1.0, r), exp(-r));
-    }
-    default: {
-      const double r = sqrt(__dmul_rn(5.0, s));
-      return __dmul_rn(__dadd_rn(__dadd_rn(1.0, r), __ddiv_rn(__dmul_rn(r, r), 3.0)), exp(-r));
-    }
-  }
-}
-__device__ double ref_shape_ds(int f, double s) {
-  switch (f) {
-    case kRBF: return __dmul_rn(-0.5, exp(-0.5 * s));
-    case kMatern12: {
-      if (s <= 0.0) return 0.0;
-      const double r = sqrt(s);
-      return __ddiv_rn(-exp(-r), __dmul_rn(2.0, r));
-    }
-    case kMatern32: return __dmul_rn(-1.5, exp(-sqrt(__dmul_rn(3.0, s))));
-    default: {
-      const double r = sqrt(__dmul_rn(5.0, s));
-      return __dmul_rn(__dmul_rn(-(5.0 / 6.0), __dadd_rn(1.0, r)), exp(-r));
-    }
-  }
 }
 
 __global__ void kernel_column_kernel(int f, const double* __restrict__ sx, const double* __restrict__ x,
