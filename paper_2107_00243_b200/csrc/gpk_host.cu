@@ -27,6 +27,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gpk_internal.h"
@@ -404,6 +405,13 @@ struct gpk_ctx {
   DBuf<double> st_X[2], st_R[2], st_P[2], st_Z;
   DBuf<float> w_v32, w_f32, w_vhi, w_vlo;
   bool use_tc = false;  // GPK_PREC_TF32X3: value MVMs on the tcgen05 tensor cores
+  bool vmax_ready = false;  // w_vmax holds the column maxima of the next direction block
+  bool use_fused_cg = [] {  // env GPK_FUSED_CG=0 selects the unfused per-step kernels (A/B checks)
+    const char* e = std::getenv("GPK_FUSED_CG");
+    return !(e && std::atoi(e) == 0);
+  }();
+  DBuf<unsigned> w_cnt;
+  DBuf<double> w_prz, w_pzz;
   bool use_persistent_pchol = [] {  // env GPK_PCHOL_STEPS=1 selects the per-step kernels (A/B checks)
     const char* e = std::getenv("GPK_PCHOL_STEPS");
     return !(e && std::atoi(e) == 1);
@@ -650,9 +658,15 @@ struct gpk_ctx {
           w_h16lo.ensure(static_cast<size_t>(n_pad) * npad);
           w_vmax.ensure(tc);
           w_colscale.ensure(tc);
-          check_launch(gpk::launch_pack_v_f16(V + c0 * ldv, ldv, tc, n, n_pad, npad, o2, w_vmax.p, w_colscale.p,
-                                              w_h16hi.p, w_h16lo.p, st),
-                       2, "pack_v_f16");
+          if (vmax_ready && c0 == 0 && tc == t) {  // maxima from the fused CG p-update
+            check_launch(gpk::launch_pack_v_f16_only(V, ldv, tc, n, n_pad, npad, o2, w_vmax.p, w_colscale.p,
+                                                     w_h16hi.p, w_h16lo.p, st),
+                         1, "pack_v_f16");
+          } else {
+            check_launch(gpk::launch_pack_v_f16(V + c0 * ldv, ldv, tc, n, n_pad, npad, o2, w_vmax.p, w_colscale.p,
+                                                w_h16hi.p, w_h16lo.p, st),
+                         2, "pack_v_f16");
+          }
           const int nt64 = n_pad / 64;
           const int sg = splits_for_tcg();
           const int per64 = (nt64 + sg - 1) / sg;
@@ -692,6 +706,7 @@ struct gpk_ctx {
         entries += static_cast<long long>(nl) * n;
         flops += static_cast<long long>(fl);
       }
+      vmax_ready = false;
       return;
     }
     for (int c0 = 0; c0 < t; c0 += chunk) {
@@ -834,6 +849,7 @@ struct gpk_ctx {
     }
     int cur = 0;
     double *Xs = st_X[0].p, *Rs = st_R[0].p, *Ps = st_P[0].p, *Zs = st_Z.p;
+    double* Rspare = st_R[1].p;  // r is double-buffered by pointer (the fused x/r update writes a new block)
     gpk::SlotState* ss = w_ss[0].p;
     std::vector<gpk::SlotState> hs(t);
     for (int s = 0; s < t; ++s) {
@@ -889,7 +905,7 @@ struct gpk_ctx {
       if (nt > 0) {
         h2d(w_map.p, keep.data(), sizeof(int) * nt);
         check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, nl, nt, st_X[nb].p, ldn, st), 1, "compact");
-        check_launch(gpk::launch_gather_cols(Rs, ldn, w_map.p, 1.0, nl, nt, st_R[nb].p, ldn, st), 1, "compact");
+        check_launch(gpk::launch_gather_cols(Rs, ldn, w_map.p, 1.0, nl, nt, Rspare, ldn, st), 1, "compact");
         check_launch(gpk::launch_gather_cols(Ps, ldn, w_map.p, 1.0, nl, nt, st_P[nb].p, ldn, st), 1, "compact");
         std::vector<gpk::SlotState> ns(nt);
         for (int q = 0; q < nt; ++q) ns[q] = hs[keep[q]];
@@ -901,8 +917,9 @@ struct gpk_ctx {
       }
       cur = nb;
       Xs = st_X[cur].p;
-      Rs = st_R[cur].p;
+      if (nt > 0) std::swap(Rs, Rspare);
       Ps = st_P[cur].p;
+      vmax_ready = false;
       ss = w_ss[cur].p;
       ta = nt;
     };
@@ -944,9 +961,40 @@ struct gpk_ctx {
       }
     };
     handle_flags();  // zero right-hand sides finish with 0 iterations
+    // single-rank Woodbury path: the fused iteration (gpk_cgfused.cu)
+    const bool fused = use_fused_cg && world == 1 && pkind == 2 && k > 0;
+    if (fused) {
+      w_cnt.ensure(static_cast<size_t>(t) + 64);
+      CK(cudaMemsetAsync(w_cnt.p, 0, sizeof(unsigned) * (static_cast<size_t>(t) + 64), st));
+      const int nbx = gpk::g2_row_blocks(nl);
+      w_prz.ensure(static_cast<size_t>(t) * nbx);
+      w_pzz.ensure(static_cast<size_t>(t) * nbx);
+      w_g1.ensure(gpk::g1_workspace(nl, k, t));
+      w_W.ensure(static_cast<size_t>(k) * t);
+      w_vmax.ensure(t);
+    }
+    vmax_ready = false;
     for (int it = 1; it <= max_iters && ta > 0; ++it) {
       w_kx.ensure(static_cast<size_t>(ta) * ldn);
       apply_kernel(Ps, ldn, ta, w_kx.p, ldn, fp64, -1);  // K p (noise-free)
+      if (fused) {
+        check_launch(gpk::launch_cg_pap_alpha(Ps, w_kx.p, noise, nl, ldn, ta, ppap, w_cnt.p, it, ss, dh_a, max_iters,
+                                              st),
+                     1, "cg_pap_alpha");
+        check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, nl, ldn, ta, ss, st), 1, "cg_xr");
+        check_launch(gpk::launch_g1(L.p, n, k, Rs, ldn, ta, nl, w_g1.p, w_W.p, k, st), 2, "g1");
+        unsigned long long* vm = (!fp64 && use_tc && gram_ok && ta <= 96) ? w_vmax.p : nullptr;
+        check_launch(gpk::launch_g2_dots_beta(C.p, n, k, w_W.p, k, ta, nl, Zs, Rs, ldn, pnoise, w_prz.p, w_pzz.p,
+                                              w_cnt.p + t, it, rel_tol, ss, dh_b, dh_r, max_iters, vm, st),
+                     1, "g2_dots_beta");
+        check_launch(gpk::launch_cg_p_vmax(Ps, Zs, nl, ldn, ta, ss, vm, st), 1, "cg_p");
+        vmax_ready = vm != nullptr;
+        if (it % sync_every == 0 || it == max_iters) {
+          d2h(hs.data(), ss, sizeof(gpk::SlotState) * ta);
+          handle_flags();
+        }
+        continue;
+      }
       check_launch(gpk::launch_dot_partials(1, Ps, w_kx.p, noise, nl, ldn, ta, ppap, st), 1, "dots");
       const double* gpap = global_partials(ppap, nrb, ta, tot + 2 * t, &nrg);
       check_launch(gpk::launch_cg_alpha(gpap, nrg, ta, it, ss, dh_a, max_iters, st), 1, "cg_alpha");
@@ -965,6 +1013,7 @@ struct gpk_ctx {
         handle_flags();
       }
     }
+    vmax_ready = false;
     // columns that hit max_iters: not an error, converged = false (krylov.hpp:120)
     if (ta > 0) {
       std::vector<int> all;
@@ -1165,12 +1214,17 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   const double* U = Xs.p;
   const double* S = Xs.p + ldn;
 
-  // ---- SLQ per probe (trace_estimation.hpp:163-176) on the host
+  // ---- SLQ per probe (trace_estimation.hpp:163-176) on the host: the l tridiagonal
+  // eigen-solves run on host threads while the device works on the backward pass; the
+  // value is finished after the join (same per-probe arithmetic, fixed-order sums).
   std::vector<double> gam(l);
-  for (int i = 0; i < l; ++i) {
+  std::vector<std::string> slq_err(l);
+  auto slq_probe = [&](int i) {
     const int col = 1 + i;
     const int m = cg.iters[col];
     std::vector<double> dg, sb;
+    dg.reserve(m);
+    sb.reserve(m);
     for (int kk = 1; kk <= m; ++kk) {  // krylov.hpp:85-92
       const double a = ah[static_cast<size_t>(col) * mi + kk - 1];
       double dv = 1.0 / a;
@@ -1185,24 +1239,46 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
     try {
       gam[i] = slq_log(dg, sb).value;
     } catch (const GpkError& e) {
-      fail(GPK_NUMERICAL_ERROR, "vr_logdet: probe " + std::to_string(i) + ": " + e.msg);
+      slq_err[i] = e.msg;
     }
-    if (res->forward_cg_iterations) res->forward_cg_iterations[i] = m;
-    if (res->forward_gammas) res->forward_gammas[i] = gam[i];
+  };
+  std::vector<std::thread> slq_threads;
+  {
+    const int nth = std::max(1, std::min<int>(l, std::min(16u, std::max(1u, std::thread::hardware_concurrency()))));
+    for (int th = 0; th < nth; ++th)
+      slq_threads.emplace_back([&slq_probe, l, nth, th] {
+        for (int i = th; i < l; i += nth) slq_probe(i);
+      });
   }
-  const double plogdet = c->pkind == 1 ? 0.0 : c->plogdet;
-  double stoch = 0.0;  // finish_estimate (trace_estimation.hpp:132-141)
-  for (double g : gam) stoch += g;
-  stoch *= static_cast<double>(n) / static_cast<double>(l);
-  std::vector<double> scaled(l);
-  for (int i = 0; i < l; ++i) scaled[i] = static_cast<double>(n) * gam[i];
-  res->value_sample_variance = unbiased_variance(scaled);
-  res->logdet = plogdet + stoch;
-  res->logdet_precond = plogdet;
+  auto finish_forward = [&]() {
+    for (auto& th : slq_threads) th.join();
+    slq_threads.clear();
+    for (int i = 0; i < l; ++i) {
+      if (!slq_err[i].empty()) fail(GPK_NUMERICAL_ERROR, "vr_logdet: probe " + std::to_string(i) + ": " + slq_err[i]);
+      if (res->forward_cg_iterations) res->forward_cg_iterations[i] = cg.iters[1 + i];
+      if (res->forward_gammas) res->forward_gammas[i] = gam[i];
+    }
+    const double plogdet = c->pkind == 1 ? 0.0 : c->plogdet;
+    double stoch = 0.0;  // finish_estimate (trace_estimation.hpp:132-141)
+    for (double g : gam) stoch += g;
+    stoch *= static_cast<double>(n) / static_cast<double>(l);
+    std::vector<double> scaled(l);
+    for (int i = 0; i < l; ++i) scaled[i] = static_cast<double>(n) * gam[i];
+    res->value_sample_variance = unbiased_variance(scaled);
+    res->logdet = plogdet + stoch;
+    res->logdet_precond = plogdet;
+    const double kPi = 3.14159265358979323846;
+    res->value = -0.5 * (res->quad + res->logdet + static_cast<double>(n) * std::log(2.0 * kPi));
+  };
+  struct JoinGuard {  // never leave the SLQ threads running on an error path
+    std::vector<std::thread>& t;
+    ~JoinGuard() {
+      for (auto& th : t)
+        if (th.joinable()) th.join();
+    }
+  } slq_guard{slq_threads};
   const double quad = c->col_dots(dy + r0, U, 1, ldn)[0];  // y.u
   res->quad = quad;
-  const double kPi = 3.14159265358979323846;
-  res->value = -0.5 * (quad + res->logdet + static_cast<double>(n) * std::log(2.0 * kPi));
   res->solve_iterations = cg.iters[0];
   res->total_cg_iterations = 0;
   for (int col = 0; col < t; ++col) res->total_cg_iterations += cg.iters[col];
@@ -1242,31 +1318,36 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         require(c->have_dl, "DiagPlusLowRank: derivative factors not attached");
         const int k = c->k;
         // [Q Zc] is contiguous: columns 0..l-1 of Q then Zc (separate buffers -> two G1s)
-        DBuf<double> A, Bw, part;
+        DBuf<double> A, part;
         A.ensure(static_cast<size_t>(2) * l * k);
-        Bw.ensure(static_cast<size_t>(2) * l * k);
         part.ensure(gpk::g1_workspace(nl, k, l));
         c->check_launch(gpk::launch_g1(c->L.p + r0, n, k, Q.p, ldn, l, nl, part.p, A.p, k, c->st), 2, "g1");
         c->check_launch(gpk::launch_g1(c->L.p + r0, n, k, Zc.p, ldn, l, nl, part.p, A.p + static_cast<size_t>(l) * k,
                                        k, c->st),
                         2, "g1");
         c->allreduce_sum(A.p, 2LL * l * k);
-        std::vector<double> hA(static_cast<size_t>(2) * l * k), hB(static_cast<size_t>(2) * l * k);
+        std::vector<double> hA(static_cast<size_t>(2) * l * k);
         c->d2h(hA.data(), A.p, sizeof(double) * hA.size());
+        // all d+1 derivative factors at once: dL is [w][n x k], i.e. one n x (d+1)k matrix
+        const int kw = (d + 1) * k;
+        DBuf<double> Bq, Bz, partw;
+        Bq.ensure(static_cast<size_t>(l) * kw);
+        Bz.ensure(static_cast<size_t>(l) * kw);
+        partw.ensure(gpk::g1_workspace(nl, kw, l));
+        c->check_launch(gpk::launch_g1(c->dL.p + r0, n, kw, Q.p, ldn, l, nl, partw.p, Bq.p, kw, c->st), 2, "g1");
+        c->check_launch(gpk::launch_g1(c->dL.p + r0, n, kw, Zc.p, ldn, l, nl, partw.p, Bz.p, kw, c->st), 2, "g1");
+        c->allreduce_sum(Bq.p, static_cast<long long>(l) * kw);
+        c->allreduce_sum(Bz.p, static_cast<long long>(l) * kw);
+        std::vector<double> hq(static_cast<size_t>(l) * kw), hz(static_cast<size_t>(l) * kw);
+        CK(cudaMemcpyAsync(hq.data(), Bq.p, sizeof(double) * hq.size(), cudaMemcpyDeviceToHost, c->st));
+        c->d2h(hz.data(), Bz.p, sizeof(double) * hz.size());
         for (int w = 0; w <= d; ++w) {
           tdet[w] = c->trace_det[w];
-          const double* dLw = c->dL.p + static_cast<size_t>(w) * n * k;
-          c->check_launch(gpk::launch_g1(dLw + r0, n, k, Q.p, ldn, l, nl, part.p, Bw.p, k, c->st), 2, "g1");
-          c->check_launch(
-              gpk::launch_g1(dLw + r0, n, k, Zc.p, ldn, l, nl, part.p, Bw.p + static_cast<size_t>(l) * k, k, c->st),
-              2, "g1");
-          c->allreduce_sum(Bw.p, 2LL * l * k);
-          c->d2h(hB.data(), Bw.p, sizeof(double) * hB.size());
           for (int i = 0; i < l; ++i) {
             // (dL' q_i).(L' z_i) + (L' q_i).(dL' z_i)   (LowRankDerivOp::apply, preconditioners.hpp:62-69)
             double acc = 0.0;
-            const double* bq = hB.data() + static_cast<size_t>(i) * k;
-            const double* bz = hB.data() + static_cast<size_t>(l + i) * k;
+            const double* bq = hq.data() + static_cast<size_t>(i) * kw + static_cast<size_t>(w) * k;
+            const double* bz = hz.data() + static_cast<size_t>(i) * kw + static_cast<size_t>(w) * k;
             const double* aq = hA.data() + static_cast<size_t>(i) * k;
             const double* az = hA.data() + static_cast<size_t>(l + i) * k;
             for (int q = 0; q < k; ++q) acc += bq[q] * az[q] + aq[q] * bz[q];
@@ -1452,6 +1533,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
     }
   }
   CK(cudaEventRecord(e2, c->st));
+  finish_forward();  // join the SLQ threads, finish the value (overlapped with the backward pass)
   c->sync();
   float ms1 = 0, ms2 = 0;
   CK(cudaEventElapsedTime(&ms1, e0, e1));

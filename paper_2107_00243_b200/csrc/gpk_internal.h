@@ -67,6 +67,8 @@ cudaError_t launch_gram_pack(const double* X, long long ldx, int n, int d, int n
 // V (t <= 96 columns) -> per-column power-of-two scaled fp16 hi/lo tiles (+ colscale_c =
 // scale / (2^10 sigma_c) applied to the output); vmax: t uint64 scratch, colscale: t doubles.
 int tcg_npad(int t);  // padded column count (multiple of 8, <= 96), -1 if t > 96
+cudaError_t launch_pack_v_f16_only(const double* V, long long ldv, int t, int n, int n_pad, int npad, double scale,
+                                   const void* vmax, double* colscale, void* vhi, void* vlo, cudaStream_t st);
 cudaError_t launch_pack_v_f16(const double* V, long long ldv, int t, int n, int n_pad, int npad, double scale,
                               void* vmax, double* colscale, void* vhi, void* vlo, cudaStream_t st);
 cudaError_t launch_fused_kmvm_tcg(int family, int d, const float* xh, const float* xl, const float* xn,

@@ -386,6 +386,16 @@ __global__ void g1_reduce_kernel(const double* __restrict__ part, int nch, int k
   }
 }
 
+int g1_chunk_rows(int n) { return g1_chunk(n); }
+
+cudaError_t launch_g1_reduce(const double* part, int n, int ka, int tb, double* W, long long ldw, cudaStream_t st) {
+  const int ch = g1_chunk(n);
+  const int nch = (n + ch - 1) / ch;
+  const long long tot = static_cast<long long>(ka) * tb;
+  g1_reduce_kernel<<<static_cast<unsigned>((tot + 63) / 64), 256, 0, st>>>(part, nch, ka, tb, W, ldw);
+  return cudaGetLastError();
+}
+
 size_t g1_workspace(int n, int ka, int tb) {
   const int ch = g1_chunk(n);
   return static_cast<size_t>((n + ch - 1) / ch) * ka * tb;

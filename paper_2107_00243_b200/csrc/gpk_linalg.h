@@ -47,6 +47,23 @@ cudaError_t launch_woodbury_apply(const double* C, long long ldc, int ka, const 
                                   const double* R, long long ldr, double sig2, int tb, int n, double* Z,
                                   long long ldz, cudaStream_t st);
 
+// gpk_cgfused.cu: the fused single-rank CG iteration (see the file header)
+int g1_chunk_rows(int n);
+cudaError_t launch_g1_reduce(const double* part, int n, int ka, int tb, double* W, long long ldw, cudaStream_t st);
+int g2_row_blocks(int n);
+cudaError_t launch_cg_pap_alpha(const double* P, const double* Y, double sig2, int n, long long ldn, int t,
+                                double* part, unsigned* cnt, int k, SlotState* ss, double* alpha_hist, int max_iters,
+                                cudaStream_t st);
+cudaError_t launch_g1_xr(const double* L, long long ldl, int ka, double* X, const double* R, double* Rn,
+                         const double* P, const double* Y, double sig2, long long ldn, int tb, int n,
+                         const SlotState* ss, double* part, double* W, long long ldw, cudaStream_t st);
+cudaError_t launch_g2_dots_beta(const double* C, long long ldc, int ka, const double* W, long long ldw, int tb, int n,
+                                double* Z, const double* R, long long ldn, double sig2, double* prz, double* pzz,
+                                unsigned* cnt, int k, double rel_tol, SlotState* ss, double* beta_hist,
+                                double* resid_hist, int max_iters, unsigned long long* vmax, cudaStream_t st);
+cudaError_t launch_cg_p_vmax(double* P, const double* Z, int n, long long ldn, int t, const SlotState* ss,
+                             unsigned long long* vmax, cudaStream_t st);
+
 int pchol_blocks(int n);
 struct PivotState {
   double dp;        // remaining diagonal at the current pivot

@@ -126,6 +126,16 @@ cudaError_t launch_pack_v_f16(const double* V, long long ldv, int t, int n, int 
   return cudaGetLastError();
 }
 
+// pack only, with column maxima already in vmax (the fused CG p-update computed them)
+cudaError_t launch_pack_v_f16_only(const double* V, long long ldv, int t, int n, int n_pad, int npad, double scale,
+                                   const void* vmax, double* colscale, void* vhi, void* vlo, cudaStream_t st) {
+  const long long total = static_cast<long long>(n_pad) * npad;
+  pack_v_f16_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+      V, ldv, t, n, n_pad, npad, static_cast<const unsigned long long*>(vmax), scale, colscale,
+      static_cast<__half*>(vhi), static_cast<__half*>(vlo));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fused_kmvm_tcg(int family, int d, const float* xh, const float* xl, const float* xn,
                                   const float* x32, const void* vhi, const void* vlo, const double* colscale,
                                   double* out, const MvmArgs& a, int splits, cudaStream_t st) {
