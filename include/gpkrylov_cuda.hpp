@@ -128,6 +128,7 @@ class KernelOperator {
   int num_params() const { return dim() + 2; }
   const Hyperparameters& params() const { return params_; }
   gpk_ctx* ctx() const { return ctx_.get(); }
+  KernelFamily family() const { return fam_; }
 
   // (K + sigma^2 I) V, t columns (kernels.hpp:184-195)
   std::vector<double> apply(const std::vector<double>& v, int t = 1, gpk_precision prec = GPK_PREC_FP64) const {
@@ -258,6 +259,100 @@ inline MllEvaluation evaluate_mll(const std::vector<double>& y, const KernelOper
   out.backward_gammas.assign(static_cast<size_t>(np), std::vector<double>(static_cast<size_t>(l)));
   for (int w = 0; w < np; ++w)
     for (int i = 0; i < l; ++i) out.backward_gammas[w][i] = bg[static_cast<size_t>(w) * l + i];
+  return out;
+}
+
+// ---- the callers of the hot path ---------------------------
+
+struct ExactMll {  // gp_likelihood.hpp:119-122
+  double value = 0.0;
+  std::vector<double> gradient;
+};
+// mll_exact (gp_likelihood.hpp:124-146): dense fp64 on the device (cuSOLVER Cholesky)
+inline ExactMll mll_exact(const std::vector<double>& y, const KernelOperator& k, bool with_gradient = true) {
+  ExactMll out;
+  if (with_gradient) out.gradient.assign(static_cast<size_t>(k.num_params()), 0.0);
+  check(gpk_mll_exact(k.ctx(), y.data(), &out.value, with_gradient ? out.gradient.data() : nullptr), k.ctx());
+  return out;
+}
+
+// run_training_arm's predictive mean (experiments.hpp:403-414): cross_kernel(test, X) K_hat^{-1} y
+// with the preconditioner attached to k; x_test is n_test x d column-major
+inline std::vector<double> predict_mean(const KernelOperator& k, const std::vector<double>& y,
+                                        const std::vector<double>& x_test, std::int64_t n_test, const CgConfig& cfg) {
+  std::vector<double> mean(static_cast<size_t>(n_test));
+  const gpk_cg_cfg c = cfg.c();
+  check(gpk_predict_mean(k.ctx(), y.data(), x_test.data(), n_test, n_test, &c, mean.data(), nullptr), k.ctx());
+  return mean;
+}
+
+struct OptOptions {  // optimizer.hpp:24-43
+  gpk_opt_method method = GPK_OPT_LBFGS;
+  int max_steps = 20, lbfgs_memory = 10;
+  double armijo_c1 = 1e-4, wolfe_c2 = 0.9, adam_lr = 0.1;
+  int early_stop_patience = 3;
+  double grad_tol = 1e-8;
+  int max_line_search = 20;
+  gpk_opt_options c() const {
+    return gpk_opt_options{method, max_steps, lbfgs_memory, armijo_c1, wolfe_c2, adam_lr, early_stop_patience,
+                           grad_tol, max_line_search};
+  }
+};
+
+struct OptimizeResult {  // optimizer.hpp:356-361 (+ MinimizeResult, the step trace)
+  Hyperparameters best;
+  double best_validation = 0.0, final_train_neg_mll_per_point = 0.0, final_objective = 0.0;
+  int minimizer_steps = 0, stop_reason = 0;
+  bool converged = false;
+  std::vector<std::vector<double>> step_theta;
+  std::vector<double> step_objective, step_validation, step_wall_time;
+  std::vector<int> step_accepted;
+  long long model_evaluations = 0;
+};
+
+// optimize() (optimizer.hpp:404-505) on the device: train / validation are operators holding the
+// data (the validation operator may be null); precond_rank < 0 selects IdentityPreconditioner.
+inline OptimizeResult optimize(KernelOperator& train, const std::vector<double>& y, KernelOperator* validation,
+                               const std::vector<double>* y_val, bool ard, const Hyperparameters& init,
+                               int precond_rank, int probe_count, const OptOptions& opts, const MllConfig& mll,
+                               std::uint64_t seed, std::int64_t dense_limit = 4096, double diag_tol = 0.0) {
+  const int d = train.dim(), np = ard ? d + 2 : 3, ms = opts.max_steps;
+  std::vector<double> theta0{init.log_outputscale};
+  theta0.insert(theta0.end(), init.log_lengthscales.begin(), init.log_lengthscales.end());
+  theta0.push_back(init.log_noise);
+  std::vector<double> best(static_cast<size_t>(d + 2)), th(static_cast<size_t>(ms) * np), obj(ms), val(ms), wall(ms);
+  std::vector<int> acc(ms);
+  gpk_opt_result r{};
+  r.best_log_params = best.data();
+  r.step_theta = th.data();
+  r.step_objective = obj.data();
+  r.step_validation = val.data();
+  r.step_wall_time = wall.data();
+  r.step_accepted = acc.data();
+  const gpk_opt_options oc = opts.c();
+  const gpk_mll_cfg mc{mll.solver.c(), mll.share_probes ? 1 : 0, 1, mll.backward_mode};
+  check(gpk_optimize(train.ctx(), y.data(), validation ? validation->ctx() : nullptr,
+                     y_val ? y_val->data() : nullptr, static_cast<int>(train.family()), ard ? 1 : 0, theta0.data(),
+                     precond_rank, diag_tol, probe_count, &oc, &mc, seed, dense_limit, &r),
+        train.ctx());
+  OptimizeResult out;
+  out.best.log_outputscale = best[0];
+  out.best.log_lengthscales.assign(best.begin() + 1, best.begin() + 1 + d);
+  out.best.log_noise = best[static_cast<size_t>(d + 1)];
+  out.best_validation = r.best_validation;
+  out.final_train_neg_mll_per_point = r.final_train_neg_mll_per_point;
+  out.final_objective = r.final_objective;
+  out.minimizer_steps = r.minimizer_steps;
+  out.stop_reason = r.stop_reason;
+  out.converged = r.converged != 0;
+  out.model_evaluations = r.n_evaluations;
+  for (int s = 0; s < r.n_steps; ++s) {
+    out.step_theta.emplace_back(th.begin() + static_cast<long>(s) * np, th.begin() + static_cast<long>(s + 1) * np);
+    out.step_objective.push_back(obj[s]);
+    out.step_validation.push_back(val[s]);
+    out.step_wall_time.push_back(wall[s]);
+    out.step_accepted.push_back(acc[s]);
+  }
   return out;
 }
 

@@ -34,7 +34,17 @@ int main() {
   for (size_t w = 0; w < e.gradient.size(); ++w) std::printf("%s%.17g", w ? ", " : "", e.gradient[w]);
   std::printf("], \"pivots\": [");
   for (size_t s = 0; s < prec.pivots().size(); ++s) std::printf("%s%lld", s ? ", " : "", (long long)prec.pivots()[s]);
-  std::printf("], \"seed\": %llu}\n", (unsigned long long)batch.seed);
+  std::printf("], \"seed\": %llu", (unsigned long long)batch.seed);
+  // the callers: dense exact mLL and a 3-step Adam optimize()
+  const ExactMll ex = mll_exact(y, op, false);
+  std::printf(", \"exact\": %.17g", ex.value);
+  OptOptions oo;
+  oo.method = GPK_OPT_ADAM;
+  oo.max_steps = 3;
+  const OptimizeResult opt = optimize(op, y, nullptr, nullptr, true, p, rank, l, oo, cfg, 17);
+  std::printf(", \"opt_best\": [%.17g", opt.best.log_outputscale);
+  for (double v : opt.best.log_lengthscales) std::printf(", %.17g", v);
+  std::printf(", %.17g], \"opt_evals\": %lld}\n", opt.best.log_noise, opt.model_evaluations);
   // error mapping: a bad hyperparameter index is an input_error
   try {
     op.deriv_apply(7, y);

@@ -43,3 +43,9 @@ def test_facade_cpp_caller_matches_oracle(tmp_path, orc):
     assert got["pivots"] == list(ref_piv)
     assert got["value"] == pytest.approx(want["value"], rel=1e-9)
     np.testing.assert_allclose(got["gradient"], want["gradient"], rtol=1e-7, atol=1e-9)
+    # SURVEY.md §8(f) through the facade: dense exact mLL, optimize()
+    assert got["exact"] == pytest.approx(orc.mll_exact_value(orc.MATERN52, x, p, y), rel=1e-10)
+    opt = orc.optimize(orc.MATERN52, x, y, None, None, p, rank=12, probe_count=l, max_iters=400, rel_tol=1e-10,
+                       seed=17, method=1, max_steps=3)
+    assert got["opt_evals"] == len(opt["evaluations"])
+    np.testing.assert_allclose(got["opt_best"], opt["best"], rtol=1e-6, atol=1e-7)
