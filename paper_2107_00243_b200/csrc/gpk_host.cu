@@ -433,6 +433,7 @@ struct gpk_ctx {
     return v >= 0 && v <= 2 ? v : 0;
   }();
   bool gram_ok = false;   // the value MVMs of the tf32x3 path use the Gram kernel
+  bool tcg_direct = false;  // ... or the same tcgen05 pipeline with direct-difference distances (d <= 8)
   float gram_maxnorm = 0.0f;
   DBuf<float> Xgh, Xgl, Xgn;
   DBuf<double> Xgmu;
@@ -554,6 +555,7 @@ struct gpk_ctx {
                                     sx.p, sq.p, st),
                  1, "pack_x");
     gram_ok = false;
+    tcg_direct = false;
     // Gram variant: RBF / Matern-3/2 / Matern-5/2, d <= 32, and centred pre-scaled
     // coordinates small enough that the expanded-distance cancellation stays at the
     // fp32 level (max |x~|^2 <= kGramMaxNorm; see gpk_mvm_tcg.cuh).
@@ -571,6 +573,8 @@ struct gpk_ctx {
       for (float v : nr) gram_maxnorm = std::max(gram_maxnorm, v);
       gram_ok = mvm_variant == GPK_MVM_GRAM || (gram_maxnorm <= kGramMaxNorm && d >= kGramMinDim);
     }
+    // low dimension (or Matern-1/2, or large norms): direct differences on the tcgen05 pipeline
+    tcg_direct = !gram_ok && mvm_variant != GPK_MVM_GRAM && dp <= 8;
     packed = true;
   }
   static constexpr float kGramMaxNorm = 320.0f;
@@ -640,7 +644,8 @@ struct gpk_ctx {
     const int per = (ntiles + splits - 1) / splits;
     const long long ldp = (nl + 127) / 128 * 128;  // split-K partial leading dimension (local rows)
     if (!fp64 && use_tc && which < 0) {  // tcgen05 path (value mode)
-      const int cmax = gram_ok ? 96 : 128;
+      const bool tcg = gram_ok || tcg_direct;  // the gpk_mvm_tcg.cuh pipeline
+      const int cmax = tcg ? 96 : 128;
       for (int c0 = 0; c0 < t; c0 += cmax) {
         const int tc = std::min(cmax, t - c0);
         gpk::MvmArgs a{};
@@ -652,7 +657,7 @@ struct gpk_ctx {
         a.row_begin = r0;
         a.row_end = r1;
         int sp = splits;
-        if (gram_ok) {  // Gram variant: 64-wide j-tiles, fp16 V with per-column scales
+        if (tcg) {  // 64-wide j-tiles, fp16 V with per-column scales
           const int npad = gpk::tcg_npad(tc);
           w_h16hi.ensure(static_cast<size_t>(n_pad) * npad);
           w_h16lo.ensure(static_cast<size_t>(n_pad) * npad);
@@ -686,7 +691,9 @@ struct gpk_ctx {
         const double fl = static_cast<double>(nl) * n * (2.0 * tc + 3.0 * d + cf[family]);
         auto ev = prof_begin(0);
         auto launch = [&](double* o, int nsp) {
-          return gram_ok ? gpk::launch_fused_kmvm_tcg(family, d, Xgh.p, Xgl.p, Xgn.p, X32.p, w_h16hi.p, w_h16lo.p,
+          return tcg ? gpk::launch_fused_kmvm_tcg(family, d, gram_ok ? 0 : dp, gram_ok ? Xgh.p : X32.p,
+                                                  gram_ok ? Xgl.p : X32.p, gram_ok ? Xgn.p : X32.p, X32.p, w_h16hi.p,
+                                                  w_h16lo.p,
                                                       w_colscale.p, o, a, nsp, st)
                          : gpk::launch_fused_kmvm_tc(family, dp, X32.p, w_vhi.p, w_vlo.p, o, a, nsp, st);
         };
@@ -983,7 +990,7 @@ struct gpk_ctx {
                      1, "cg_pap_alpha");
         check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, nl, ldn, ta, ss, st), 1, "cg_xr");
         check_launch(gpk::launch_g1(L.p, n, k, Rs, ldn, ta, nl, w_g1.p, w_W.p, k, st), 2, "g1");
-        unsigned long long* vm = (!fp64 && use_tc && gram_ok && ta <= 96) ? w_vmax.p : nullptr;
+        unsigned long long* vm = (!fp64 && use_tc && (gram_ok || tcg_direct) && ta <= 96) ? w_vmax.p : nullptr;
         check_launch(gpk::launch_g2_dots_beta(C.p, n, k, w_W.p, k, ta, nl, Zs, Rs, ldn, pnoise, w_prz.p, w_pzz.p,
                                               w_cnt.p + t, it, rel_tol, ss, dh_b, dh_r, max_iters, vm, st),
                      1, "g2_dots_beta");

@@ -71,9 +71,10 @@ cudaError_t launch_pack_v_f16_only(const double* V, long long ldv, int t, int n,
                                    const void* vmax, double* colscale, void* vhi, void* vlo, cudaStream_t st);
 cudaError_t launch_pack_v_f16(const double* V, long long ldv, int t, int n, int n_pad, int npad, double scale,
                               void* vmax, double* colscale, void* vhi, void* vlo, cudaStream_t st);
-cudaError_t launch_fused_kmvm_tcg(int family, int d, const float* xh, const float* xl, const float* xn,
-                                  const float* x32, const void* vhi, const void* vlo, const double* colscale,
-                                  double* out, const MvmArgs& a, int splits, cudaStream_t st);
+cudaError_t launch_fused_kmvm_tcg(int family, int d, int direct_dp, const float* xh, const float* xl,
+                                  const float* xn, const float* x32, const void* vhi, const void* vlo,
+                                  const double* colscale, double* out, const MvmArgs& a, int splits,
+                                  cudaStream_t st);
 
 // Reference-formula kernel column (kernels.hpp:235-243) / derivative column (:252-267), fp64.
 // which < 0: K[:, p];  which == 0: outputscale;  1..d: lengthscale which-1.

@@ -8,9 +8,9 @@
 namespace gpk {
 namespace tcg {
 template <int FAM>
-cudaError_t launch_tcg_fam(int ks, int nc8, const float* Xh, const float* Xl, const float* Xn, const float* X32,
-                           const __half* Vhi, const __half* Vlo, const double* colscale, double* out,
-                           const MvmArgs& a, dim3 g, cudaStream_t st);
+cudaError_t launch_tcg_fam(int ks, int dpd, int nc8, const float* Xh, const float* Xl, const float* Xn,
+                           const float* X32, const __half* Vhi, const __half* Vlo, const double* colscale,
+                           double* out, const MvmArgs& a, dim3 g, cudaStream_t st);
 }
 
 // mu[k] = mean_i X[i, k] / l_k (fixed-order block reduction, one block per coordinate)
@@ -136,9 +136,10 @@ cudaError_t launch_pack_v_f16_only(const double* V, long long ldv, int t, int n,
   return cudaGetLastError();
 }
 
-cudaError_t launch_fused_kmvm_tcg(int family, int d, const float* xh, const float* xl, const float* xn,
-                                  const float* x32, const void* vhi, const void* vlo, const double* colscale,
-                                  double* out, const MvmArgs& a, int splits, cudaStream_t st) {
+cudaError_t launch_fused_kmvm_tcg(int family, int d, int direct_dp, const float* xh, const float* xl,
+                                  const float* xn, const float* x32, const void* vhi, const void* vlo,
+                                  const double* colscale, double* out, const MvmArgs& a, int splits,
+                                  cudaStream_t st) {
   const int npad = tcg_npad(a.t);
   if (npad < 0 || d < 1 || d > 32) return cudaErrorInvalidValue;
   const int ks = (d + 7) / 8;
@@ -146,12 +147,14 @@ cudaError_t launch_fused_kmvm_tcg(int family, int d, const float* xh, const floa
   const int nc8 = npad / 8;
   const __half* h = static_cast<const __half*>(vhi);
   const __half* l = static_cast<const __half*>(vlo);
+  const int dd = direct_dp;
   switch (family) {
-    case kRBF: return tcg::launch_tcg_fam<kRBF>(ks, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
-    case kMatern32: return tcg::launch_tcg_fam<kMatern32>(ks, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
-    case kMatern52: return tcg::launch_tcg_fam<kMatern52>(ks, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
+    case kRBF: return tcg::launch_tcg_fam<kRBF>(ks, dd, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
+    case kMatern12: return tcg::launch_tcg_fam<kMatern12>(ks, dd, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
+    case kMatern32: return tcg::launch_tcg_fam<kMatern32>(ks, dd, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
+    case kMatern52: return tcg::launch_tcg_fam<kMatern52>(ks, dd, nc8, xh, xl, xn, x32, h, l, colscale, out, a, g, st);
   }
-  return cudaErrorInvalidValue;  // Matern-1/2 stays on the direct-difference kernels
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace gpk

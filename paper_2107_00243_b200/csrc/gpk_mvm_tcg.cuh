@@ -114,7 +114,10 @@ GPK_DEV uint32_t elect_one() {
 }
 GPK_DEV uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
-template <int FAM, int KS, int NC8>
+// DPD > 0: direct-difference mode (no Gram MMA): s_ij from the fp32 rows of X32 staged in
+// shared memory (DPD = the padded coordinate count, <= 8) -- the low-dimensional / Matern-1/2
+// path, sharing the pipeline, the fp16 split and the K_tile V_j contraction.
+template <int FAM, int KS, int NC8, int DPD>
 __global__ void __launch_bounds__(THREADS, 1)
     fused_kmvm_tcg_kernel(const float* __restrict__ Xh, const float* __restrict__ Xl, const float* __restrict__ Xn,
                           const float* __restrict__ X32, const __half* __restrict__ Vhi,
@@ -122,6 +125,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                           double* __restrict__ out, MvmArgs a) {
   constexpr int NPAD = 8 * NC8;
   static_assert(NPAD <= MAX_NPAD, "NPAD");
+  constexpr bool DIRECT = DPD > 0;
+  static_assert(DPD % 4 == 0 && DPD <= 8, "DPD");
   constexpr uint32_t VTILE = NPAD * BK * 2;  // fp16 V_j tile (hi or lo)
   constexpr int HC = (NC8 + RPT - 1) / RPT;
   constexpr uint32_t TMEM_COLS = 512;
@@ -205,11 +210,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait_sleep(&xv_empty[s], ((it / SG) & 1) ^ 1);
       if (elect_one()) {
         const long long jt = jt0 + it;
-        mbar_arrive_expect_tx(&xv_full[s], 2 * XG_TILE + BK * 4 + 2 * VTILE + xjb);
-        bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
-        bulk_g2s(sbase + (sBx - base) + (s * 2 + 0) * XG_TILE, Xh + jt * (BK * 32), XG_TILE, &xv_full[s]);
-        bulk_g2s(sbase + (sBx - base) + (s * 2 + 1) * XG_TILE, Xl + jt * (BK * 32), XG_TILE, &xv_full[s]);
-        bulk_g2s(sbase + (sN - base) + s * BK * 4, Xn + jt * BK, BK * 4, &xv_full[s]);
+        if constexpr (DIRECT) {
+          mbar_arrive_expect_tx(&xv_full[s], 2 * VTILE + xjb);
+          bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
+        } else {
+          mbar_arrive_expect_tx(&xv_full[s], 2 * XG_TILE + BK * 4 + 2 * VTILE + xjb);
+          bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
+          bulk_g2s(sbase + (sBx - base) + (s * 2 + 0) * XG_TILE, Xh + jt * (BK * 32), XG_TILE, &xv_full[s]);
+          bulk_g2s(sbase + (sBx - base) + (s * 2 + 1) * XG_TILE, Xl + jt * (BK * 32), XG_TILE, &xv_full[s]);
+          bulk_g2s(sbase + (sN - base) + s * BK * 4, Xn + jt * BK, BK * 4, &xv_full[s]);
+        }
         bulk_g2s(sbase + (sV - base) + (s * 2 + 0) * VTILE, Vhi + jt * NPAD * BK, VTILE, &xv_full[s]);
         bulk_g2s(sbase + (sV - base) + (s * 2 + 1) * VTILE, Vlo + jt * NPAD * BK, VTILE, &xv_full[s]);
       }
@@ -220,8 +230,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (nt > 0) {
       constexpr uint32_t idesc_v = idesc_f16(NPAD);
       constexpr uint32_t idesc_g = tc::idesc_tf32(BK);
-      mbar_wait_sleep(ax_ready, 0);
+      if constexpr (!DIRECT) mbar_wait_sleep(ax_ready, 0);
       auto gram = [&](int k) {
+        if constexpr (DIRECT) return;
         const int s = k % SG, gb = k & 1;
         mbar_wait_sleep(&xv_full[s], (k / SG) & 1);
         mbar_wait_sleep(&g_empty[gb], ((k >> 1) & 1) ^ 1);
@@ -280,10 +291,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = pw >> 2;     // 16-column slice of the j-tile, and column-chunk subset of the drain
     const int r = lg * 32 + lane;
     const int row = row0 + r;
-    const float ni = Xn[row];
+    const float ni = DIRECT ? 0.0f : Xn[row];
     const float2 ni2 = make_float2(ni, ni);
     const uint32_t tlane = static_cast<uint32_t>(lg * 32) << 16;
-    {  // this row's centred coordinates (tf32 hi / lo, columns q*8 .. q*8+7) -> A_x in TMEM
+    if constexpr (!DIRECT) {  // this row's centred coordinates (tf32 hi / lo, columns q*8 .. q*8+7) -> A_x in TMEM
       const long long rb = static_cast<long long>(row >> 3) * 256 + (row & 7) * 32;
       uint32_t h8[8], l8[8];
 #pragma unroll
@@ -303,7 +314,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     double acc64[HC * 8];
 #pragma unroll
     for (int e = 0; e < HC * 8; ++e) acc64[e] = 0.0;
-    if (nt > 0) mbar_wait_sleep(xi_full, 0);  // the CTA's fp32 rows (guard path)
+    if (nt > 0) mbar_wait_sleep(xi_full, 0);  // the CTA's fp32 rows (guard path / direct mode)
+    float xi[DIRECT ? DPD : 1];
+    if constexpr (DIRECT) {
+#pragma unroll
+      for (int k4 = 0; k4 < DPD / 4; ++k4) {
+        const float4 v = reinterpret_cast<const float4*>(XIs + r * DPD)[k4];
+        xi[4 * k4] = v.x;
+        xi[4 * k4 + 1] = v.y;
+        xi[4 * k4 + 2] = v.z;
+        xi[4 * k4 + 3] = v.w;
+      }
+    }
     auto drain = [&](int g) {
       const int buf = g & 1;
       mbar_wait_sleep(&acc_full[buf], (g >> 1) & 1);
@@ -327,13 +349,35 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int s = it % SG, as = it % AS, gb = it & 1;
       const int jb = (jt0 + it) * BK + q * JPT;  // global index of this thread's first column
       if (threadIdx.x == 64) GPK_TRACE(1, it);
-      mbar_wait_sleep(&g_full[gb], (it >> 1) & 1);
+      if constexpr (!DIRECT) mbar_wait_sleep(&g_full[gb], (it >> 1) & 1);
       if (threadIdx.x == 64) GPK_TRACE(2, it);
       tc::tc_fence_after();
       mbar_wait_sleep(&xv_full[s], (it / SG) & 1);  // |x_j|^2 of this stage visible to the generic proxy
       mbar_wait_sleep(&a_empty[as], ((it / AS) & 1) ^ 1);
 #pragma unroll
       for (int hf8 = 0; hf8 < 2; ++hf8) {  // two halves of 8 entries: Gram -> s -> entry -> TMEM
+        float sv[8];
+        if constexpr (DIRECT) {  // fp32 direct differences, two entries per paired FFMA2
+          const float* xjb = XJs + s * (XJ_TILE / 4) + (q * JPT + hf8 * 8) * DPD;
+#pragma unroll
+          for (int u = 0; u < 8; u += 2) {
+            float2 acc2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int k4 = 0; k4 < DPD / 4; ++k4) {
+              const float4 a4 = reinterpret_cast<const float4*>(xjb + u * DPD)[k4];
+              const float4 b4 = reinterpret_cast<const float4*>(xjb + (u + 1) * DPD)[k4];
+              const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 df = __ffma2_rn(make_float2(av[e], bv[e]), make_float2(1.0f, 1.0f),
+                                             make_float2(-xi[4 * k4 + e], -xi[4 * k4 + e]));
+                acc2 = __ffma2_rn(df, df, acc2);
+              }
+            }
+            sv[u] = acc2.x;
+            sv[u + 1] = acc2.y;
+          }
+        } else {
         uint32_t gv[8];
         tc::tmem_ld8(tmem_base + tlane + T_GRAM + gb * BK + q * JPT + hf8 * 8, gv);
         tc::tmem_wait_ld();
@@ -343,7 +387,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (lane == 0) tc::mbar_arrive(&g_empty[gb]);
         }
         const float* nsj = Ns + s * BK + q * JPT + hf8 * 8;
-        float sv[8];
         float2 gmin = make_float2(1.0f, 1.0f);  // min over entries of s - kGuard (|x_i|^2 + |x_j|^2)
 #pragma unroll
         for (int p4 = 0; p4 < 2; ++p4) {
@@ -384,6 +427,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (sv[u] <= kGuard * (nsj[u] + ni)) sv[u] = acc;
           }
         }
+        }  // Gram mode
         uint32_t eh[4], el[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
@@ -436,13 +480,13 @@ constexpr size_t tcg_smem_bytes() {
          (2 * SG + 2 * AS + 10) * 8 + 16;
 }
 
-template <int FAM, int KS, int NC8>
+template <int FAM, int KS, int NC8, int DPD>
 cudaError_t launch_tcg_t(const float* Xh, const float* Xl, const float* Xn, const float* X32, const __half* Vhi,
                          const __half* Vlo, const double* colscale, double* out, const MvmArgs& a, dim3 grid,
                          cudaStream_t st) {
   constexpr size_t sm = tcg_smem_bytes<NC8>();
   static_assert(sm <= 232448, "tcg smem");
-  auto k = fused_kmvm_tcg_kernel<FAM, KS, NC8>;
+  auto k = fused_kmvm_tcg_kernel<FAM, KS, NC8, DPD>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
@@ -454,27 +498,47 @@ cudaError_t launch_tcg_t(const float* Xh, const float* Xl, const float* Xn, cons
 }
 
 template <int FAM>
-cudaError_t launch_tcg_fam(int ks, int nc8, const float* Xh, const float* Xl, const float* Xn, const float* X32,
-                           const __half* Vhi, const __half* Vlo, const double* colscale, double* out,
-                           const MvmArgs& a, dim3 g, cudaStream_t st) {
+cudaError_t launch_tcg_fam(int ks, int dpd, int nc8, const float* Xh, const float* Xl, const float* Xn,
+                           const float* X32, const __half* Vhi, const __half* Vlo, const double* colscale,
+                           double* out, const MvmArgs& a, dim3 g, cudaStream_t st) {
 #define GPK_TCG_ARGS Xh, Xl, Xn, X32, Vhi, Vlo, colscale, out, a, g, st
+  if (dpd > 0) {  // direct-difference mode
+#define GPK_TCG_ND(N)                                                \
+  case N:                                                            \
+    switch (dpd) {                                                   \
+      case 4: return launch_tcg_t<FAM, 0, N, 4>(GPK_TCG_ARGS);       \
+      case 8: return launch_tcg_t<FAM, 0, N, 8>(GPK_TCG_ARGS);       \
+      default: return cudaErrorInvalidValue;                         \
+    }
+    switch (nc8) {
+      GPK_TCG_ND(1) GPK_TCG_ND(2) GPK_TCG_ND(4) GPK_TCG_ND(6) GPK_TCG_ND(7) GPK_TCG_ND(8) GPK_TCG_ND(9)
+      GPK_TCG_ND(10) GPK_TCG_ND(12)
+      default: break;
+    }
+#undef GPK_TCG_ND
+    return cudaErrorInvalidValue;
+  }
+  if constexpr (FAM == kMatern12) {
+    return cudaErrorInvalidValue;  // Matern-1/2 is never evaluated from expanded distances
+  } else {
 #define GPK_TCG_NC(N)                                               \
   case N:                                                           \
     switch (ks) {                                                   \
-      case 1: return launch_tcg_t<FAM, 1, N>(GPK_TCG_ARGS);         \
-      case 2: return launch_tcg_t<FAM, 2, N>(GPK_TCG_ARGS);         \
-      case 3: return launch_tcg_t<FAM, 3, N>(GPK_TCG_ARGS);         \
-      case 4: return launch_tcg_t<FAM, 4, N>(GPK_TCG_ARGS);         \
+      case 1: return launch_tcg_t<FAM, 1, N, 0>(GPK_TCG_ARGS);      \
+      case 2: return launch_tcg_t<FAM, 2, N, 0>(GPK_TCG_ARGS);      \
+      case 3: return launch_tcg_t<FAM, 3, N, 0>(GPK_TCG_ARGS);      \
+      case 4: return launch_tcg_t<FAM, 4, N, 0>(GPK_TCG_ARGS);      \
       default: return cudaErrorInvalidValue;                        \
     }
-  switch (nc8) {
-    GPK_TCG_NC(1) GPK_TCG_NC(2) GPK_TCG_NC(4) GPK_TCG_NC(6) GPK_TCG_NC(7) GPK_TCG_NC(8) GPK_TCG_NC(9)
-    GPK_TCG_NC(10) GPK_TCG_NC(12)
-    default: break;
-  }
+    switch (nc8) {
+      GPK_TCG_NC(1) GPK_TCG_NC(2) GPK_TCG_NC(4) GPK_TCG_NC(6) GPK_TCG_NC(7) GPK_TCG_NC(8) GPK_TCG_NC(9)
+      GPK_TCG_NC(10) GPK_TCG_NC(12)
+      default: break;
+    }
 #undef GPK_TCG_NC
+    return cudaErrorInvalidValue;
+  }
 #undef GPK_TCG_ARGS
-  return cudaErrorInvalidValue;
 }
 
 }  // namespace tcg
@@ -483,7 +547,7 @@ cudaError_t launch_tcg_fam(int ks, int nc8, const float* Xh, const float* Xl, co
 #define GPK_INSTANTIATE_TCG_FAMILY(FAM)                                                                      \
   namespace gpk {                                                                                            \
   namespace tcg {                                                                                            \
-  template cudaError_t launch_tcg_fam<FAM>(int, int, const float*, const float*, const float*, const float*, \
+  template cudaError_t launch_tcg_fam<FAM>(int, int, int, const float*, const float*, const float*, const float*, \
                                            const __half*, const __half*, const double*, double*,             \
                                            const MvmArgs&, dim3, cudaStream_t);                              \
   }                                                                                                          \
