@@ -1,0 +1,90 @@
+"""One full-size mLL + gradient evaluation of a BASELINE config on one GPU (device-resident
+inputs), for the configs too large for bench.py's warm-up / e2e protocol (C4, C5).  Modules are
+loaded by a small warm-up evaluation first; the timed evaluation is bracketed by CUDA events.
+python tools/big_eval.py C5 [rank] > profiles/r1_big_c5.json"""
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2107_00243_b200 import capi, workloads  # noqa: E402
+
+wl = sys.argv[1] if len(sys.argv) > 1 else "C5"
+rank = int(sys.argv[2]) if len(sys.argv) > 2 else None
+lib = capi.lib()
+Dp = C.POINTER(C.c_double)
+dev = torch.device("cuda", 0)
+
+
+def run(w, timed):
+    x, y = workloads.generate(w)
+    n, d, l = w.n, w.d, w.probes
+    seed = int(lib.gpk_mix_seed(workloads.PROBE_SEED, 1))
+    z = np.empty((n, l), order="F")
+    t0 = time.perf_counter()
+    assert lib.gpk_make_probes(n, l, C.c_uint64(seed), z.ctypes.data_as(Dp)) == 0
+    t_probes = time.perf_counter() - t0
+    X_d = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(x).T)).to(dev)
+    y_d = torch.from_numpy(y.copy()).to(dev)
+    Z_d = torch.from_numpy(np.ascontiguousarray(z.T)).to(dev)
+    del z
+    lo, lls, ln = w.log_params
+    lls = np.ascontiguousarray(lls)
+    ctx = C.c_void_p()
+    assert lib.gpk_create(0, C.byref(ctx)) == 0
+    cfg = capi.gpk_mll_cfg(capi.gpk_cg_cfg(w.max_iters, w.rel_tol, 0, capi.GPK_PREC_TF32X3, 2), 1, 1, 0)
+    g = np.zeros(d + 2)
+    res = capi.gpk_mll_result()
+    res.gradient = g.ctypes.data_as(Dp)
+    lib.gpk_profile_enable(ctx, 1)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    e[0].record()
+    assert lib.gpk_set_data_device(ctx, C.c_void_p(X_d.data_ptr()), n, d, n) == 0
+    assert lib.gpk_set_params(ctx, w.family, 1.0, lo, lls.ctypes.data_as(Dp), ln) == 0
+    torch.cuda.synchronize()
+    e[1].record()
+    if w.rank > 0:
+        assert lib.gpk_pivoted_cholesky(ctx, w.rank, 0.0, w.noise, None, None, None) == 0, lib.gpk_last_error(ctx)
+        assert lib.gpk_precond_deriv_factors(ctx) == 0, lib.gpk_last_error(ctx)
+    else:
+        assert lib.gpk_precond_identity(ctx) == 0
+    torch.cuda.synchronize()
+    e[2].record()
+    rc = lib.gpk_evaluate_mll_device(ctx, C.c_void_p(y_d.data_ptr()), C.c_void_p(Z_d.data_ptr()), n, l,
+                                     C.c_uint64(seed), C.byref(cfg), C.byref(res))
+    assert rc == 0, lib.gpk_last_error(ctx)
+    torch.cuda.synchronize()
+    e[3].record()
+    torch.cuda.synchronize()
+    ms, cnt, fl, en = C.c_double(), C.c_longlong(), C.c_double(), C.c_double()
+    lib.gpk_profile_read(ctx, 0, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en))
+    out = None
+    if timed:
+        out = dict(workload=w.name, n=n, d=d, probes=l, precond_rank=w.rank, max_iters=w.max_iters,
+                   rel_tol=w.rel_tol, precision="tf32x3", gpus=1,
+                   s_per_eval=(e[0].elapsed_time(e[3])) / 1e3,
+                   s_setup=e[0].elapsed_time(e[1]) / 1e3, s_precond=e[1].elapsed_time(e[2]) / 1e3,
+                   s_evaluate=e[2].elapsed_time(e[3]) / 1e3, s_probe_generation_host=t_probes,
+                   value=res.value, logdet=res.logdet, gradient=list(g), solve_iterations=res.solve_iterations,
+                   total_cg_iterations=res.total_cg_iterations, refine_passes=res.refine_passes,
+                   max_true_rel_residual=res.max_true_rel_residual,
+                   mvm=dict(launches=cnt.value, avg_launch_ms=ms.value / max(cnt.value, 1),
+                            tflops_algorithmic=fl.value / ms.value * 1e3 / 1e12 if ms.value else 0.0,
+                            entries_per_s=en.value / ms.value * 1e3 if ms.value else 0.0,
+                            share_of_eval=ms.value / 1e3 / ((e[2].elapsed_time(e[3])) / 1e3)),
+                   gpu=torch.cuda.get_device_name(0))
+    lib.gpk_destroy(ctx)
+    return out
+
+
+w0 = workloads.config(wl, n=4096)  # warm-up: loads every module of the path
+w0.max_iters = 10
+run(w0, False)
+w = workloads.config(wl, rank=rank)
+print(json.dumps(run(w, True)))
