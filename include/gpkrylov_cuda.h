@@ -54,7 +54,8 @@ typedef enum { GPK_PREC_FP64 = 0, GPK_PREC_FP32 = 1, GPK_PREC_TF32X3 = 2 } gpk_p
  *   where cancellation would dominate) recomputed by direct differences;
  *   RBF / Matern-3/2 / Matern-5/2, d <= 32.
  * AUTO (default): GRAM when eligible, d >= 6 and max |x~|^2 of the centred
- *   pre-scaled coordinates <= 320, else DIRECT. */
+ *   pre-scaled coordinates <= 4096, else DIRECT (tf32x3 d <= 4: direct differences on the same
+ *   tcgen05 pipeline). */
 typedef enum { GPK_MVM_AUTO = 0, GPK_MVM_DIRECT = 1, GPK_MVM_GRAM = 2 } gpk_mvm_variant;
 
 /* krylov.hpp:15-24 CgConfig (+ GPU fields). */

@@ -21,15 +21,7 @@ struct MvmArgs {
   int row_begin;             // first output row of this rank's shard (multiple of 128)
   int row_end;               // one past the last output row; outputs are stored at row - row_begin
   int dp;                    // padded coordinate count of the packed fp32 rows (Gram guard path)
-  // stream-K work split of the tcgen05 MVM (sk_ctas > 0): CTA c owns units [c U / G, (c+1) U / G)
-  // of the U = sk_rb * (n_pad / 64) (row block, j-tile) units and writes one partial per segment
-  int sk_ctas = 0;           // G
-  int sk_rb = 0;             // row blocks of 128 rows
-  int sk_smax = 0;           // segments per CTA (partial slots)
-  double* sk_part = nullptr; // [G][sk_smax][t][128] partial outputs (already column-scaled)
 };
-// Stream-K partial reduction: out[c][row] = sum over the CTAs covering row block rb (CTA order).
-cudaError_t launch_sk_reduce(const MvmArgs& a, double* out, long long ldo, cudaStream_t st);
 
 // Packed-operand geometry for a given column count.
 struct MvmShape {

@@ -136,37 +136,6 @@ cudaError_t launch_pack_v_f16_only(const double* V, long long ldv, int t, int n,
   return cudaGetLastError();
 }
 
-// Stream-K reduction: for row block rb the CTAs c_first..c_last covering its units each left a
-// partial in slot (rb - first row block of c); summed in CTA order (deterministic, depends on n
-// and G only).
-__global__ void sk_reduce_kernel(MvmArgs a, double* __restrict__ out, long long ldo) {
-  const int rb = blockIdx.x;
-  const int col = blockIdx.y;
-  const int r = threadIdx.x;
-  const long long NT = a.n_pad / 64;
-  const long long U = static_cast<long long>(a.sk_rb) * NT, G = a.sk_ctas;
-  auto cta_of = [&](long long u) {
-    long long c = u * G / U;
-    while (c + 1 < G && (c + 1) * U / G <= u) ++c;
-    while (c > 0 && c * U / G > u) --c;
-    return c;
-  };
-  const long long c0 = cta_of(static_cast<long long>(rb) * NT), c1 = cta_of(static_cast<long long>(rb + 1) * NT - 1);
-  double acc = 0.0;
-  for (long long c = c0; c <= c1; ++c) {
-    const long long first_rb = (c * U / G) / NT;
-    const long long slot = rb - first_rb;
-    acc += a.sk_part[((c * a.sk_smax + slot) * a.t + col) * 128 + r];
-  }
-  const long long row = static_cast<long long>(rb) * 128 + r;
-  if (a.row_begin + row < a.row_end) out[col * ldo + row] = acc;
-}
-
-cudaError_t launch_sk_reduce(const MvmArgs& a, double* out, long long ldo, cudaStream_t st) {
-  sk_reduce_kernel<<<dim3(a.sk_rb, a.t), 128, 0, st>>>(a, out, ldo);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_fused_kmvm_tcg(int family, int d, int direct_dp, const float* xh, const float* xl,
                                   const float* xn, const float* x32, const void* vhi, const void* vlo,
                                   const double* colscale, double* out, const MvmArgs& a, int splits,
@@ -174,7 +143,7 @@ cudaError_t launch_fused_kmvm_tcg(int family, int d, int direct_dp, const float*
   const int npad = tcg_npad(a.t);
   if (npad < 0 || d < 1 || d > 32) return cudaErrorInvalidValue;
   const int ks = (d + 7) / 8;
-  dim3 g = a.sk_ctas > 0 ? dim3(a.sk_ctas, 1) : dim3((a.row_end - a.row_begin + tcg::BM - 1) / tcg::BM, splits);
+  dim3 g((a.row_end - a.row_begin + tcg::BM - 1) / tcg::BM, splits);
   const int nc8 = npad / 8;
   const __half* h = static_cast<const __half*>(vhi);
   const __half* l = static_cast<const __half*>(vlo);

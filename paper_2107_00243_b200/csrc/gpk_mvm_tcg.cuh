@@ -144,8 +144,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t sXJ = sN + SG * BK * 4;
   const uint32_t sXI = sXJ + SG * XJ_TILE;
   const float* XJs = reinterpret_cast<const float*>(sbase + (sXJ - base));
-  const float* XIs0 = reinterpret_cast<const float*>(sbase + (sXI - base));  // [2][BM][dp]: by segment parity
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (sXI - base) + 2 * XI_BLOCK);
+  const float* XIs = reinterpret_cast<const float*>(sbase + (sXI - base));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (sXI - base) + XI_BLOCK);
   uint64_t* xv_full = bars;
   uint64_t* xv_empty = bars + SG;
   uint64_t* a_full = bars + 2 * SG;
@@ -155,29 +155,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* acc_full = g_full + 4;
   uint64_t* acc_empty = g_full + 6;
   uint64_t* ax_ready = g_full + 8;
-  uint64_t* xi_full = g_full + 9;    // [2]
-  uint64_t* xi_empty = g_full + 11;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g_full + 13);
+  uint64_t* xi_full = g_full + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g_full + 10);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // Work: a contiguous range [u0, u1) of (row block, j-tile) units, unit u = rb * NT + jt.
-  // Legacy split-K: row block blockIdx.x, j-tiles of split blockIdx.y (one segment).  Stream-K
-  // (a.sk_ctas > 0): CTA c owns [c U / G, (c+1) U / G) of all U = RB NT units, cut into
-  // segments at row-block boundaries; each segment's rows are written as a partial that
-  // sk_reduce_kernel sums in CTA order (so every SM gets an equal share for any n).
-  const int NT = a.n_pad / BK;
-  long long u0, u1;
-  if (a.sk_ctas > 0) {
-    const long long U = static_cast<long long>(a.sk_rb) * NT;
-    u0 = static_cast<long long>(blockIdx.x) * U / a.sk_ctas;
-    u1 = static_cast<long long>(blockIdx.x + 1) * U / a.sk_ctas;
-  } else {
-    const int jt0 = blockIdx.y * a.jtiles_per_split;
-    const int jt1 = min(jt0 + a.jtiles_per_split, NT);
-    u0 = static_cast<long long>(blockIdx.x) * NT + jt0;
-    u1 = static_cast<long long>(blockIdx.x) * NT + max(jt0, jt1);
-  }
+  const int row0 = a.row_begin + blockIdx.x * BM;
+  const int jt0 = blockIdx.y * a.jtiles_per_split;
+  const int jt1 = min(jt0 + a.jtiles_per_split, a.n_pad / BK);
+  const int nt = jt1 - jt0;
   const int F = a.flush > 0 ? a.flush : 1;
   if (threadIdx.x == 0) GPK_TRACE(0, 0);
 
@@ -197,10 +183,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&acc_empty[s], NPW);
     }
     mbar_init(ax_ready, NPW);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&xi_full[b], 1);
-      mbar_init(&xi_empty[b], NPW);
-    }
+    mbar_init(xi_full, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -217,46 +200,37 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer (converged warp, elected lane) ----------------
     const uint32_t xjb = static_cast<uint32_t>(BK * a.dp * 4);
-    int gi = 0, sg = 0;
-    for (long long u = u0; u < u1; ++sg) {
-      const int rb = static_cast<int>(u / NT), ja = static_cast<int>(u % NT);
-      const int len = static_cast<int>(min(static_cast<long long>(NT - ja), u1 - u));
-      const int xb = sg & 1;
-      mbar_wait_sleep(&xi_empty[xb], ((sg >> 1) & 1) ^ 1);  // the segment two back is done with it
+    if (nt > 0 && elect_one()) {
+      mbar_arrive_expect_tx(xi_full, BM * a.dp * 4);
+      bulk_g2s(sbase + (sXI - base), X32 + static_cast<long long>(row0) * a.dp, BM * a.dp * 4, xi_full);
+    }
+    __syncwarp();
+    for (int it = 0; it < nt; ++it) {
+      const int s = it % SG;
+      mbar_wait_sleep(&xv_empty[s], ((it / SG) & 1) ^ 1);
       if (elect_one()) {
-        const int row0 = a.row_begin + rb * BM;
-        mbar_arrive_expect_tx(&xi_full[xb], BM * a.dp * 4);
-        bulk_g2s(sbase + (sXI - base) + xb * XI_BLOCK, X32 + static_cast<long long>(row0) * a.dp, BM * a.dp * 4,
-                 &xi_full[xb]);
+        const long long jt = jt0 + it;
+        if constexpr (DIRECT) {
+          mbar_arrive_expect_tx(&xv_full[s], 2 * VTILE + xjb);
+          bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
+        } else {
+          mbar_arrive_expect_tx(&xv_full[s], 2 * XG_TILE + BK * 4 + 2 * VTILE + xjb);
+          bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
+          bulk_g2s(sbase + (sBx - base) + (s * 2 + 0) * XG_TILE, Xh + jt * (BK * 32), XG_TILE, &xv_full[s]);
+          bulk_g2s(sbase + (sBx - base) + (s * 2 + 1) * XG_TILE, Xl + jt * (BK * 32), XG_TILE, &xv_full[s]);
+          bulk_g2s(sbase + (sN - base) + s * BK * 4, Xn + jt * BK, BK * 4, &xv_full[s]);
+        }
+        bulk_g2s(sbase + (sV - base) + (s * 2 + 0) * VTILE, Vhi + jt * NPAD * BK, VTILE, &xv_full[s]);
+        bulk_g2s(sbase + (sV - base) + (s * 2 + 1) * VTILE, Vlo + jt * NPAD * BK, VTILE, &xv_full[s]);
       }
       __syncwarp();
-      for (int il = 0; il < len; ++il, ++gi) {
-        const int s = gi % SG;
-        mbar_wait_sleep(&xv_empty[s], ((gi / SG) & 1) ^ 1);
-        if (elect_one()) {
-          const long long jt = ja + il;
-          if constexpr (DIRECT) {
-            mbar_arrive_expect_tx(&xv_full[s], 2 * VTILE + xjb);
-            bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
-          } else {
-            mbar_arrive_expect_tx(&xv_full[s], 2 * XG_TILE + BK * 4 + 2 * VTILE + xjb);
-            bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
-            bulk_g2s(sbase + (sBx - base) + (s * 2 + 0) * XG_TILE, Xh + jt * (BK * 32), XG_TILE, &xv_full[s]);
-            bulk_g2s(sbase + (sBx - base) + (s * 2 + 1) * XG_TILE, Xl + jt * (BK * 32), XG_TILE, &xv_full[s]);
-            bulk_g2s(sbase + (sN - base) + s * BK * 4, Xn + jt * BK, BK * 4, &xv_full[s]);
-          }
-          bulk_g2s(sbase + (sV - base) + (s * 2 + 0) * VTILE, Vhi + jt * NPAD * BK, VTILE, &xv_full[s]);
-          bulk_g2s(sbase + (sV - base) + (s * 2 + 1) * VTILE, Vlo + jt * NPAD * BK, VTILE, &xv_full[s]);
-        }
-        __syncwarp();
-      }
-      u += len;
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (converged warp, elected lane) ----------------
-    {
+    if (nt > 0) {
       constexpr uint32_t idesc_v = idesc_f16(NPAD);
       constexpr uint32_t idesc_g = tc::idesc_tf32(BK);
+      if constexpr (!DIRECT) mbar_wait_sleep(ax_ready, 0);
       auto gram = [&](int k) {
         if constexpr (DIRECT) return;
         const int s = k % SG, gb = k & 1;
@@ -280,46 +254,34 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         if (lane == 0) GPK_TRACE(7, k);
       };
-      int gi = 0, gc = 0, sg = 0;  // global tile, accumulation group, segment counters
-      for (long long u = u0; u < u1; ++sg) {
-        const int ja = static_cast<int>(u % NT);
-        const int len = static_cast<int>(min(static_cast<long long>(NT - ja), u1 - u));
-        // the segment's A_x is in TMEM (no Gram look-ahead across a segment boundary)
-        if constexpr (!DIRECT) mbar_wait_sleep(ax_ready, sg & 1);
-        gram(gi);
-        for (int il = 0; il < len; ++il) {
-          const int k = gi + il;
-          if (il + 1 < len) gram(k + 1);  // the next Gram tile overlaps this tile's kernel-shape evaluation
-          const int s = k % SG, as = k % AS;
-          const int buf = gc & 1;
-          if (il % F == 0) mbar_wait_sleep(&acc_empty[buf], ((gc >> 1) & 1) ^ 1);
-          mbar_wait_sleep(&a_full[as], (k / AS) & 1);
-          if (lane == 0) GPK_TRACE(3, k);
-          tc::tc_fence_after();
-          const uint32_t d_tmem = tmem_base + T_ACC + buf * NPAD;
-          const uint32_t tah = tmem_base + T_AT + as * 64, tal = tah + 32;
-          const uint32_t bhi = sV + (s * 2 + 0) * VTILE, blo = sV + (s * 2 + 1) * VTILE;
-          const bool close = il % F == F - 1 || il == len - 1;
-          if (elect_one()) {
+      gram(0);
+      for (int it = 0; it < nt; ++it) {
+        if (it + 1 < nt) gram(it + 1);  // the next Gram tile overlaps this tile's kernel-shape evaluation
+        const int s = it % SG, as = it % AS;
+        const int g = it / F, buf = g & 1;
+        if (it % F == 0) mbar_wait_sleep(&acc_empty[buf], ((g >> 1) & 1) ^ 1);
+        mbar_wait_sleep(&a_full[as], (it / AS) & 1);
+        if (lane == 0) GPK_TRACE(3, it);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + T_ACC + buf * NPAD;
+        const uint32_t tah = tmem_base + T_AT + as * 64, tal = tah + 32;
+        const uint32_t bhi = sV + (s * 2 + 0) * VTILE, blo = sV + (s * 2 + 1) * VTILE;
+        if (elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < BK / 16; ++ks) {
-              const uint32_t koff = ks * 32;  // 16 fp16 along K
-              const uint64_t dbh = tc::smem_desc_sw128(bhi + koff), dbl = tc::smem_desc_sw128(blo + koff);
-              const uint32_t acc = (il % F != 0 || ks > 0) ? 1u : 0u;
-              mma_ts_f16(d_tmem, tah + ks * 8, dbh, idesc_v, acc);
-              mma_ts_f16(d_tmem, tah + ks * 8, dbl, idesc_v, 1u);
-              mma_ts_f16(d_tmem, tal + ks * 8, dbh, idesc_v, 1u);
-            }
-            tc::tc_commit(&a_empty[as]);
-            tc::tc_commit(&xv_empty[s]);  // also covers the Gram MMA of this stage and the producers' norm reads
-            if (close) tc::tc_commit(&acc_full[buf]);
+          for (int ks = 0; ks < BK / 16; ++ks) {
+            const uint32_t koff = ks * 32;  // 16 fp16 along K
+            const uint64_t dbh = tc::smem_desc_sw128(bhi + koff), dbl = tc::smem_desc_sw128(blo + koff);
+            const uint32_t acc = (it % F != 0 || ks > 0) ? 1u : 0u;
+            mma_ts_f16(d_tmem, tah + ks * 8, dbh, idesc_v, acc);
+            mma_ts_f16(d_tmem, tah + ks * 8, dbl, idesc_v, 1u);
+            mma_ts_f16(d_tmem, tal + ks * 8, dbh, idesc_v, 1u);
           }
-          __syncwarp();
-          if (close) ++gc;
-          if (lane == 0) GPK_TRACE(6, k);
+          tc::tc_commit(&a_empty[as]);
+          tc::tc_commit(&xv_empty[s]);  // also covers the Gram MMA of this stage and the producers' norm reads
+          if (it % F == F - 1 || it == nt - 1) tc::tc_commit(&acc_full[buf]);
         }
-        gi += len;
-        u += len;
+        __syncwarp();
+        if (lane == 0) GPK_TRACE(6, it);
       }
     }
   } else {
@@ -328,8 +290,42 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int lg = warp & 3;   // TMEM lane group
     const int q = pw >> 2;     // 16-column slice of the j-tile, and column-chunk subset of the drain
     const int r = lg * 32 + lane;
+    const int row = row0 + r;
+    const float ni = DIRECT ? 0.0f : Xn[row];
+    const float2 ni2 = make_float2(ni, ni);
     const uint32_t tlane = static_cast<uint32_t>(lg * 32) << 16;
+    if constexpr (!DIRECT) {  // this row's centred coordinates (tf32 hi / lo, columns q*8 .. q*8+7) -> A_x in TMEM
+      const long long rb = static_cast<long long>(row >> 3) * 256 + (row & 7) * 32;
+      uint32_t h8[8], l8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = q * 8 + u;
+        const long long off = rb + ((((k >> 2) ^ (row & 7))) << 2) + (k & 3);
+        h8[u] = __float_as_uint(Xh[off]);
+        l8[u] = __float_as_uint(Xl[off]);
+      }
+      tmem_st8(tmem_base + tlane + T_AX + q * 8, h8);
+      tmem_st8(tmem_base + tlane + T_AX + 32 + q * 8, l8);
+      tmem_wait_st();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(ax_ready);
+    }
     double acc64[HC * 8];
+#pragma unroll
+    for (int e = 0; e < HC * 8; ++e) acc64[e] = 0.0;
+    if (nt > 0) mbar_wait_sleep(xi_full, 0);  // the CTA's fp32 rows (guard path / direct mode)
+    float xi[DIRECT ? DPD : 1];
+    if constexpr (DIRECT) {
+#pragma unroll
+      for (int k4 = 0; k4 < DPD / 4; ++k4) {
+        const float4 v = reinterpret_cast<const float4*>(XIs + r * DPD)[k4];
+        xi[4 * k4] = v.x;
+        xi[4 * k4 + 1] = v.y;
+        xi[4 * k4 + 2] = v.z;
+        xi[4 * k4 + 3] = v.w;
+      }
+    }
     auto drain = [&](int g) {
       const int buf = g & 1;
       mbar_wait_sleep(&acc_full[buf], (g >> 1) & 1);
@@ -349,52 +345,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&acc_empty[buf]);
     };
-    int gi = 0, gc = 0, sg = 0;  // global tile, accumulation group, segment counters
-    for (long long u = u0; u < u1; ++sg) {
-      const int rbk = static_cast<int>(u / NT), ja = static_cast<int>(u % NT);
-      const int len = static_cast<int>(min(static_cast<long long>(NT - ja), u1 - u));
-      const int row0 = a.row_begin + rbk * BM;
-      const int row = row0 + r;
-      const float ni = DIRECT ? 0.0f : Xn[row];
-      const float2 ni2 = make_float2(ni, ni);
-      // (Gram mode) the segment's A_x: every Gram MMA of the previous segment has completed --
-      // this thread consumed their g_full -- and the MMA warp waits for ax_ready
-    if constexpr (!DIRECT) {  // this row's centred coordinates (tf32 hi / lo, columns q*8 .. q*8+7) -> A_x in TMEM
-      const long long rb = static_cast<long long>(row >> 3) * 256 + (row & 7) * 32;
-      uint32_t h8[8], l8[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = q * 8 + u;
-        const long long off = rb + ((((k >> 2) ^ (row & 7))) << 2) + (k & 3);
-        h8[u] = __float_as_uint(Xh[off]);
-        l8[u] = __float_as_uint(Xl[off]);
-      }
-      tmem_st8(tmem_base + tlane + T_AX + q * 8, h8);
-      tmem_st8(tmem_base + tlane + T_AX + 32 + q * 8, l8);
-      tmem_wait_st();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(ax_ready);
-    }
-#pragma unroll
-      for (int e = 0; e < HC * 8; ++e) acc64[e] = 0.0;
-      const int xb = sg & 1;
-      mbar_wait_sleep(&xi_full[xb], (sg >> 1) & 1);  // the segment's fp32 rows (guard path / direct mode)
-      const float* XIs = XIs0 + xb * (XI_BLOCK / 4);
-      float xi[DIRECT ? DPD : 1];
-      if constexpr (DIRECT) {
-#pragma unroll
-        for (int k4 = 0; k4 < DPD / 4; ++k4) {
-          const float4 v = reinterpret_cast<const float4*>(XIs + r * DPD)[k4];
-          xi[4 * k4] = v.x;
-          xi[4 * k4 + 1] = v.y;
-          xi[4 * k4 + 2] = v.z;
-          xi[4 * k4 + 3] = v.w;
-        }
-      }
-      for (int il = 0; il < len; ++il) {
-      const int it = gi + il;  // global tile index (ring stages / phases)
+    for (int it = 0; it < nt; ++it) {
       const int s = it % SG, as = it % AS, gb = it & 1;
+      const int jb = (jt0 + it) * BK + q * JPT;  // global index of this thread's first column
       if (threadIdx.x == 64) GPK_TRACE(1, it);
       if constexpr (!DIRECT) mbar_wait_sleep(&g_full[gb], (it >> 1) & 1);
       if (threadIdx.x == 64) GPK_TRACE(2, it);
@@ -494,37 +447,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&a_full[as]);
       if (lane == 0 && it < 64) GPK_TRACE(4, it * 16 + pw);
-      if (il % F == 0 && il > 0) drain(gc + il / F - 1);
-      }
-      drain(gc + (len - 1) / F);
-      gc += (len + F - 1) / F;
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&xi_empty[xb]);  // the segment's rows are no longer read
-      if (row < a.row_end) {
-        double* o;
-        long long ld, orow;
-        if (a.sk_ctas > 0) {  // stream-K partial [cta][segment][col][BM]
-          o = a.sk_part + (static_cast<long long>(blockIdx.x) * a.sk_smax + sg) * static_cast<long long>(a.t) * BM;
-          ld = BM;
-          orow = r;
-        } else {
-          o = out + static_cast<long long>(blockIdx.y) * a.split_stride;
-          ld = a.ldo;
-          orow = row - a.row_begin;
-        }
+      if (it % F == 0 && it > 0) drain(it / F - 1);
+    }
+    if (nt > 0) drain((nt - 1) / F);
+    if (threadIdx.x == 64) GPK_TRACE(0, 2);
+    if (row < a.row_end) {
+      double* o = out + static_cast<long long>(blockIdx.y) * a.split_stride;
 #pragma unroll
-        for (int h = 0; h < HC; ++h) {
-          const int c8 = q + h * RPT;
-          if (c8 >= NC8) continue;
+      for (int h = 0; h < HC; ++h) {
+        const int c8 = q + h * RPT;
+        if (c8 >= NC8) continue;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int col = c8 * 8 + e;
-            if (col < a.t) o[static_cast<long long>(col) * ld + orow] = colscale[col] * acc64[h * 8 + e];
-          }
+        for (int e = 0; e < 8; ++e) {
+          const int col = c8 * 8 + e;
+          if (col < a.t) o[static_cast<long long>(col) * a.ldo + (row - a.row_begin)] = colscale[col] * acc64[h * 8 + e];
         }
       }
-      gi += len;
-      u += len;
     }
   }
   tc::tc_fence_before();
@@ -538,8 +476,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 template <int NC8>
 constexpr size_t tcg_smem_bytes() {
-  return 1024 + SG * 2 * XG_TILE + SG * 2 * (8 * NC8 * BK * 2) + SG * BK * 4 + SG * XJ_TILE + 2 * XI_BLOCK +
-         (2 * SG + 2 * AS + 13) * 8 + 16;
+  return 1024 + SG * 2 * XG_TILE + SG * 2 * (8 * NC8 * BK * 2) + SG * BK * 4 + SG * XJ_TILE + XI_BLOCK +
+         (2 * SG + 2 * AS + 10) * 8 + 16;
 }
 
 template <int FAM, int KS, int NC8, int DPD>
