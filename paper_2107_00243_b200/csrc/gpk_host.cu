@@ -1196,6 +1196,20 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   CK(cudaEventCreate(&e1));
   CK(cudaEventCreate(&e2));
   CK(cudaEventRecord(e0, c->st));
+  // unshared backward batch (gp_likelihood.hpp:79-84): its host mt19937_64 stream is drawn on a
+  // host thread while the device runs the forward solve
+  std::vector<double> hz_bwd;
+  std::thread bwd_draw;
+  if (cfg->with_gradient && !cfg->share_probes) {
+    hz_bwd.resize(static_cast<size_t>(n) * l);
+    bwd_draw = std::thread([&hz_bwd, n, l, seed] { make_probes_impl(n, l, mix_seed_impl(seed, 0xb2dULL), hz_bwd.data()); });
+  }
+  struct DrawJoin {
+    std::thread& t;
+    ~DrawJoin() {
+      if (t.joinable()) t.join();
+    }
+  } draw_join{bwd_draw};
 
   // ---- forward: one mBCG over [y, z_1..z_l] (pcg_solve(y) + vr_logdet's probe solves)
   const int t = 1 + l;
@@ -1305,11 +1319,10 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
     const double* Sb = S;
     long long ldsb = ldn;
     if (!cfg->share_probes) {
-      std::vector<double> hz(static_cast<size_t>(n) * l);
-      make_probes_impl(n, l, mix_seed_impl(seed, 0xb2dULL), hz.data());
+      bwd_draw.join();
       Zu.ensure(static_cast<size_t>(l) * ldn);
-      CK(cudaMemcpy2DAsync(Zu.p, ldn * sizeof(double), hz.data() + r0, n * sizeof(double), nl * sizeof(double), l,
-                           cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpy2DAsync(Zu.p, ldn * sizeof(double), hz_bwd.data() + r0, n * sizeof(double), nl * sizeof(double),
+                           l, cudaMemcpyHostToDevice, c->st));
       Zb = Zu.p;
       ldzb = ldn;
     }
