@@ -317,11 +317,24 @@ class KernelOperator : public ApplyOp {
     const Index nb = r1 - r0, n = rows(), d = x_.cols;
     const double o2 = std::pow(p_.outputscale(), 2);
     Mat out(nb, n);
+    // ORC_DIRECT_DIST=1 (sensitivity experiments only, not the reference): direct differences
+    static const bool direct = [] {
+      const char* e = std::getenv("ORC_DIRECT_DIST");
+      return e && e[0] == '1';
+    }();
     for (Index j = 0; j < n; ++j)
       for (Index i = 0; i < nb; ++i) {
-        double g = 0.0;
-        for (Index k = 0; k < d; ++k) g += sx_(r0 + i, k) * sx_(j, k);
-        double s = (-2.0 * g + sq_[static_cast<size_t>(r0 + i)]) + sq_[static_cast<size_t>(j)];
+        double g = 0.0, s;
+        if (direct) {
+          s = 0.0;
+          for (Index k = 0; k < d; ++k) {
+            const double df = sx_(r0 + i, k) - sx_(j, k);
+            s += df * df;
+          }
+        } else {
+          for (Index k = 0; k < d; ++k) g += sx_(r0 + i, k) * sx_(j, k);
+          s = (-2.0 * g + sq_[static_cast<size_t>(r0 + i)]) + sq_[static_cast<size_t>(j)];
+        }
         s = std::max(s, 0.0);
         out(i, j) = o2 * shape(fam_, alpha_, s);
       }

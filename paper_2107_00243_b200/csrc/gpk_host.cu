@@ -191,6 +191,42 @@ __global__ void to_padded_kernel(const double* __restrict__ src, long long lds, 
   const int c = static_cast<int>(idx / n_pad), i = static_cast<int>(idx % n_pad);
   dst[idx] = static_cast<T>(i < n ? src[c * lds + i] : 0.0);
 }
+__global__ void gather_slots_kernel(const gpk::SlotState* __restrict__ src, const int* __restrict__ map, int nt,
+                                    gpk::SlotState* __restrict__ dst) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nt) dst[q] = src[map[q]];
+}
+// page-locked host memory (the pipelined CG state read-back and the small uploads of the
+// compaction maps must not drain the stream)
+struct Pinned {
+  char* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    if (cudaMallocHost(reinterpret_cast<void**>(&p), bytes) != cudaSuccess) {
+      p = nullptr;
+      fail(GPK_CUDA_ERROR, "cudaMallocHost failed");
+    }
+    cap = bytes;
+  }
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+struct EventPair {
+  cudaEvent_t e[2] = {nullptr, nullptr};
+  cudaEvent_t get(int i) {
+    if (!e[i]) CK(cudaEventCreateWithFlags(&e[i], cudaEventDisableTiming));
+    return e[i];
+  }
+  ~EventPair() {
+    for (auto x : e)
+      if (x) cudaEventDestroy(x);
+  }
+};
 __global__ void add_diag_kernel(double* __restrict__ a, int k, double v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < k) a[static_cast<long long>(i) * (k + 1)] += v;
@@ -410,12 +446,45 @@ struct gpk_ctx {
     const char* e = std::getenv("GPK_FUSED_CG");
     return !(e && std::atoi(e) == 0);
   }();
-  DBuf<unsigned> w_cnt;
-  DBuf<double> w_prz, w_pzz;
+  DBuf<unsigned> w_cnt, w_cnt2;
+  DBuf<double> w_prz, w_pzz, w_grz, w_gzz;
+  bool use_wood_s = [] {  // env GPK_WOOD=0 selects the unstaged g1/g2 Woodbury kernels (A/B checks)
+    const char* e = std::getenv("GPK_WOOD");
+    return !(e && std::atoi(e) == 0);
+  }();
   bool use_persistent_pchol = [] {  // env GPK_PCHOL_STEPS=1 selects the per-step kernels (A/B checks)
     const char* e = std::getenv("GPK_PCHOL_STEPS");
     return !(e && std::atoi(e) == 1);
   }();
+  // Pipelined CG state read-back (env GPK_PIPE=0 disables): the slot states of iteration
+  // it are copied to pinned memory asynchronously and examined after iteration it + 1 has
+  // been enqueued, so the device never idles on the host round trip.  Converged columns are
+  // frozen on the device (flag), so the one-iteration-late decision changes no result.
+  bool use_pipe = [] {
+    const char* e = std::getenv("GPK_PIPE");
+    return !(e && std::atoi(e) == 0);
+  }();
+  Pinned snap_h, ring_h;
+  size_t ring_off = 0;
+  EventPair snap_ev;
+  // upload through a pinned ring (stream-ordered, no drain); wraps after a stream sync
+  void h2d_ring(void* dst, const void* src, size_t bytes) {
+    constexpr size_t cap = 1 << 20;
+    ring_h.ensure(cap);
+    const size_t b = (bytes + 255) & ~static_cast<size_t>(255);
+    if (b > cap) {
+      h2d(dst, src, bytes);
+      sync();
+      return;
+    }
+    if (ring_off + b > cap) {
+      sync();
+      ring_off = 0;
+    }
+    std::memcpy(ring_h.p + ring_off, src, bytes);
+    CK(cudaMemcpyAsync(dst, ring_h.p + ring_off, bytes, cudaMemcpyHostToDevice, st));
+    ring_off += b;
+  }
   int sync_every = [] {  // CG iterations between host round trips (env GPK_SYNC_EVERY, default 1:
     const char* e = std::getenv("GPK_SYNC_EVERY");  // measured no gain from lazier syncs at C2)
     const int v = e ? std::atoi(e) : 1;
@@ -859,7 +928,7 @@ struct gpk_ctx {
       fill_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(w_hist.p, cnt, 0.0);
       check_launch(cudaGetLastError(), 1, "fill");
     }
-    int cur = 0;
+    int cur = 0, compactions = 0;
     double *Xs = st_X[0].p, *Rs = st_R[0].p, *Ps = st_P[0].p, *Zs = st_Z.p;
     double* Rspare = st_R[1].p;  // r is double-buffered by pointer (the fused x/r update writes a new block)
     gpk::SlotState* ss = w_ss[0].p;
@@ -903,27 +972,31 @@ struct gpk_ctx {
         cols.push_back(hs[s].col);
       }
       // gather finished slots into w_kx then scatter by column
-      h2d(w_map.p, slots.data(), sizeof(int) * slots.size());
+      h2d_ring(w_map.p, slots.data(), sizeof(int) * slots.size());
       check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, nl, static_cast<int>(slots.size()), w_kx.p, ldn, st),
                    1, "gather");
-      h2d(w_map.p, cols.data(), sizeof(int) * cols.size());
+      h2d_ring(w_map.p, cols.data(), sizeof(int) * cols.size());
       check_launch(gpk::launch_scatter_cols(w_kx.p, ldn, w_map.p, nl, static_cast<int>(cols.size()), Xout, ldx, st), 1,
                    "scatter");
-      sync();
+      if (!use_pipe) sync();
     };
     auto compact = [&](const std::vector<int>& keep) {
       const int nt = static_cast<int>(keep.size());
       const int nb = cur ^ 1;
       if (nt > 0) {
-        h2d(w_map.p, keep.data(), sizeof(int) * nt);
+        h2d_ring(w_map.p, keep.data(), sizeof(int) * nt);
         check_launch(gpk::launch_gather_cols(Xs, ldn, w_map.p, 1.0, nl, nt, st_X[nb].p, ldn, st), 1, "compact");
         check_launch(gpk::launch_gather_cols(Rs, ldn, w_map.p, 1.0, nl, nt, Rspare, ldn, st), 1, "compact");
         check_launch(gpk::launch_gather_cols(Ps, ldn, w_map.p, 1.0, nl, nt, st_P[nb].p, ldn, st), 1, "compact");
+        // slot states gathered on the device: with the pipelined read-back the host copy is
+        // one iteration old, the device copy is current
+        gather_slots_kernel<<<(nt + 127) / 128, 128, 0, st>>>(ss, w_map.p, nt, w_ss[nb].p);
+        check_launch(cudaGetLastError(), 1, "compact");
         std::vector<gpk::SlotState> ns(nt);
         for (int q = 0; q < nt; ++q) ns[q] = hs[keep[q]];
-        h2d(w_ss[nb].p, ns.data(), sizeof(gpk::SlotState) * nt);
-        sync();
+        if (!use_pipe) sync();
         hs = ns;
+        ++compactions;
       } else {
         hs.clear();
       }
@@ -984,7 +1057,36 @@ struct gpk_ctx {
       w_g1.ensure(gpk::g1_workspace(nl, k, t));
       w_W.ensure(static_cast<size_t>(k) * t);
       w_vmax.ensure(t);
+      if (use_wood_s) {
+        w_g1.ensure(gpk::wood_g1_workspace(k, t));
+        w_prz.ensure(gpk::wood_g2_partials(t));
+        w_pzz.ensure(gpk::wood_g2_partials(t));
+        w_grz.ensure(gpk::wood_g2_groups(t));
+        w_gzz.ensure(gpk::wood_g2_groups(t));
+        w_cnt2.ensure(gpk::wood_g2_counters(t));
+        CK(cudaMemsetAsync(w_cnt2.p, 0, sizeof(unsigned) * gpk::wood_g2_counters(t), st));
+      }
     }
+    // pipelined read-back: snapshot of iteration it (async), then the decision on the
+    // snapshot of iteration it - 1 (already complete while iteration it runs).  A snapshot
+    // taken before a compaction has the old slot layout and is skipped.
+    int pend_buf = -1;
+    snap_h.ensure(sizeof(gpk::SlotState) * 2 * static_cast<size_t>(t));
+    auto* snaps = reinterpret_cast<gpk::SlotState*>(snap_h.p);
+    auto readback = [&](int it) {
+      const int bcur = it & 1;
+      CK(cudaMemcpyAsync(snaps + static_cast<size_t>(bcur) * t, ss, sizeof(gpk::SlotState) * ta,
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(snap_ev.get(bcur), st));
+      const int take = it == max_iters ? bcur : pend_buf;  // the last iteration drains
+      pend_buf = bcur;
+      if (take < 0) return;
+      CK(cudaEventSynchronize(snap_ev.get(take)));
+      std::memcpy(hs.data(), snaps + static_cast<size_t>(take) * t, sizeof(gpk::SlotState) * ta);
+      const int c0 = compactions;
+      handle_flags();
+      if (compactions != c0) pend_buf = -1;  // the in-flight snapshot has the old layout
+    };
     vmax_ready = false;
     for (int it = 1; it <= max_iters && ta > 0; ++it) {
       w_kx.ensure(static_cast<size_t>(ta) * ldn);
@@ -993,14 +1095,27 @@ struct gpk_ctx {
         check_launch(gpk::launch_cg_pap_alpha(Ps, w_kx.p, noise, nl, ldn, ta, ppap, w_cnt.p, it, ss, dh_a, max_iters,
                                               st),
                      1, "cg_pap_alpha");
-        check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, nl, ldn, ta, ss, st), 1, "cg_xr");
-        check_launch(gpk::launch_g1(L.p, n, k, Rs, ldn, ta, nl, w_g1.p, w_W.p, k, st), 2, "g1");
         unsigned long long* vm = (!fp64 && use_tc && (gram_ok || tcg_direct) && ta <= 96) ? w_vmax.p : nullptr;
-        check_launch(gpk::launch_g2_dots_beta(C.p, n, k, w_W.p, k, ta, nl, Zs, Rs, ldn, pnoise, w_prz.p, w_pzz.p,
-                                              w_cnt.p + t, it, rel_tol, ss, dh_b, dh_r, max_iters, vm, st),
-                     1, "g2_dots_beta");
+        if (use_wood_s) {  // gpk_wood.cu: x/r update fused into the staged G1, staged G2 + dots + beta
+          check_launch(gpk::launch_g1s(L.p, n, k, Rs, ldn, ta, nl, w_g1.p, w_W.p, k, Xs, Ps, w_kx.p, noise, ss, st),
+                       2, "g1s");
+          check_launch(gpk::launch_g2s_dots_beta(C.p, n, k, w_W.p, k, ta, nl, Zs, Rs, ldn, pnoise, w_prz.p, w_pzz.p,
+                                                 w_grz.p, w_gzz.p, w_cnt2.p, it, rel_tol, ss, dh_b, dh_r, max_iters,
+                                                 vm, st),
+                       1, "g2s_dots_beta");
+        } else {
+          check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, nl, ldn, ta, ss, st), 1, "cg_xr");
+          check_launch(gpk::launch_g1(L.p, n, k, Rs, ldn, ta, nl, w_g1.p, w_W.p, k, st), 2, "g1");
+          check_launch(gpk::launch_g2_dots_beta(C.p, n, k, w_W.p, k, ta, nl, Zs, Rs, ldn, pnoise, w_prz.p, w_pzz.p,
+                                                w_cnt.p + t, it, rel_tol, ss, dh_b, dh_r, max_iters, vm, st),
+                       1, "g2_dots_beta");
+        }
         check_launch(gpk::launch_cg_p_vmax(Ps, Zs, nl, ldn, ta, ss, vm, st), 1, "cg_p");
         vmax_ready = vm != nullptr;
+        if (use_pipe) {
+          readback(it);
+          continue;
+        }
         if (it % sync_every == 0 || it == max_iters) {
           d2h(hs.data(), ss, sizeof(gpk::SlotState) * ta);
           handle_flags();
@@ -1018,6 +1133,10 @@ struct gpk_ctx {
       const double* gzz2 = global_partials(pzz, nrb, ta, tot + t, &nrg);
       check_launch(gpk::launch_cg_beta(grz2, gzz2, nrg, ta, it, rel_tol, ss, dh_b, dh_r, max_iters, st), 1, "cg_beta");
       check_launch(gpk::launch_cg_update_p(Ps, Zs, nl, ldn, ta, ss, st), 1, "cg_p");
+      if (use_pipe) {
+        readback(it);
+        continue;
+      }
       // Host round trip only every sync_every iterations: converged / failed columns freeze
       // on the device (their flag) and are compacted out at the next sync.
       if (it % sync_every == 0 || it == max_iters) {

@@ -64,6 +64,23 @@ cudaError_t launch_g2_dots_beta(const double* C, long long ldc, int ka, const do
 cudaError_t launch_cg_p_vmax(double* P, const double* Z, int n, long long ldn, int t, const SlotState* ss,
                              unsigned long long* vmax, cudaStream_t st);
 
+// gpk_wood.cu: shared-memory-staged Woodbury GEMMs of the fused iteration (grid = 2 x SMs)
+int wood_grid();
+size_t wood_g1_workspace(int ka, int tb);
+size_t wood_g2_partials(int tb);
+size_t wood_g2_groups(int tb);
+int wood_g2_counters(int tb);
+// W = A^T R_new (A: ka columns, ld lda); with X != null, R_new = R - alpha (Y + s2 P) for live
+// slots is written back to R and X += alpha P (krylov.hpp:94-95)
+cudaError_t launch_g1s(const double* A, long long lda, int ka, double* R, long long ldr, int tb, int n,
+                       double* part, double* W, long long ldw, double* X, const double* P, const double* Y,
+                       double sig2, const SlotState* ss, cudaStream_t st);
+cudaError_t launch_g2s_dots_beta(const double* C, long long ldc, int ka, const double* W, long long ldw, int tb,
+                                 int n, double* Z, const double* R, long long ldn, double sig2, double* prz,
+                                 double* pzz, double* grz, double* gzz, unsigned* cnt, int k, double rel_tol,
+                                 SlotState* ss, double* beta_hist, double* resid_hist, int max_iters,
+                                 unsigned long long* vmax, cudaStream_t st);
+
 int pchol_blocks(int n);
 struct PivotState {
   double dp;        // remaining diagonal at the current pivot
