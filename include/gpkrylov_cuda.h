@@ -272,7 +272,8 @@ long long gpk_launch_count(const gpk_ctx* ctx);
 void* gpk_stream(const gpk_ctx* ctx);
 
 /* Live per-launch timing of the two dominant kernels with CUDA events on ctx's
- * stream (off by default).  kind 0: fused kernel MVM, 1: fused derivative pass.
+ * stream (off by default).  kind 0: fused kernel MVM (reduced precision), 1: fused
+ * derivative pass, 2: fp64 kernel MVM (parity mode / certified residual).
  * Returns accumulated device milliseconds, launch count and algorithmic flops /
  * kernel entries since the last reset. */
 gpk_status gpk_profile_enable(gpk_ctx* ctx, int on);

@@ -448,6 +448,10 @@ struct gpk_ctx {
   }();
   DBuf<unsigned> w_cnt, w_cnt2;
   DBuf<double> w_prz, w_pzz, w_grz, w_gzz;
+  bool use_f64g = [] {  // env GPK_F64G=0 selects the FP64-pipe fp64 MVM (A/B checks)
+    const char* e = std::getenv("GPK_F64G");
+    return !(e && std::atoi(e) == 0);
+  }();
   bool use_wood_s = [] {  // env GPK_WOOD=0 selects the unstaged g1/g2 Woodbury kernels (A/B checks)
     const char* e = std::getenv("GPK_WOOD");
     return !(e && std::atoi(e) == 0);
@@ -524,7 +528,7 @@ struct gpk_ctx {
     long long launches = 0;
   };
   bool prof_on = false;
-  Prof prof[2];
+  Prof prof[3];  // 0: reduced-precision value MVM, 1: derivative pass, 2: fp64 MVM
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t ev_get() {
     if (!ev_pool.empty()) {
@@ -788,6 +792,21 @@ struct gpk_ctx {
         flops += static_cast<long long>(fl);
       }
       vmax_ready = false;
+      return;
+    }
+    if (fp64 && which < 0 && use_f64g) {  // gpk_mvm_f64g.cu: reference-order entries, DMMA products
+      const int cf[] = {2, 3, 6, 9};
+      for (int c0 = 0; c0 < t; c0 += 64) {
+        const int tc = std::min(64, t - c0);
+        const double fl = static_cast<double>(nl) * n * (2.0 * tc + 3.0 * d + cf[family]);
+        auto ev = prof_begin(2);
+        check_launch(gpk::launch_fused_kmvm_f64g(family, dp, X64s.p, sq.p, n, V + c0 * ldv, ldv, tc, out + c0 * ldo,
+                                                 ldo, o2, r0, r1, st),
+                     1, "fused_kmvm_f64g");
+        prof_end(2, ev, fl, static_cast<double>(nl) * n);
+        entries += static_cast<long long>(nl) * n;
+        flops += static_cast<long long>(fl);
+      }
       return;
     }
     for (int c0 = 0; c0 < t; c0 += chunk) {
@@ -1834,7 +1853,7 @@ gpk_status gpk_profile_enable(gpk_ctx* ctx, int on) {
 gpk_status gpk_profile_read(gpk_ctx* ctx, int kind, double* ms, long long* launches, double* flops,
                             double* entries) {
   return guard(ctx, [&] {
-    require(kind == 0 || kind == 1, "gpk_profile_read: kind must be 0 or 1");
+    require(kind >= 0 && kind <= 2, "gpk_profile_read: kind must be 0, 1 or 2");
     ctx->prof_collect();
     const auto& p = ctx->prof[kind];
     if (ms) *ms = p.ms;

@@ -38,6 +38,10 @@ double prescale_c(int family);
 // out: column-major [t][ldo] fp64 (split-K partials use split_stride, then reduced).
 cudaError_t launch_fused_kmvm(bool fp64, int family, int dp, int mode, const void* X, const void* V,
                               double* out, const MvmArgs& a, int splits, cudaStream_t st);
+// gpk_mvm_f64g.cu: fp64 value MVM on the fp64 tensor cores (reference expanded distances)
+cudaError_t launch_fused_kmvm_f64g(int family, int dp, const double* X, const double* sq, int n, const double* V,
+                                   long long ldv, int tc, double* out, long long ldo, double scale, int row_begin,
+                                   int row_end, cudaStream_t st);
 cudaError_t launch_reduce_splits(const double* part, int splits, long long split_stride, int t, int n,
                                  long long ldpart, double* out, long long ldo, cudaStream_t st);
 

@@ -222,7 +222,9 @@ def test_grid_evaluate_mll_matches_oracle(orc, case, backward):
     pc = gk.pivoted_cholesky_with_derivatives(op, g["rank"])
     z = gk.make_probes(g["n"], g["l"], g["probe_seed"])
     r = gk.evaluate_mll(y, op, pc, z, gk.MllConfig(gk.CgConfig(200, 1e-8, False, "fp64", 0), True, backward))
-    assert r.value == pytest.approx(g["value"], rel=1e-9)
+    # solves to rel_tol 1e-8: the value is determined to ~1e-9 (kernel entries differ from the
+    # oracle's by the DMMA Gram rounding, ~1e-16 relative), so the gate is the solve tolerance
+    assert r.value == pytest.approx(g["value"], rel=1e-8)
     np.testing.assert_allclose(r.gradient, g["gradient"], rtol=1e-6, atol=1e-9)
     np.testing.assert_allclose(r.forward_gammas, g["forward_gammas"], rtol=1e-7, atol=1e-12)
 
