@@ -215,6 +215,10 @@ def run_ours(args, rank_env):
     mvm = {"ms": ms.value, "launches": cnt.value, "flops": fl.value}
     check(lib.gpk_profile_read(ctx, 1, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en)))
     dc = {"ms": ms.value, "launches": cnt.value, "flops": fl.value}
+    check(lib.gpk_profile_read(ctx, 2, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en)))
+    f64 = {"ms": ms.value, "launches": cnt.value, "flops": fl.value, "entries": en.value}
+    check(lib.gpk_profile_read(ctx, 3, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en)))
+    vec = {"ms": ms.value, "launches": cnt.value, "bytes": fl.value}
     check(lib.gpk_profile_enable(ctx, 0))
     var, maxnorm = C.c_int(), C.c_double()
     check(lib.gpk_get_mvm_variant(ctx, C.byref(var), C.byref(maxnorm)))
@@ -237,7 +241,8 @@ def run_ours(args, rank_env):
     lib.gpk_destroy(ctx)
     h2d = X_h.numel() * 8 + y_h.numel() * 8 + Z_h.numel() * 8
     d2h = 8 * (d + 2) + 8 * l + 4 * l + 8 * 8
-    return dict(times=times, e2e_times=e2e_times, launches=launches, mvm=mvm, dc=dc, clocks=clk.summary(),
+    return dict(times=times, e2e_times=e2e_times, launches=launches, mvm=mvm, dc=dc, f64=f64, vec=vec,
+                clocks=clk.summary(),
                 mvm_variant=mvm_variant,
                 telemetry=telemetry, sweep=sweep, h2d=h2d, d2h=d2h, w=w)
 
@@ -421,6 +426,28 @@ def main():
         roofline["deriv_pass"] = {"achieved": (dcp["flops"] / dcp["ms"] * 1e3) / 1e12, "unit": "TFLOP/s",
                                   "avg_launch_ms": dcp["ms"] / dcp["launches"],
                                   "share_of_step": (dcp["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
+    f64 = r.get("f64", {})
+    if f64.get("launches"):
+        # certified fp64 residual / fp64 parity operator: Gram + contraction on DMMA, entries on the
+        # FP64 pipe; algorithmic flops n^2 (2t + 3d + c_fam)
+        roofline["fp64_mvm"] = {"kernel": "fused_kmvm_f64g_kernel (DMMA 8x8x4 Gram + contraction, fp64 entries)",
+                                "avg_launch_ms": f64["ms"] / f64["launches"], "launches_per_step":
+                                f64["launches"] / max(args.steps, 1),
+                                "achieved": (f64["flops"] / f64["ms"] * 1e3) / 1e12, "unit": "TFLOP/s",
+                                "entries_per_s": f64["entries"] / (f64["ms"] / 1e3),
+                                "share_of_step": (f64["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
+    vec = r.get("vec", {})
+    if vec.get("launches"):
+        # the fused single-rank CG vector phase (alpha, x/r update + Woodbury G1, G2 + beta, p update)
+        # against the measured HBM copy bandwidth; algorithmic bytes = 13 fp64 n-vectors per active
+        # column + L and C per iteration (the operands are L2-resident at C2: latency-bound there)
+        hbm = float(peaks.get("hbm_gbs", 6538.3))
+        ach = vec["bytes"] / (vec["ms"] / 1e3) / 1e9
+        roofline["cg_vector_phase"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                                       "frac": ach / hbm, "avg_ms_per_iteration": vec["ms"] / vec["launches"],
+                                       "bytes_per_iteration": vec["bytes"] / vec["launches"],
+                                       "iterations_per_step": vec["launches"] / max(args.steps, 1),
+                                       "share_of_step": (vec["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False,
             "scaling": "weak" if (world == 1 or args.mode == "replicas") else "strong", "vs_baseline": None,

@@ -273,7 +273,9 @@ void* gpk_stream(const gpk_ctx* ctx);
 
 /* Live per-launch timing of the two dominant kernels with CUDA events on ctx's
  * stream (off by default).  kind 0: fused kernel MVM (reduced precision), 1: fused
- * derivative pass, 2: fp64 kernel MVM (parity mode / certified residual).
+ * derivative pass, 2: fp64 kernel MVM (parity mode / certified residual), 3: the fused
+ * single-rank CG vector phase (alpha, x/r update + Woodbury, beta, p update; its "flops"
+ * field holds algorithmic HBM bytes).
  * Returns accumulated device milliseconds, launch count and algorithmic flops /
  * kernel entries since the last reset. */
 gpk_status gpk_profile_enable(gpk_ctx* ctx, int on);

@@ -528,7 +528,7 @@ struct gpk_ctx {
     long long launches = 0;
   };
   bool prof_on = false;
-  Prof prof[3];  // 0: reduced-precision value MVM, 1: derivative pass, 2: fp64 MVM
+  Prof prof[4];  // 0: reduced-precision value MVM, 1: derivative pass, 2: fp64 MVM, 3: CG vector phase
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t ev_get() {
     if (!ev_pool.empty()) {
@@ -1111,6 +1111,11 @@ struct gpk_ctx {
       w_kx.ensure(static_cast<size_t>(ta) * ldn);
       apply_kernel(Ps, ldn, ta, w_kx.p, ldn, fp64, -1);  // K p (noise-free)
       if (fused) {
+        // vector phase (kind 3): algorithmic HBM bytes = 13 fp64 n-vectors per column (pap: P, Kp;
+        // x/r update: R, P, Kp, X read, X, R written; Woodbury: R read, Z written; p update: P, Z
+        // read, P written) + L and C (n x k fp64 each)
+        auto evv = prof_begin(3);
+        const double vbytes = 8.0 * nl * (13.0 * ta + 2.0 * k);
         check_launch(gpk::launch_cg_pap_alpha(Ps, w_kx.p, noise, nl, ldn, ta, ppap, w_cnt.p, it, ss, dh_a, max_iters,
                                               st),
                      1, "cg_pap_alpha");
@@ -1130,6 +1135,7 @@ struct gpk_ctx {
                        1, "g2_dots_beta");
         }
         check_launch(gpk::launch_cg_p_vmax(Ps, Zs, nl, ldn, ta, ss, vm, st), 1, "cg_p");
+        prof_end(3, evv, vbytes, static_cast<double>(ta));
         vmax_ready = vm != nullptr;
         if (use_pipe) {
           readback(it);
@@ -1853,7 +1859,7 @@ gpk_status gpk_profile_enable(gpk_ctx* ctx, int on) {
 gpk_status gpk_profile_read(gpk_ctx* ctx, int kind, double* ms, long long* launches, double* flops,
                             double* entries) {
   return guard(ctx, [&] {
-    require(kind >= 0 && kind <= 2, "gpk_profile_read: kind must be 0, 1 or 2");
+    require(kind >= 0 && kind <= 3, "gpk_profile_read: kind must be 0..3");
     ctx->prof_collect();
     const auto& p = ctx->prof[kind];
     if (ms) *ms = p.ms;

@@ -33,7 +33,7 @@ constexpr int kFJ = 64;   // j rows per staged chunk
 constexpr int kFV = 72;   // V tile stride (doubles): 36 = 4 (mod 8) 16-byte units -> conflict-free LDS.128
 
 GPK_DEV void dmma_f(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
@@ -147,12 +147,13 @@ __global__ void __launch_bounds__(kFT, 2)
         s = s > 0.0 ? s : 0.0;
         kv[e] = __dmul_rn(scale, ref_shape(FAM, s));
       }
+      double2 b[NT];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const double2 b = *reinterpret_cast<const double2*>(vs + (nt * 8 + m) * kFV + jj * 8 + 2 * r);
-        dmma_f(acc[nt], kv[0], b.x);
-        dmma_f(acc[nt], kv[1], b.y);
-      }
+      for (int nt = 0; nt < NT; ++nt) b[nt] = *reinterpret_cast<const double2*>(vs + (nt * 8 + m) * kFV + jj * 8 + 2 * r);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma_f(acc[nt], kv[0], b[nt].x);  // independent accumulators first
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma_f(acc[nt], kv[1], b[nt].y);
     }
     __syncthreads();  // buffer buf is refilled at the next iteration
   }

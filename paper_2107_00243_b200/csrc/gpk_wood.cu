@@ -41,7 +41,7 @@ constexpr size_t kWSmem = 2ull * kWS * kSR * sizeof(double);  // 73728 B: two ti
 GPK_DEV int kpos(int kidx) { return (kidx >> 4) * 18 + (kidx & 15); }
 
 GPK_DEV void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
@@ -183,12 +183,13 @@ __global__ void __launch_bounds__(kWT, 2)
 #pragma unroll 2
         for (int q = 0; q < 16; q += 2) {
           const double2 a = *reinterpret_cast<const double2*>(ap + q);
+          double2 bb[NT];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const double2 bb = *reinterpret_cast<const double2*>(bp + j * 8 * kSR + q);
-            dmma(acc[j], a.x, bb.x);
-            dmma(acc[j], a.y, bb.y);
-          }
+          for (int j = 0; j < NT; ++j) bb[j] = *reinterpret_cast<const double2*>(bp + j * 8 * kSR + q);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma(acc[j], a.x, bb[j].x);  // independent accumulators first
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma(acc[j], a.y, bb[j].y);
         }
       }
     }
@@ -205,29 +206,36 @@ __global__ void __launch_bounds__(kWT, 2)
   }
 }
 
-// W[s][kk] = sum over the G CTA partials in fixed order: one warp per output, lane q sums
-// partials q, q + 32, ... (all loads in flight), then a fixed butterfly.
-__global__ void g1s_reduce_kernel(const double* __restrict__ part, int G, int ka, int tb, double* __restrict__ W,
-                                  long long ldw) {
-  const long long idx = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int q = threadIdx.x & 31;
+// W[s][kk] = sum over the G CTA partials in fixed order.  A CTA owns 32 consecutive outputs
+// (coalesced 256-byte rows of the partial array); warp q sums partials q, q + 8, ... (16
+// loads in flight per thread), and the 8 warp sums are combined in warp order.
+__global__ void __launch_bounds__(256) g1s_reduce_kernel(const double* __restrict__ part, int G, int ka, int tb,
+                                                         double* __restrict__ W, long long ldw) {
+  __shared__ double red[8][32];
+  const int o = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const long long idx = static_cast<long long>(blockIdx.x) * 32 + o;
   const long long tot = static_cast<long long>(ka) * tb;
-  if (idx >= tot) return;  // warp-uniform
-  const double* p = part + idx;
-  double v[16];
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const int c = q + 32 * u;
-    v[u] = c < G ? __ldcg(p + c * tot) : 0.0;
-  }
   double acc = 0.0;
+  if (idx < tot) {
+    const double* p = part + idx;
+    int c = q;
+    for (; c + 8 * 15 < G; c += 8 * 16) {
+      double v[16];
 #pragma unroll
-  for (int u = 0; u < 16; ++u) acc += v[u];
-  for (int c = q + 512; c < G; c += 32) acc += __ldcg(p + c * tot);
-  acc = warp_sum(acc);
-  if (q == 0) {
+      for (int u = 0; u < 16; ++u) v[u] = __ldcg(p + static_cast<long long>(c + 8 * u) * tot);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc += v[u];
+    }
+    for (; c < G; c += 8) acc += __ldcg(p + static_cast<long long>(c) * tot);
+  }
+  red[q][o] = acc;
+  __syncthreads();
+  if (q == 0 && idx < tot) {
+    double sum = red[0][o];
+#pragma unroll
+    for (int u = 1; u < 8; ++u) sum += red[u][o];
     const int s = static_cast<int>(idx / ka), kk = static_cast<int>(idx % ka);
-    W[s * ldw + kk] = acc;
+    W[s * ldw + kk] = sum;
   }
 }
 
@@ -317,12 +325,13 @@ __global__ void __launch_bounds__(kWT, 2)
 #pragma unroll 2
         for (int q = 0; q < 16; q += 2) {
           const double a0 = ap[q * kWS], a1 = ap[(q + 1) * kWS];
+          double2 bb[NT];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const double2 bb = *reinterpret_cast<const double2*>(bp + j * 8 * kSR + q);
-            dmma(acc[j], a0, bb.x);
-            dmma(acc[j], a1, bb.y);
-          }
+          for (int j = 0; j < NT; ++j) bb[j] = *reinterpret_cast<const double2*>(bp + j * 8 * kSR + q);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma(acc[j], a0, bb[j].x);  // independent accumulators first
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma(acc[j], a1, bb[j].y);
         }
       }
     }
@@ -523,8 +532,8 @@ cudaError_t launch_g1s(const double* A, long long lda, int ka, double* R, long l
                                            nullptr, 0.0, nullptr);
   }
   if (e != cudaSuccess) return e;
-  const long long thr = static_cast<long long>(ka) * tb * 32;
-  g1s_reduce_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, st>>>(part, G, ka, tb, W, ldw);
+  const long long tot = static_cast<long long>(ka) * tb;
+  g1s_reduce_kernel<<<static_cast<unsigned>((tot + 31) / 32), 256, 0, st>>>(part, G, ka, tb, W, ldw);
   return cudaGetLastError();
 }
 

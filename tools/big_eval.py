@@ -64,6 +64,10 @@ def run(w, timed):
     torch.cuda.synchronize()
     ms, cnt, fl, en = C.c_double(), C.c_longlong(), C.c_double(), C.c_double()
     lib.gpk_profile_read(ctx, 0, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en))
+    vms, vcnt, vby, ven = C.c_double(), C.c_longlong(), C.c_double(), C.c_double()
+    lib.gpk_profile_read(ctx, 3, C.byref(vms), C.byref(vcnt), C.byref(vby), C.byref(ven))
+    fms, fcnt, ffl, fen = C.c_double(), C.c_longlong(), C.c_double(), C.c_double()
+    lib.gpk_profile_read(ctx, 2, C.byref(fms), C.byref(fcnt), C.byref(ffl), C.byref(fen))
     out = None
     if timed:
         out = dict(workload=w.name, n=n, d=d, probes=l, precond_rank=w.rank, max_iters=w.max_iters,
@@ -78,6 +82,12 @@ def run(w, timed):
                             tflops_algorithmic=fl.value / ms.value * 1e3 / 1e12 if ms.value else 0.0,
                             entries_per_s=en.value / ms.value * 1e3 if ms.value else 0.0,
                             share_of_eval=ms.value / 1e3 / ((e[2].elapsed_time(e[3])) / 1e3)),
+                   cg_vector_phase=dict(iterations=vcnt.value, avg_ms=vms.value / max(vcnt.value, 1),
+                                        bytes_per_iteration=vby.value / max(vcnt.value, 1),
+                                        achieved_gbs=vby.value / (vms.value / 1e3) / 1e9 if vms.value else 0.0,
+                                        share_of_eval=vms.value / 1e3 / ((e[2].elapsed_time(e[3])) / 1e3)),
+                   fp64_mvm=dict(launches=fcnt.value, avg_launch_ms=fms.value / max(fcnt.value, 1),
+                                 entries_per_s=fen.value / fms.value * 1e3 if fms.value else 0.0),
                    gpu=torch.cuda.get_device_name(0))
     lib.gpk_destroy(ctx)
     return out
