@@ -10,7 +10,9 @@
 // n^2 kernel entries:
 //     quad[w]  = sum_ab dK_w[a,b] u_a u_b
 //     gamma[w] = sum_ab dK_w[a,b] W_ab,   W_ab = sum_i S[a,i] Z[b,i]
-// with dK_0 = 2 o shape(s) and dK_{l_j} = (-2 o^2 / l_j) shape_ds(s) ds_j^2.
+// with dK_0 = 2 o shape(s) and dK_{l_j} = (-2 o^2 / l_j) shape_ds(s) ds_j^2.  The gradient
+// (gp_likelihood.hpp:97-100) needs them only as quad[w] - (n/l) gamma[w], so every pair
+// contributes the single weight u_a u_b - (n/l) W_ab: one accumulator per hyperparameter.
 //
 // CTA = 256 threads = 16 x 16 threads, each owning a 4 x 4 tile of (a, b)
 // pairs of a 64 x 64 block tile; W tiles come from register-blocked outer
@@ -71,12 +73,13 @@ GPK_DEV void shape_pair(T s, T& e, T& ds) {
 
 // X: [n_pad][DP] packed scaled coordinates (fp32 pre-scaled / fp64 plain);
 // U: [n_pad]; S, Z: column-major [l][n_pad] (zero in padded rows).
-// partials: per CTA, 2*(DP+1) doubles = {Q0, Q_1..Q_DP, G0, G_1..G_DP}.
+// partials: per CTA, DP+1 doubles = {M0, M_1..M_DP}, M = Q - cmix G.
 template <typename T, int FAM, int DP>
 __global__ void __launch_bounds__(kDThreads, 1)
     deriv_contract_kernel(const T* __restrict__ X, const T* __restrict__ U, const T* __restrict__ S,
-                          const T* __restrict__ Z, int n_pad, int l, int a_begin, double* __restrict__ partials) {
-  constexpr int NA = 2 * (DP + 1);
+                          const T* __restrict__ Z, int n_pad, int l, int a_begin, T cmix,
+                          double* __restrict__ partials) {
+  constexpr int NA = DP + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Ss = reinterpret_cast<T*>(smem_raw);  // [l][kDA]
   T* Zs = Ss + l * kDA;                    // [l][kDB]
@@ -125,10 +128,17 @@ __global__ void __launch_bounds__(kDThreads, 1)
       for (int c = 0; c < 4; ++c) w[r][c] = T(0);
     for (int i = 0; i < l; ++i) {
       T sa[4], zb[4];
+      if constexpr (sizeof(T) == 4) {  // one 128-bit shared load per operand quad
+        const float4 va = *reinterpret_cast<const float4*>(Ss + i * kDA + ta * 4);
+        const float4 vb = *reinterpret_cast<const float4*>(Zs + i * kDB + tb * 4);
+        sa[0] = va.x, sa[1] = va.y, sa[2] = va.z, sa[3] = va.w;
+        zb[0] = vb.x, zb[1] = vb.y, zb[2] = vb.z, zb[3] = vb.w;
+      } else {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) sa[r] = Ss[i * kDA + ta * 4 + r];
+        for (int r = 0; r < 4; ++r) sa[r] = Ss[i * kDA + ta * 4 + r];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) zb[c] = Zs[i * kDB + tb * 4 + c];
+        for (int c = 0; c < 4; ++c) zb[c] = Zs[i * kDB + tb * 4 + c];
+      }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -158,16 +168,11 @@ __global__ void __launch_bounds__(kDThreads, 1)
         }
         T e, ds;
         shape_pair<T, FAM>(s, e, ds);
-        const T q = Ua[al] * ub;
-        const T wv = w[r][c];
+        const T q = fma(-cmix, w[r][c], Ua[al] * ub);  // u_a u_b - (n/l) W_ab
         acc[0] = fma(e, q, acc[0]);
-        acc[DP + 1] = fma(e, wv, acc[DP + 1]);
-        const T g = ds * q, h = ds * wv;
+        const T g = ds * q;
 #pragma unroll
-        for (int k = 0; k < DP; ++k) {
-          acc[1 + k] = fma(g, dd[k], acc[1 + k]);
-          acc[DP + 2 + k] = fma(h, dd[k], acc[DP + 2 + k]);
-        }
+        for (int k = 0; k < DP; ++k) acc[1 + k] = fma(g, dd[k], acc[1 + k]);
       }
     }
 #pragma unroll
@@ -184,7 +189,8 @@ __global__ void __launch_bounds__(kDThreads, 1)
 
 template <typename T, int FAM, int DP>
 static cudaError_t launch_dc_t(const void* X, const void* U, const void* S, const void* Z, int n_pad, int l,
-                               int a_begin, int a_rows, double* partials, int* nblocks, cudaStream_t st) {
+                               int a_begin, int a_rows, double cmix, double* partials, int* nblocks,
+                               cudaStream_t st) {
   const size_t sm = sizeof(T) * (static_cast<size_t>(l) * (kDA + kDB) + (kDA + kDB) * DP + kDA + kDB);
   auto k = deriv_contract_kernel<T, FAM, DP>;
   if (sm > 48 * 1024) {
@@ -197,44 +203,45 @@ static cudaError_t launch_dc_t(const void* X, const void* U, const void* S, cons
   *nblocks = static_cast<int>(g.x * g.y);
   if (partials == nullptr) return cudaSuccess;  // size query
   k<<<g, kDThreads, sm, st>>>(static_cast<const T*>(X), static_cast<const T*>(U), static_cast<const T*>(S),
-                              static_cast<const T*>(Z), n_pad, l, a_begin, partials);
+                              static_cast<const T*>(Z), n_pad, l, a_begin, static_cast<T>(cmix), partials);
   return cudaGetLastError();
 }
 
 template <typename T, int FAM>
 static cudaError_t launch_dc_dp(int dp, const void* X, const void* U, const void* S, const void* Z, int n_pad, int l,
-                                int a_begin, int a_rows, double* partials, int* nblocks, cudaStream_t st) {
+                                int a_begin, int a_rows, double cmix, double* partials, int* nblocks,
+                                cudaStream_t st) {
   switch (dp) {
-    case 4: return launch_dc_t<T, FAM, 4>(X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
-    case 12: return launch_dc_t<T, FAM, 12>(X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
-    case 20: return launch_dc_t<T, FAM, 20>(X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
-    case 32: return launch_dc_t<T, FAM, 32>(X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+    case 4: return launch_dc_t<T, FAM, 4>(X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
+    case 12: return launch_dc_t<T, FAM, 12>(X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
+    case 20: return launch_dc_t<T, FAM, 20>(X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
+    case 32: return launch_dc_t<T, FAM, 32>(X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
   }
   return cudaErrorInvalidValue;
 }
 
 template <typename T>
 static cudaError_t launch_dc_fam(int fam, int dp, const void* X, const void* U, const void* S, const void* Z,
-                                 int n_pad, int l, int a_begin, int a_rows, double* partials, int* nblocks,
-                                 cudaStream_t st) {
+                                 int n_pad, int l, int a_begin, int a_rows, double cmix, double* partials,
+                                 int* nblocks, cudaStream_t st) {
   switch (fam) {
-    case kRBF: return launch_dc_dp<T, kRBF>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
-    case kMatern12: return launch_dc_dp<T, kMatern12>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
-    case kMatern32: return launch_dc_dp<T, kMatern32>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
-    case kMatern52: return launch_dc_dp<T, kMatern52>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+    case kRBF: return launch_dc_dp<T, kRBF>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
+    case kMatern12: return launch_dc_dp<T, kMatern12>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
+    case kMatern32: return launch_dc_dp<T, kMatern32>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
+    case kMatern52: return launch_dc_dp<T, kMatern52>(dp, X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
   }
   return cudaErrorInvalidValue;
 }
 
 // U/S/Z layout: U [n_pad], S and Z column-major [l][n_pad]; X [n_pad][dp].
 cudaError_t launch_deriv_contract(bool fp64, int family, int dp, const void* X, const void* U, const void* SZ,
-                                  int a_begin, int a_rows, int n_pad, int l, double* partials, int* nblocks,
-                                  cudaStream_t st) {
+                                  int a_begin, int a_rows, int n_pad, int l, double cmix, double* partials,
+                                  int* nblocks, cudaStream_t st) {
   const size_t elem = fp64 ? 8 : 4;
   const void* S = SZ;
   const void* Z = static_cast<const unsigned char*>(SZ) + elem * static_cast<size_t>(l) * n_pad;
-  return fp64 ? launch_dc_fam<double>(family, dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st)
-              : launch_dc_fam<float>(family, dp, X, U, S, Z, n_pad, l, a_begin, a_rows, partials, nblocks, st);
+  return fp64 ? launch_dc_fam<double>(family, dp, X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st)
+              : launch_dc_fam<float>(family, dp, X, U, S, Z, n_pad, l, a_begin, a_rows, cmix, partials, nblocks, st);
 }
 
 }  // namespace gpk

@@ -1595,14 +1595,15 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
       conv(Zall, ldZ, l, SZp + elem * static_cast<size_t>(l) * n_pad);
       const void* Xp = fp64 ? static_cast<const void*>(c->X64s.p) : static_cast<const void*>(c->X32.p);
       int nblk = 0;
-      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, r0, nl, n_pad, l, nullptr,
+      const double cmix = static_cast<double>(n) / static_cast<double>(l);
+      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, r0, nl, n_pad, l, cmix, nullptr,
                                                  &nblk, c->st),
                       0, "deriv_contract");
-      const int na = 2 * (c->dp + 1);
+      const int na = c->dp + 1;
       DBuf<double> part;
       part.ensure(static_cast<size_t>(nblk) * na);
       auto ev = c->prof_begin(1);
-      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, r0, nl, n_pad, l, part.p,
+      c->check_launch(gpk::launch_deriv_contract(fp64, c->family, c->dp, Xp, Up, SZp, r0, nl, n_pad, l, cmix, part.p,
                                                  &nblk, c->st),
                       1, "deriv_contract");
       {
@@ -1617,28 +1618,24 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         for (int q = 0; q < na; ++q) tot[q] += hp[static_cast<size_t>(b) * na + q];
       tot = c->allreduce_host(tot);  // rank-ordered sum of the per-rank pair sums
       const double cpre = fp64 ? 1.0 : gpk::prescale_c(c->family);
-      const int DP = c->dp;
-      // outputscale: dK = 2 o shape ; lengthscale j: dK = (-2 o^2 / l_j) shape_ds ds_j^2
-      quadw[0] = 2.0 * c->o * tot[0];
-      const double g0 = 2.0 * c->o * tot[DP + 1];
+      // outputscale: dK = 2 o shape ; lengthscale j: dK = (-2 o^2 / l_j) shape_ds ds_j^2;
+      // tot[w] = quad[w] - (n/l) gamma[w] (raw), so the gradient is
+      // 0.5 (quad - tdet - (n/l)(gamma - sum_i t_wi)) theta_w   (gp_likelihood.hpp:97-100)
+      double mix[64];
+      mix[0] = 2.0 * c->o * tot[0];
       for (int i = 0; i < l; ++i) zw[0][i] = std::nan("");
       per_probe[0] = false;
-      double gsum[64];
-      gsum[0] = g0;
       for (int j = 0; j < d; ++j) {
         const double fac = (-2.0 * c->o2 / c->ls[j]) / cpre;
-        quadw[1 + j] = fac * tot[1 + j];
-        gsum[1 + j] = fac * tot[DP + 2 + j];
+        mix[1 + j] = fac * tot[1 + j];
         per_probe[1 + j] = false;
       }
       c->entries += static_cast<long long>(nl) * n;
-      // gradient for the non-noise parameters from the summed stochastic term
       for (int w = 0; w <= d; ++w) {
         double tsum = 0.0;
         for (int i = 0; i < l; ++i) tsum += tw[w][i];
-        const double stoch_w = static_cast<double>(n) / static_cast<double>(l) * (gsum[w] - tsum);
-        const double tau = tdet[w] + stoch_w;
-        res->gradient[w] = 0.5 * (quadw[w] - tau) * (w == 0 ? c->o : c->ls[w - 1]);
+        const double num = mix[w] - tdet[w] + static_cast<double>(n) / static_cast<double>(l) * tsum;
+        res->gradient[w] = 0.5 * num * (w == 0 ? c->o : c->ls[w - 1]);
         if (res->backward_gammas)
           for (int i = 0; i < l; ++i) res->backward_gammas[static_cast<size_t>(w) * l + i] = std::nan("");
       }

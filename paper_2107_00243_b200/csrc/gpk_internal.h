@@ -94,12 +94,12 @@ cudaError_t launch_kernel_column(int family, const double* sx, const double* x, 
                                  long long p, int which, double o2, double fac, double* out, cudaStream_t st);
 
 // Bilinear derivative contraction (backward pass, fast mode): for w = 0..d
-//   quad[w]  = sum_ab dK_w[a,b] u_a u_b
-//   gamma[w] = sum_ab dK_w[a,b] sum_i S[a,i] Z[b,i]
-// returns the raw (unscaled) sums; the host applies the factors.
+//   quad[w] - cmix gamma[w] = sum_ab dK_w[a,b] (u_a u_b - cmix sum_i S[a,i] Z[b,i])
+// (the gradient only needs this combination, cmix = n / l); returns the raw (unscaled) sums
+// per CTA, dp + 1 of them; the host applies the factors.
 // a-rows restricted to [a_begin, a_begin + a_rows) (this rank's shard), b over all n_pad rows.
 cudaError_t launch_deriv_contract(bool fp64, int family, int dp, const void* X, const void* U, const void* Zt,
-                                  int a_begin, int a_rows, int n_pad, int l, double* partials, int* nblocks,
-                                  cudaStream_t st);
+                                  int a_begin, int a_rows, int n_pad, int l, double cmix, double* partials,
+                                  int* nblocks, cudaStream_t st);
 
 }  // namespace gpk
