@@ -76,7 +76,7 @@ GPK_DEV void beta_step(SlotState& x, double rz_new, double zz, int k, double rel
 __global__ void cg_pap_alpha_kernel(const double* __restrict__ P, const double* __restrict__ Y, double sig2, int n,
                                     long long ldn, int nrb, double* __restrict__ part, unsigned* __restrict__ cnt,
                                     int k, SlotState* __restrict__ ss, double* __restrict__ alpha_hist,
-                                    int max_iters) {
+                                    int max_iters, unsigned long long* __restrict__ vmax) {
   __shared__ double red[kVT / 32];
   __shared__ bool last;
   const int s = blockIdx.y, b = blockIdx.x;
@@ -99,17 +99,18 @@ __global__ void cg_pap_alpha_kernel(const double* __restrict__ P, const double* 
   const double pap = reduce_chunks_cg(part + static_cast<long long>(s) * nrb, nrb, red);
   if (threadIdx.x == 0) {
     alpha_step(ss[s], pap, k, alpha_hist, max_iters);
+    if (vmax) vmax[s] = 0ull;
     cnt[s] = 0;
   }
 }
 
 cudaError_t launch_cg_pap_alpha(const double* P, const double* Y, double sig2, int n, long long ldn, int t,
                                 double* part, unsigned* cnt, int k, SlotState* ss, double* alpha_hist, int max_iters,
-                                cudaStream_t st) {
+                                cudaStream_t st, unsigned long long* vmax) {
   if (t <= 0) return cudaSuccess;
   const int nrb = (n + kRB - 1) / kRB;
   cg_pap_alpha_kernel<<<dim3(nrb, t), kVT, 0, st>>>(P, Y, sig2, n, ldn, nrb, part, cnt, k, ss, alpha_hist,
-                                                    max_iters);
+                                                    max_iters, vmax);
   return cudaGetLastError();
 }
 

@@ -447,7 +447,7 @@ struct gpk_ctx {
     return !(e && std::atoi(e) == 0);
   }();
   DBuf<unsigned> w_cnt, w_cnt2;
-  DBuf<double> w_prz, w_pzz, w_grz, w_gzz;
+  DBuf<double> w_prz, w_pzz;
   bool use_f64g = [] {  // env GPK_F64G=0 selects the FP64-pipe fp64 MVM (A/B checks)
     const char* e = std::getenv("GPK_F64G");
     return !(e && std::atoi(e) == 0);
@@ -1080,10 +1080,8 @@ struct gpk_ctx {
         w_g1.ensure(gpk::wood_g1_workspace(k, t));
         w_prz.ensure(gpk::wood_g2_partials(t));
         w_pzz.ensure(gpk::wood_g2_partials(t));
-        w_grz.ensure(gpk::wood_g2_groups(t));
-        w_gzz.ensure(gpk::wood_g2_groups(t));
-        w_cnt2.ensure(gpk::wood_g2_counters(t));
-        CK(cudaMemsetAsync(w_cnt2.p, 0, sizeof(unsigned) * gpk::wood_g2_counters(t), st));
+        w_cnt2.ensure(t);
+        CK(cudaMemsetAsync(w_cnt2.p, 0, sizeof(unsigned) * t, st));
       }
     }
     // pipelined read-back: snapshot of iteration it (async), then the decision on the
@@ -1116,25 +1114,27 @@ struct gpk_ctx {
         // read, P written) + L and C (n x k fp64 each)
         auto evv = prof_begin(3);
         const double vbytes = 8.0 * nl * (13.0 * ta + 2.0 * k);
-        check_launch(gpk::launch_cg_pap_alpha(Ps, w_kx.p, noise, nl, ldn, ta, ppap, w_cnt.p, it, ss, dh_a, max_iters,
-                                              st),
-                     1, "cg_pap_alpha");
         unsigned long long* vm = (!fp64 && use_tc && (gram_ok || tcg_direct) && ta <= 96) ? w_vmax.p : nullptr;
-        if (use_wood_s) {  // gpk_wood.cu: x/r update fused into the staged G1, staged G2 + dots + beta
+        check_launch(gpk::launch_cg_pap_alpha(Ps, w_kx.p, noise, nl, ldn, ta, ppap, w_cnt.p, it, ss, dh_a, max_iters,
+                                              st, use_wood_s ? vm : nullptr),
+                     1, "cg_pap_alpha");
+        if (use_wood_s) {  // gpk_wood.cu: x/r update fused into the staged G1, staged G2 + dots, beta + p
           check_launch(gpk::launch_g1s(L.p, n, k, Rs, ldn, ta, nl, w_g1.p, w_W.p, k, Xs, Ps, w_kx.p, noise, ss, st),
                        2, "g1s");
           check_launch(gpk::launch_g2s_dots_beta(C.p, n, k, w_W.p, k, ta, nl, Zs, Rs, ldn, pnoise, w_prz.p, w_pzz.p,
-                                                 w_grz.p, w_gzz.p, w_cnt2.p, it, rel_tol, ss, dh_b, dh_r, max_iters,
-                                                 vm, st),
-                       1, "g2s_dots_beta");
+                                                 st),
+                       (ta + 63) / 64, "g2s_dots");
+          check_launch(gpk::launch_cg_beta_p(Ps, Zs, nl, ldn, ta, ss, w_prz.p, w_pzz.p, w_cnt2.p, it, rel_tol, dh_b,
+                                             dh_r, max_iters, vm, st),
+                       1, "cg_beta_p");
         } else {
           check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, nl, ldn, ta, ss, st), 1, "cg_xr");
           check_launch(gpk::launch_g1(L.p, n, k, Rs, ldn, ta, nl, w_g1.p, w_W.p, k, st), 2, "g1");
           check_launch(gpk::launch_g2_dots_beta(C.p, n, k, w_W.p, k, ta, nl, Zs, Rs, ldn, pnoise, w_prz.p, w_pzz.p,
                                                 w_cnt.p + t, it, rel_tol, ss, dh_b, dh_r, max_iters, vm, st),
                        1, "g2_dots_beta");
+          check_launch(gpk::launch_cg_p_vmax(Ps, Zs, nl, ldn, ta, ss, vm, st), 1, "cg_p");
         }
-        check_launch(gpk::launch_cg_p_vmax(Ps, Zs, nl, ldn, ta, ss, vm, st), 1, "cg_p");
         prof_end(3, evv, vbytes, static_cast<double>(ta));
         vmax_ready = vm != nullptr;
         if (use_pipe) {

@@ -51,9 +51,11 @@ cudaError_t launch_woodbury_apply(const double* C, long long ldc, int ka, const 
 int g1_chunk_rows(int n);
 cudaError_t launch_g1_reduce(const double* part, int n, int ka, int tb, double* W, long long ldw, cudaStream_t st);
 int g2_row_blocks(int n);
+// vmax (nullable): cleared per column by the last CTA (the |p| maxima of this iteration's p
+// update are accumulated into it afterwards)
 cudaError_t launch_cg_pap_alpha(const double* P, const double* Y, double sig2, int n, long long ldn, int t,
                                 double* part, unsigned* cnt, int k, SlotState* ss, double* alpha_hist, int max_iters,
-                                cudaStream_t st);
+                                cudaStream_t st, unsigned long long* vmax = nullptr);
 cudaError_t launch_g1_xr(const double* L, long long ldl, int ka, double* X, const double* R, double* Rn,
                          const double* P, const double* Y, double sig2, long long ldn, int tb, int n,
                          const SlotState* ss, double* part, double* W, long long ldw, cudaStream_t st);
@@ -68,18 +70,21 @@ cudaError_t launch_cg_p_vmax(double* P, const double* Z, int n, long long ldn, i
 int wood_grid();
 size_t wood_g1_workspace(int ka, int tb);
 size_t wood_g2_partials(int tb);
-size_t wood_g2_groups(int tb);
-int wood_g2_counters(int tb);
 // W = A^T R_new (A: ka columns, ld lda); with X != null, R_new = R - alpha (Y + s2 P) for live
 // slots is written back to R and X += alpha P (krylov.hpp:94-95)
 cudaError_t launch_g1s(const double* A, long long lda, int ka, double* R, long long ldr, int tb, int n,
                        double* part, double* W, long long ldw, double* X, const double* P, const double* Y,
                        double sig2, const SlotState* ss, cudaStream_t st);
+// Z = (R - C W) / s2 with per-CTA r.z / z.z partials (prz, pzz: [tb][wood_grid()])
 cudaError_t launch_g2s_dots_beta(const double* C, long long ldc, int ka, const double* W, long long ldw, int tb,
                                  int n, double* Z, const double* R, long long ldn, double sig2, double* prz,
-                                 double* pzz, double* grz, double* gzz, unsigned* cnt, int k, double rel_tol,
-                                 SlotState* ss, double* beta_hist, double* resid_hist, int max_iters,
-                                 unsigned long long* vmax, cudaStream_t st);
+                                 double* pzz, cudaStream_t st);
+// beta_step from the G2s partials + p = z + beta p + |p| column maxima (vmax pre-cleared);
+// cnt: t zeroed counters (re-armed by the kernel)
+cudaError_t launch_cg_beta_p(double* P, const double* Z, int n, long long ldn, int t, SlotState* ss,
+                             const double* prz, const double* pzz, unsigned* cnt, int k, double rel_tol,
+                             double* beta_hist, double* resid_hist, int max_iters, unsigned long long* vmax,
+                             cudaStream_t st);
 
 int pchol_blocks(int n);
 struct PivotState {

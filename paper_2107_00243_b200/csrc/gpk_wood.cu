@@ -3,8 +3,8 @@
 //
 //   G1s: W = L^T r_new              (k x t, reduction over the n rows)
 //        fused with x += alpha p, r -= alpha (Kp + s2 p)            (krylov.hpp:94-95)
-//   G2s: z = (r - C W) / s2, per-block r.z / z.z partials, beta in the last CTA
-//                                                                     (krylov.hpp:96-119)
+//   G2s: z = (r - C W) / s2 and per-CTA r.z / z.z partials
+//   cg_beta_p: beta from those partials + p = z + beta p             (krylov.hpp:96-119)
 //
 // Both kernels give every CTA one contiguous run of rows (16-row units, the partition
 // is a function of n and the grid only), stage 64x64 fp64 operand tiles in padded shared
@@ -30,7 +30,6 @@ constexpr int kWT = 256;   // threads per CTA (8 warps)
 constexpr int kWS = 64;    // tile edge: rows per sub-chunk, columns per group, K per slab
 constexpr int kSR = 72;    // smem row stride (doubles) of the K-permuted tiles; 36 = 4 (mod 8) units
 constexpr int kUnit = 16;  // row-partition granularity
-constexpr int kGroup = 32; // CTAs per first-level group of the last-arrival reduction
 constexpr size_t kWSmem = 2ull * kWS * kSR * sizeof(double);  // 73728 B: two tiles
 
 // K permutation inside a 64-long K tile: DMMA k-step q (0..15) takes K indices
@@ -270,6 +269,63 @@ GPK_DEV void beta_step_s(SlotState& x, double rz_new, double zz, int k, double r
   x.rz = rz_new;
 }
 
+// ---- beta + p update (krylov.hpp:96-119): every CTA of column s sums the G2s partials in
+// the same fixed order (identical rz_new, zz), runs beta_step on its own copy of the slot
+// state and updates its rows of p = z + beta p with the |p| maxima of the next fp16 pack;
+// the LAST CTA of the column to arrive (every other one has read the old state by then)
+// stores the updated state.  This replaces G2s's last-arrival tail, during which the rest
+// of the GPU idled (ncu: SMs active 56% of the G2s elapsed time).
+__global__ void __launch_bounds__(kWT) cg_beta_p_kernel(double* __restrict__ P, const double* __restrict__ Z, int n,
+                                                        long long ldn, SlotState* __restrict__ ss,
+                                                        const double* __restrict__ prz,
+                                                        const double* __restrict__ pzz, int G,
+                                                        unsigned* __restrict__ cnt, int k, double rel_tol,
+                                                        double* __restrict__ beta_hist,
+                                                        double* __restrict__ resid_hist, int max_iters,
+                                                        unsigned long long* __restrict__ vmax) {
+  __shared__ double red[kWT / 32];
+  const int s = blockIdx.y, tid = threadIdx.x;
+  SlotState x = ss[s];
+  double a = 0.0, z = 0.0;
+  for (int b = tid; b < G; b += kWT) {  // thread-strided, then the fixed block tree
+    a += __ldcg(prz + static_cast<long long>(s) * G + b);
+    z += __ldcg(pzz + static_cast<long long>(s) * G + b);
+  }
+  const double rz_new = block_sum(a, red);
+  const double zz = block_sum(z, red);
+  const bool first = blockIdx.x == 0;
+  beta_step_s(x, rz_new, zz, k, rel_tol, first ? beta_hist : nullptr, first ? resid_hist : nullptr, max_iters);
+  const bool live = x.flag == 0;
+  const double beta = x.beta;
+  double mx = 0.0;
+  for (int i = blockIdx.x * kWT + tid; i < n; i += gridDim.x * kWT) {
+    const long long o = s * ldn + i;
+    double p = P[o];
+    if (live) {
+      p = Z[o] + beta * p;  // krylov.hpp:116 (cg_update_p_kernel's expression)
+      P[o] = p;
+    }
+    mx = fmax(mx, fabs(p));
+  }
+  if (vmax) {  // CTA maximum first: one atomic per CTA (order-independent, so deterministic)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 1; q < kWT / 32; ++q) mx = fmax(mx, red[q]);
+      if (mx > 0.0) atomicMax(vmax + s, static_cast<unsigned long long>(__double_as_longlong(mx)));
+    }
+  }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(cnt + s, 1u) == gridDim.x - 1) {
+      ss[s] = x;
+      cnt[s] = 0;
+    }
+  }
+}
+
 // Z tile operand layout: Cs[kk][i ^ 4 ((kk >> 4) & 3)] (row stride 64): the A fragments of
 // the permuted k-steps are conflict-free 64-bit loads; pairs (2p, 2p+1) stay adjacent.
 GPK_DEV int cswz(int kk) { return ((kk >> 4) & 3) * 4; }
@@ -280,15 +336,11 @@ template <bool VEC, int NT>
 __global__ void __launch_bounds__(kWT, 2)
     g2s_dots_beta_kernel(const double* __restrict__ C, long long ldc, int ka, const double* __restrict__ W,
                          long long ldw, int s0, int ns, int n, double* __restrict__ Z, const double* __restrict__ R,
-                         long long ldn, double sig2, double* __restrict__ prz, double* __restrict__ pzz,
-                         double* __restrict__ grz, double* __restrict__ gzz, unsigned* __restrict__ cnt, int k,
-                         double rel_tol, SlotState* __restrict__ ss, double* __restrict__ beta_hist,
-                         double* __restrict__ resid_hist, int max_iters, unsigned long long* __restrict__ vmax) {
+                         long long ldn, double sig2, double* __restrict__ prz, double* __restrict__ pzz) {
   extern __shared__ __align__(16) double wsm[];
   double* Cs = wsm;              // [kk][i ^ cswz(kk)], stride 64
   double* Ws = wsm + kWS * kSR;  // [s][kpos(kk)], stride 72
   __shared__ double srz[8][kWS], szz[8][kWS];
-  __shared__ int stage;  // 0: not last; 1: last of its group; 2: last group too
   const int G = gridDim.x, b = blockIdx.x;
   int r0, r1;
   rows_of(b, G, n, r0, r1);
@@ -390,68 +442,13 @@ __global__ void __launch_bounds__(kWT, 2)
     prz[static_cast<long long>(s0 + tid) * G + b] = crun;
     pzz[static_cast<long long>(s0 + tid) * G + b] = zrun;
   }
-  // ---- last-arrival reduction: group g = b / 32 first, then the groups.  Each stage stages
-  // every partial it needs in the free operand tiles (all loads in flight at once) and sums
-  // per column in fixed order.
-  const int ng = (G + kGroup - 1) / kGroup, g = b / kGroup;
-  const int g0 = g * kGroup, gc = min(kGroup, G - g0);
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    stage = atomicAdd(cnt + g, 1u) == static_cast<unsigned>(gc - 1) ? 1 : 0;
-  }
-  __syncthreads();
-  if (stage == 0) return;
-  __threadfence();
-  double* sp = wsm;
-  for (int e = tid; e < 2 * ns * gc; e += kWT) {  // sp[h][s][q]
-    const int h = e / (ns * gc), rem = e % (ns * gc), sl = rem / gc, q = rem % gc;
-    sp[e] = __ldcg((h ? pzz : prz) + static_cast<long long>(s0 + sl) * G + g0 + q);
-  }
-  __syncthreads();
-  if (tid < ns) {
-    double a = 0.0, z = 0.0;
-    for (int q = 0; q < gc; ++q) {
-      a += sp[tid * gc + q];
-      z += sp[(ns + tid) * gc + q];
-    }
-    grz[static_cast<long long>(s0 + tid) * ng + g] = a;
-    gzz[static_cast<long long>(s0 + tid) * ng + g] = z;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    cnt[g] = 0;
-    __threadfence();
-    stage = atomicAdd(cnt + ng, 1u) == static_cast<unsigned>(ng - 1) ? 2 : 0;
-  }
-  __syncthreads();
-  if (stage != 2) return;
-  __threadfence();
-  for (int e = tid; e < 2 * ns * ng; e += kWT) {  // sp[h][s][q]
-    const int h = e / (ns * ng), rem = e % (ns * ng);
-    sp[e] = __ldcg((h ? gzz : grz) + static_cast<long long>(s0) * ng + rem);
-  }
-  __syncthreads();
-  if (tid < ns) {
-    double rz = 0.0, zz = 0.0;
-    for (int q = 0; q < ng; ++q) {
-      rz += sp[tid * ng + q];
-      zz += sp[(ns + tid) * ng + q];
-    }
-    beta_step_s(ss[s0 + tid], rz, zz, k, rel_tol, beta_hist, resid_hist, max_iters);
-    if (vmax) vmax[s0 + tid] = 0ull;
-  }
-  if (tid == 0) cnt[ng] = 0;
 }
 
 int wood_grid() { return 2 * sm_count(); }
 
 size_t wood_g1_workspace(int ka, int tb) { return static_cast<size_t>(wood_grid()) * ka * tb; }
-// prz, pzz: tb * G each; grz, gzz: tb * ceil(G / 32) each; counters: (ceil(G / 32) + 1) per
-// 64-column group
+// prz, pzz: tb * G each
 size_t wood_g2_partials(int tb) { return static_cast<size_t>(tb) * wood_grid(); }
-size_t wood_g2_groups(int tb) { return static_cast<size_t>(tb) * ((wood_grid() + kGroup - 1) / kGroup); }
-int wood_g2_counters(int tb) { return ((wood_grid() + kGroup - 1) / kGroup + 1) * ((tb + kWS - 1) / kWS); }
 
 namespace {
 
@@ -491,8 +488,7 @@ cudaError_t g1s_dispatch(int nt, dim3 g, cudaStream_t st, const double* A, long 
 template <bool VEC, int NT>
 cudaError_t g2s_launch(cudaStream_t st, const double* C, long long ldc, int ka, const double* W, long long ldw,
                        int s0, int ns, int n, double* Z, const double* R, long long ldn, double sig2, double* prz,
-                       double* pzz, double* grz, double* gzz, unsigned* cnt, int k, double rel_tol, SlotState* ss,
-                       double* beta_hist, double* resid_hist, int max_iters, unsigned long long* vmax) {
+                       double* pzz) {
   static bool cfg = false;
   if (!cfg) {
     cudaError_t e = set_smem(g2s_dots_beta_kernel<VEC, NT>);
@@ -500,8 +496,7 @@ cudaError_t g2s_launch(cudaStream_t st, const double* C, long long ldc, int ka, 
     cfg = true;
   }
   g2s_dots_beta_kernel<VEC, NT><<<wood_grid(), kWT, kWSmem, st>>>(C, ldc, ka, W, ldw, s0, ns, n, Z, R, ldn, sig2,
-                                                                   prz, pzz, grz, gzz, cnt, k, rel_tol, ss,
-                                                                   beta_hist, resid_hist, max_iters, vmax);
+                                                                   prz, pzz);
   return cudaGetLastError();
 }
 
@@ -539,22 +534,16 @@ cudaError_t launch_g1s(const double* A, long long lda, int ka, double* R, long l
 
 cudaError_t launch_g2s_dots_beta(const double* C, long long ldc, int ka, const double* W, long long ldw, int tb,
                                  int n, double* Z, const double* R, long long ldn, double sig2, double* prz,
-                                 double* pzz, double* grz, double* gzz, unsigned* cnt, int k, double rel_tol,
-                                 SlotState* ss, double* beta_hist, double* resid_hist, int max_iters,
-                                 unsigned long long* vmax, cudaStream_t st) {
+                                 double* pzz, cudaStream_t st) {
   if (tb <= 0) return cudaSuccess;
   const bool vec = aligned16(C) && aligned16(W) && ldc % 2 == 0 && ldw % 2 == 0;
-  const int ncnt = (wood_grid() + kGroup - 1) / kGroup + 1;
-  for (int s0 = 0, grp = 0; s0 < tb; s0 += kWS, ++grp) {
+  for (int s0 = 0; s0 < tb; s0 += kWS) {
     const int ns = std::min(kWS, tb - s0), nt = (ns + 7) / 8;
-    unsigned* c = cnt + grp * ncnt;
     cudaError_t e = cudaSuccess;
-#define GPK_G2S(NTV)                                                                                                \
-  case NTV:                                                                                                         \
-    e = vec ? g2s_launch<true, NTV>(st, C, ldc, ka, W, ldw, s0, ns, n, Z, R, ldn, sig2, prz, pzz, grz, gzz, c, k,    \
-                                    rel_tol, ss, beta_hist, resid_hist, max_iters, vmax)                            \
-            : g2s_launch<false, NTV>(st, C, ldc, ka, W, ldw, s0, ns, n, Z, R, ldn, sig2, prz, pzz, grz, gzz, c, k,   \
-                                     rel_tol, ss, beta_hist, resid_hist, max_iters, vmax);                          \
+#define GPK_G2S(NTV)                                                                                           \
+  case NTV:                                                                                                    \
+    e = vec ? g2s_launch<true, NTV>(st, C, ldc, ka, W, ldw, s0, ns, n, Z, R, ldn, sig2, prz, pzz)               \
+            : g2s_launch<false, NTV>(st, C, ldc, ka, W, ldw, s0, ns, n, Z, R, ldn, sig2, prz, pzz);             \
     break;
     switch (nt) {
       GPK_G2S(1) GPK_G2S(2) GPK_G2S(3) GPK_G2S(4) GPK_G2S(5) GPK_G2S(6) GPK_G2S(7) GPK_G2S(8)
@@ -563,6 +552,18 @@ cudaError_t launch_g2s_dots_beta(const double* C, long long ldc, int ka, const d
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_cg_beta_p(double* P, const double* Z, int n, long long ldn, int t, SlotState* ss,
+                             const double* prz, const double* pzz, unsigned* cnt, int k, double rel_tol,
+                             double* beta_hist, double* resid_hist, int max_iters, unsigned long long* vmax,
+                             cudaStream_t st) {
+  if (t <= 0) return cudaSuccess;
+  int bx = (n + 4 * kWT - 1) / (4 * kWT);
+  if (bx > 32) bx = 32;
+  cg_beta_p_kernel<<<dim3(bx, t), kWT, 0, st>>>(P, Z, n, ldn, ss, prz, pzz, wood_grid(), cnt, k, rel_tol, beta_hist,
+                                                resid_hist, max_iters, vmax);
+  return cudaGetLastError();
 }
 
 }  // namespace gpk
