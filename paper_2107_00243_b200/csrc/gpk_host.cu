@@ -1090,10 +1090,13 @@ struct gpk_ctx {
     int pend_buf = -1;
     snap_h.ensure(sizeof(gpk::SlotState) * 2 * static_cast<size_t>(t));
     auto* snaps = reinterpret_cast<gpk::SlotState*>(snap_h.p);
-    auto readback = [&](int it) {
+    // written_by_kernel: the iteration's last kernel already stored the snapshot into the
+    // pinned buffer (no copy-engine round trip)
+    auto readback = [&](int it, bool written_by_kernel = false) {
       const int bcur = it & 1;
-      CK(cudaMemcpyAsync(snaps + static_cast<size_t>(bcur) * t, ss, sizeof(gpk::SlotState) * ta,
-                         cudaMemcpyDeviceToHost, st));
+      if (!written_by_kernel)
+        CK(cudaMemcpyAsync(snaps + static_cast<size_t>(bcur) * t, ss, sizeof(gpk::SlotState) * ta,
+                           cudaMemcpyDeviceToHost, st));
       CK(cudaEventRecord(snap_ev.get(bcur), st));
       const int take = it == max_iters ? bcur : pend_buf;  // the last iteration drains
       pend_buf = bcur;
@@ -1125,7 +1128,8 @@ struct gpk_ctx {
                                                  st),
                        (ta + 63) / 64, "g2s_dots");
           check_launch(gpk::launch_cg_beta_p(Ps, Zs, nl, ldn, ta, ss, w_prz.p, w_pzz.p, w_cnt2.p, it, rel_tol, dh_b,
-                                             dh_r, max_iters, vm, st),
+                                             dh_r, max_iters, vm,
+                                             use_pipe ? snaps + static_cast<size_t>(it & 1) * t : nullptr, st),
                        1, "cg_beta_p");
         } else {
           check_launch(gpk::launch_cg_update_xr(Xs, Rs, Ps, w_kx.p, noise, nl, ldn, ta, ss, st), 1, "cg_xr");
@@ -1138,7 +1142,7 @@ struct gpk_ctx {
         prof_end(3, evv, vbytes, static_cast<double>(ta));
         vmax_ready = vm != nullptr;
         if (use_pipe) {
-          readback(it);
+          readback(it, use_wood_s);
           continue;
         }
         if (it % sync_every == 0 || it == max_iters) {

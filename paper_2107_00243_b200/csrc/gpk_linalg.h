@@ -80,11 +80,12 @@ cudaError_t launch_g2s_dots_beta(const double* C, long long ldc, int ka, const d
                                  int n, double* Z, const double* R, long long ldn, double sig2, double* prz,
                                  double* pzz, cudaStream_t st);
 // beta_step from the G2s partials + p = z + beta p + |p| column maxima (vmax pre-cleared);
-// cnt: t zeroed counters (re-armed by the kernel)
+// cnt: t zeroed counters (re-armed by the kernel); snap (nullable, pinned host memory): a
+// copy of the updated slot states for the host's pipelined read-back
 cudaError_t launch_cg_beta_p(double* P, const double* Z, int n, long long ldn, int t, SlotState* ss,
                              const double* prz, const double* pzz, unsigned* cnt, int k, double rel_tol,
                              double* beta_hist, double* resid_hist, int max_iters, unsigned long long* vmax,
-                             cudaStream_t st);
+                             SlotState* snap, cudaStream_t st);
 
 int pchol_blocks(int n);
 struct PivotState {

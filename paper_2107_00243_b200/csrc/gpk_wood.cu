@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(kWT) cg_beta_p_kernel(double* __restrict__ P, 
                                                         unsigned* __restrict__ cnt, int k, double rel_tol,
                                                         double* __restrict__ beta_hist,
                                                         double* __restrict__ resid_hist, int max_iters,
-                                                        unsigned long long* __restrict__ vmax) {
+                                                        unsigned long long* __restrict__ vmax,
+                                                        SlotState* __restrict__ snap) {
   __shared__ double red[kWT / 32];
   const int s = blockIdx.y, tid = threadIdx.x;
   SlotState x = ss[s];
@@ -322,6 +323,10 @@ __global__ void __launch_bounds__(kWT) cg_beta_p_kernel(double* __restrict__ P, 
     if (atomicAdd(cnt + s, 1u) == gridDim.x - 1) {
       ss[s] = x;
       cnt[s] = 0;
+      if (snap) {  // the host's copy of the slot state, straight into pinned memory
+        snap[s] = x;
+        __threadfence_system();
+      }
     }
   }
 }
@@ -557,12 +562,12 @@ cudaError_t launch_g2s_dots_beta(const double* C, long long ldc, int ka, const d
 cudaError_t launch_cg_beta_p(double* P, const double* Z, int n, long long ldn, int t, SlotState* ss,
                              const double* prz, const double* pzz, unsigned* cnt, int k, double rel_tol,
                              double* beta_hist, double* resid_hist, int max_iters, unsigned long long* vmax,
-                             cudaStream_t st) {
+                             SlotState* snap, cudaStream_t st) {
   if (t <= 0) return cudaSuccess;
   int bx = (n + 4 * kWT - 1) / (4 * kWT);
   if (bx > 32) bx = 32;
   cg_beta_p_kernel<<<dim3(bx, t), kWT, 0, st>>>(P, Z, n, ldn, ss, prz, pzz, wood_grid(), cnt, k, rel_tol, beta_hist,
-                                                resid_hist, max_iters, vmax);
+                                                resid_hist, max_iters, vmax, snap);
   return cudaGetLastError();
 }
 
