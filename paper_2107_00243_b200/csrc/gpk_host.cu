@@ -191,6 +191,24 @@ __global__ void to_padded_kernel(const double* __restrict__ src, long long lds, 
   const int c = static_cast<int>(idx / n_pad), i = static_cast<int>(idx % n_pad);
   dst[idx] = static_cast<T>(i < n ? src[c * lds + i] : 0.0);
 }
+// t_{w,i} = (dL_w' q_i).(L' z_i) + (L' q_i).(dL_w' z_i)  (LowRankDerivOp::apply,
+// preconditioners.hpp:62-69): one warp per (w, i), lane-strided sums + a fixed butterfly
+__global__ void precond_trace_terms_kernel(const double* __restrict__ Bq, const double* __restrict__ Bz,
+                                           const double* __restrict__ A, int k, int kw, int l, int nw,
+                                           double* __restrict__ out) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (gw >= nw * l) return;
+  const int w = gw / l, i = gw % l;
+  const double* bq = Bq + static_cast<size_t>(i) * kw + static_cast<size_t>(w) * k;
+  const double* bz = Bz + static_cast<size_t>(i) * kw + static_cast<size_t>(w) * k;
+  const double* aq = A + static_cast<size_t>(i) * k;
+  const double* az = A + static_cast<size_t>(l + i) * k;
+  double acc = 0.0;
+  for (int q = lane; q < k; q += 32) acc += bq[q] * az[q] + aq[q] * bz[q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[static_cast<size_t>(w) * l + i] = acc;
+}
 __global__ void gather_slots_kernel(const gpk::SlotState* __restrict__ src, const int* __restrict__ map, int nt,
                                     gpk::SlotState* __restrict__ dst) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1418,11 +1436,18 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   };
   std::vector<std::thread> slq_threads;
   {
+    // one launcher thread spawns the workers (creating 16 threads here stalled the stream's
+    // next launch by ~0.35 ms)
     const int nth = std::max(1, std::min<int>(l, std::min(16u, std::max(1u, std::thread::hardware_concurrency()))));
-    for (int th = 0; th < nth; ++th)
-      slq_threads.emplace_back([&slq_probe, l, nth, th] {
-        for (int i = th; i < l; i += nth) slq_probe(i);
-      });
+    slq_threads.emplace_back([&slq_probe, l, nth] {
+      std::vector<std::thread> workers;
+      for (int th = 1; th < nth; ++th)
+        workers.emplace_back([&slq_probe, l, nth, th] {
+          for (int i = th; i < l; i += nth) slq_probe(i);
+        });
+      for (int i = 0; i < l; i += nth) slq_probe(i);
+      for (auto& wk : workers) wk.join();
+    });
   }
   auto finish_forward = [&]() {
     for (auto& th : slq_threads) th.join();
@@ -1499,11 +1524,9 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
                                        k, c->st),
                         2, "g1");
         c->allreduce_sum(A.p, 2LL * l * k);
-        std::vector<double> hA(static_cast<size_t>(2) * l * k);
-        c->d2h(hA.data(), A.p, sizeof(double) * hA.size());
         // all d+1 derivative factors at once: dL is [w][n x k], i.e. one n x (d+1)k matrix
         const int kw = (d + 1) * k;
-        DBuf<double> Bq, Bz, partw;
+        DBuf<double> Bq, Bz, partw, dtw;
         Bq.ensure(static_cast<size_t>(l) * kw);
         Bz.ensure(static_cast<size_t>(l) * kw);
         partw.ensure(gpk::g1_workspace(nl, kw, l));
@@ -1511,21 +1534,15 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         c->check_launch(gpk::launch_g1(c->dL.p + r0, n, kw, Zc.p, ldn, l, nl, partw.p, Bz.p, kw, c->st), 2, "g1");
         c->allreduce_sum(Bq.p, static_cast<long long>(l) * kw);
         c->allreduce_sum(Bz.p, static_cast<long long>(l) * kw);
-        std::vector<double> hq(static_cast<size_t>(l) * kw), hz(static_cast<size_t>(l) * kw);
-        CK(cudaMemcpyAsync(hq.data(), Bq.p, sizeof(double) * hq.size(), cudaMemcpyDeviceToHost, c->st));
-        c->d2h(hz.data(), Bz.p, sizeof(double) * hz.size());
+        dtw.ensure(static_cast<size_t>(d + 1) * l);
+        precond_trace_terms_kernel<<<static_cast<unsigned>(((d + 1) * l * 32 + 255) / 256), 256, 0, c->st>>>(
+            Bq.p, Bz.p, A.p, k, kw, l, d + 1, dtw.p);
+        c->check_launch(cudaGetLastError(), 1, "precond_trace_terms");
+        std::vector<double> htw(static_cast<size_t>(d + 1) * l);
+        c->d2h(htw.data(), dtw.p, sizeof(double) * htw.size());
         for (int w = 0; w <= d; ++w) {
           tdet[w] = c->trace_det[w];
-          for (int i = 0; i < l; ++i) {
-            // (dL' q_i).(L' z_i) + (L' q_i).(dL' z_i)   (LowRankDerivOp::apply, preconditioners.hpp:62-69)
-            double acc = 0.0;
-            const double* bq = hq.data() + static_cast<size_t>(i) * kw + static_cast<size_t>(w) * k;
-            const double* bz = hz.data() + static_cast<size_t>(i) * kw + static_cast<size_t>(w) * k;
-            const double* aq = hA.data() + static_cast<size_t>(i) * k;
-            const double* az = hA.data() + static_cast<size_t>(l + i) * k;
-            for (int q = 0; q < k; ++q) acc += bq[q] * az[q] + aq[q] * bz[q];
-            tw[w][i] = acc;
-          }
+          for (int i = 0; i < l; ++i) tw[w][i] = htw[static_cast<size_t>(w) * l + i];
         }
       }
     }
