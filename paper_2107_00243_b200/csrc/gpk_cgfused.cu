@@ -327,7 +327,7 @@ cudaError_t launch_g1_xr(const double* L, long long ldl, int ka, double* X, cons
                          const double* P, const double* Y, double sig2, long long ldn, int tb, int n,
                          const SlotState* ss, double* part, double* W, long long ldw, cudaStream_t st) {
   if (ka <= 0 || tb <= 0) return cudaSuccess;
-  const int ch = g1_chunk_rows(n);
+  const int ch = g1_chunk_rows(n, ka);
   const int nch = (n + ch - 1) / ch;
   dim3 g(nch, (ka + 63) / 64, (tb + 63) / 64);
   g1_xr_kernel<<<g, 256, 0, st>>>(L, ldl, ka, X, R, Rn, P, Y, sig2, ldn, tb, n, ch, ss, part);

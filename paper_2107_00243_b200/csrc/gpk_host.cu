@@ -814,8 +814,8 @@ struct gpk_ctx {
     }
     if (fp64 && which < 0 && use_f64g) {  // gpk_mvm_f64g.cu: reference-order entries, DMMA products
       const int cf[] = {2, 3, 6, 9};
-      for (int c0 = 0; c0 < t; c0 += 64) {
-        const int tc = std::min(64, t - c0);
+      for (int c0 = 0; c0 < t; c0 += 72) {
+        const int tc = std::min(72, t - c0);
         const double fl = static_cast<double>(nl) * n * (2.0 * tc + 3.0 * d + cf[family]);
         auto ev = prof_begin(2);
         check_launch(gpk::launch_fused_kmvm_f64g(family, dp, X64s.p, sq.p, n, V + c0 * ldv, ldv, tc, out + c0 * ldo,

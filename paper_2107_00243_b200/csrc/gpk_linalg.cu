@@ -297,9 +297,12 @@ GPK_DEV void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// rows per G1 chunk: a function of n only (~128 chunks), multiple of 16
-static int g1_chunk(int n) {
+// rows per G1 chunk: a function of n (~128 chunks), multiple of 16; for wide products
+// (ka >= 512: the d+1 derivative factors of the backward pass, ka = (d+1) k) at most 32
+// chunks, so the chunk partials (nch x ka x tb) stay well below the A operand's size
+static int g1_chunk(int n, int ka = 0) {
   int ch = (n + 127) / 128;
+  if (ka >= 512) ch = (n + 31) / 32;
   ch = (ch + 15) / 16 * 16;
   return ch < 64 ? 64 : ch;
 }
@@ -386,10 +389,10 @@ __global__ void g1_reduce_kernel(const double* __restrict__ part, int nch, int k
   }
 }
 
-int g1_chunk_rows(int n) { return g1_chunk(n); }
+int g1_chunk_rows(int n, int ka) { return g1_chunk(n, ka); }
 
 cudaError_t launch_g1_reduce(const double* part, int n, int ka, int tb, double* W, long long ldw, cudaStream_t st) {
-  const int ch = g1_chunk(n);
+  const int ch = g1_chunk(n, ka);
   const int nch = (n + ch - 1) / ch;
   const long long tot = static_cast<long long>(ka) * tb;
   g1_reduce_kernel<<<static_cast<unsigned>((tot + 63) / 64), 256, 0, st>>>(part, nch, ka, tb, W, ldw);
@@ -397,14 +400,14 @@ cudaError_t launch_g1_reduce(const double* part, int n, int ka, int tb, double* 
 }
 
 size_t g1_workspace(int n, int ka, int tb) {
-  const int ch = g1_chunk(n);
+  const int ch = g1_chunk(n, ka);
   return static_cast<size_t>((n + ch - 1) / ch) * ka * tb;
 }
 
 cudaError_t launch_g1(const double* A, long long lda, int ka, const double* B, long long ldb, int tb, int n,
                       double* part, double* W, long long ldw, cudaStream_t st) {
   if (ka <= 0 || tb <= 0) return cudaSuccess;
-  const int ch = g1_chunk(n);
+  const int ch = g1_chunk(n, ka);
   const int nch = (n + ch - 1) / ch;
   dim3 g(nch, (ka + 63) / 64, (tb + 63) / 64);
   g1_kernel<<<g, 256, 0, st>>>(A, lda, ka, B, ldb, tb, n, ch, part);

@@ -48,7 +48,7 @@ cudaError_t launch_woodbury_apply(const double* C, long long ldc, int ka, const 
                                   long long ldz, cudaStream_t st);
 
 // gpk_cgfused.cu: the fused single-rank CG iteration (see the file header)
-int g1_chunk_rows(int n);
+int g1_chunk_rows(int n, int ka = 0);
 cudaError_t launch_g1_reduce(const double* part, int n, int ka, int tb, double* W, long long ldw, cudaStream_t st);
 int g2_row_blocks(int n);
 // vmax (nullable): cleared per column by the last CTA (the |p| maxima of this iteration's p

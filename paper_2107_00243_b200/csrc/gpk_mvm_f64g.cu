@@ -196,7 +196,7 @@ cudaError_t f64g_nt(int nt, const double* X, const double* sq, int n, const doub
   case NTV:           \
     return f64g_launch<FAM, DP, NTV, VEC>(X, sq, n, V, ldv, tc, out, ldo, scale, row_begin, row_end, st);
   switch (nt) {
-    GPK_F64G(1) GPK_F64G(2) GPK_F64G(3) GPK_F64G(4) GPK_F64G(5) GPK_F64G(6) GPK_F64G(7) GPK_F64G(8)
+    GPK_F64G(1) GPK_F64G(2) GPK_F64G(3) GPK_F64G(4) GPK_F64G(5) GPK_F64G(6) GPK_F64G(7) GPK_F64G(8) GPK_F64G(9)
   }
 #undef GPK_F64G
   return cudaErrorInvalidValue;
@@ -233,12 +233,13 @@ cudaError_t f64g_fam(int family, int dp, int nt, const double* X, const double* 
 }  // namespace
 
 // X: packed fp64 scaled rows [n_pad][dp] (zero padding), sq: reference squared norms (n),
-// V: column-major [tc][ldv] with all n rows, tc <= 64; out rows [row_begin, row_end).
+// V: column-major [tc][ldv] with all n rows, tc <= 72 (t = l + 1 = 65 at C5 in one launch: the
+// entry evaluation, not the column count, sets the cost); out rows [row_begin, row_end).
 cudaError_t launch_fused_kmvm_f64g(int family, int dp, const double* X, const double* sq, int n, const double* V,
                                    long long ldv, int tc, double* out, long long ldo, double scale, int row_begin,
                                    int row_end, cudaStream_t st) {
   if (tc <= 0 || row_end <= row_begin) return cudaSuccess;
-  if (tc > 64) return cudaErrorInvalidValue;
+  if (tc > 72) return cudaErrorInvalidValue;
   const int nt = (tc + 7) / 8;
   const bool vec = (reinterpret_cast<uintptr_t>(V) & 15) == 0 && ldv % 2 == 0;
   return vec ? f64g_fam<true>(family, dp, nt, X, sq, n, V, ldv, tc, out, ldo, scale, row_begin, row_end, st)

@@ -229,6 +229,28 @@ def test_grid_evaluate_mll_matches_oracle(orc, case, backward):
     np.testing.assert_allclose(r.forward_gammas, g["forward_gammas"], rtol=1e-7, atol=1e-12)
 
 
+@pytest.mark.parametrize("precision", ["fp64", "tf32x3"])
+def test_wide_faithful_backward_matches_oracle(orc, precision):
+    """Reference-faithful backward with (d+1) l = 96 right-hand sides: the fused single-rank CG
+    iteration runs its Woodbury G1s / G2s in two column groups (64 + 32) and the beta/p update
+    over all 96 columns; value, log-det and every gradient component match the oracle."""
+    n, d, l = 640, 3, 24
+    x = orc.random_matrix(n, d, 3100)
+    y = np.cos(3 * x[:, 1]) + 0.1 * orc.random_matrix(n, 1, 3101)[:, 0]
+    p = orc.Params(d, 1.0, 0.6, 0.03)
+    z = orc.make_probes(n, l, 3102)
+    want = orc.evaluate_mll(orc.MATERN52, x, p, y, z, seed=3102, prec="pivchol", rank=12, max_iters=400,
+                            rel_tol=1e-9)
+    op = make_op("matern52", x, p, d)
+    pc = gk.pivoted_cholesky_with_derivatives(op, 12)
+    r = gk.evaluate_mll(y, op, pc, gk.make_probes(n, l, 3102),
+                        gk.MllConfig(gk.CgConfig(400, 1e-9, False, precision, 2), True, "faithful"))
+    tol = 1e-8 if precision == "fp64" else 1e-5
+    assert r.value == pytest.approx(want["value"], rel=tol)
+    assert r.logdet == pytest.approx(want["logdet"], rel=tol)
+    np.testing.assert_allclose(r.gradient, want["gradient"], rtol=100 * tol, atol=1e-8)
+
+
 def test_identity_and_unshared_probes_match_oracle(orc):
     n, d = 250, 2
     x = orc.random_matrix(n, d, 85)
