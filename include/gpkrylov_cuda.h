@@ -277,7 +277,8 @@ void* gpk_stream(const gpk_ctx* ctx);
  * single-rank CG vector phase (alpha, x/r update + Woodbury, beta, p update; its "flops"
  * field holds algorithmic HBM bytes).
  * Returns accumulated device milliseconds, launch count and algorithmic flops /
- * kernel entries since the last reset. */
+ * kernel entries since the last reset.  on: 0 off, 1 kinds 0 and 1, otherwise a bitmask of
+ * kinds (bit k = kind k; each recorded launch costs two event records on the stream). */
 gpk_status gpk_profile_enable(gpk_ctx* ctx, int on);
 gpk_status gpk_profile_read(gpk_ctx* ctx, int kind, double* ms, long long* launches, double* flops, double* entries);
 gpk_status gpk_profile_reset(gpk_ctx* ctx);

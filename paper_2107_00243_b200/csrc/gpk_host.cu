@@ -546,6 +546,7 @@ struct gpk_ctx {
     long long launches = 0;
   };
   bool prof_on = false;
+  unsigned prof_mask = 3u;  // kinds recorded while enabled (bit k = kind k)
   Prof prof[4];  // 0: reduced-precision value MVM, 1: derivative pass, 2: fp64 MVM, 3: CG vector phase
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t ev_get() {
@@ -560,8 +561,7 @@ struct gpk_ctx {
   }
   // bracket one launch of kind `kd` with events when profiling is on
   std::pair<cudaEvent_t, cudaEvent_t> prof_begin(int kd) {
-    (void)kd;
-    if (!prof_on) return {nullptr, nullptr};
+    if (!prof_on || !(prof_mask & (1u << kd))) return {nullptr, nullptr};
     cudaEvent_t a = ev_get(), b = ev_get();
     CK(cudaEventRecord(a, st));
     return {a, b};
@@ -1872,7 +1872,10 @@ gpk_status gpk_get_mvm_variant(gpk_ctx* ctx, int* variant, double* max_sqnorm) {
 }
 
 gpk_status gpk_profile_enable(gpk_ctx* ctx, int on) {
-  return guard(ctx, [&] { ctx->prof_on = on != 0; });
+  return guard(ctx, [&] {
+    ctx->prof_on = on != 0;
+    ctx->prof_mask = on == 1 ? 3u : static_cast<unsigned>(on) & 15u;  // 1: kinds 0 and 1; else a mask
+  });
 }
 gpk_status gpk_profile_read(gpk_ctx* ctx, int kind, double* ms, long long* launches, double* flops,
                             double* entries) {

@@ -16,6 +16,7 @@
 // gpk_cgfused.cu) read fragments straight from global memory (each m-tile warp re-read the
 // R block) and were latency bound: 23 / 45 us per launch at C2 (profiles/r1_wood_*).
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <cstdint>
 
@@ -449,7 +450,13 @@ __global__ void __launch_bounds__(kWT, 2)
   }
 }
 
-int wood_grid() { return 2 * sm_count(); }
+int wood_grid() {  // CTAs per SM: 2 (env GPK_WOOD_CPS=1 for A/B checks)
+  static int cps = [] {
+    const char* e = std::getenv("GPK_WOOD_CPS");
+    return e && std::atoi(e) == 1 ? 1 : 2;
+  }();
+  return cps * sm_count();
+}
 
 size_t wood_g1_workspace(int ka, int tb) { return static_cast<size_t>(wood_grid()) * ka * tb; }
 // prz, pzz: tb * G each
