@@ -613,6 +613,49 @@ struct gpk_ctx {
     solver = nullptr;
   }
 
+  // ---- side stream: the derivative factors dL (needed only by the backward pass) are built
+  // on st2 while the forward solve runs on st; every other API entry (guard) and the
+  // backward pass first make st wait for that work (join_dl), and the host reads the
+  // tr(P^-1 dP_w) values only when it needs them (need_trace).
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_dl = nullptr;
+  bool dl_pending = false, trace_pending = false;
+  DBuf<double> w_trace;
+  bool use_side = [] {  // env GPK_SIDE_DL=0 builds dL on the main stream (A/B checks)
+    const char* e = std::getenv("GPK_SIDE_DL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  void ensure_side() {
+    if (!st2) CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    if (!ev_fork) CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    if (!ev_dl) CK(cudaEventCreateWithFlags(&ev_dl, cudaEventDisableTiming));
+  }
+  void join_dl() {
+    if (!dl_pending) return;
+    CK(cudaStreamWaitEvent(st, ev_dl, 0));
+    dl_pending = false;
+  }
+  void need_trace() {
+    join_dl();
+    if (!trace_pending) return;
+    const int nw = d + 1;
+    std::vector<double> hv(nw);
+    CK(cudaMemcpyAsync(hv.data(), w_trace.p, sizeof(double) * nw, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int w = 0; w < nw; ++w) trace_det[w] = 2.0 * hv[w];
+    trace_pending = false;
+  }
+  void release_side() {
+    if (st2) {
+      cudaStreamSynchronize(st2);
+      cudaStreamDestroy(st2);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_dl) cudaEventDestroy(ev_dl);
+    st2 = nullptr;
+    ev_fork = ev_dl = nullptr;
+  }
+
   void set_device() { CK(cudaSetDevice(device)); }
   void sync() { CK(cudaStreamSynchronize(st)); }
   void check_launch(cudaError_t e, int count, const char* what) {
@@ -1290,11 +1333,12 @@ struct gpk_ctx {
 
 namespace {
 
-gpk_status guard(gpk_ctx* ctx, const std::function<void()>& f) {
+gpk_status guard(gpk_ctx* ctx, const std::function<void()>& f, bool defer_dl = false) {
   try {
     if (ctx) {
       ctx->set_device();
       tl_stream = ctx->st;
+      if (!defer_dl) ctx->join_dl();  // side-stream derivative factors complete before any other use
     }
     f();
     if (ctx) ctx->err.clear();
@@ -1485,6 +1529,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
 
   if (cfg->with_gradient) {
     require(res->gradient != nullptr, "evaluate_mll: null gradient buffer");
+    c->need_trace();  // the side-stream derivative factors (gpk_precond_deriv_factors) are done
     // backward probe batch (gp_likelihood.hpp:79-84)
     const double* Zb = dZ + r0;  // this rank's rows of the backward batch
     long long ldzb = ldz;
@@ -1838,6 +1883,7 @@ void gpk_destroy(gpk_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->st);
+  ctx->release_side();
   ctx->release_handles();
   for (auto& p : ctx->prof)
     for (auto& e : p.pending) {
@@ -2029,6 +2075,7 @@ gpk_status gpk_precond_identity(gpk_ctx* ctx) {
     ctx->plogdet = 0.0;
     ctx->have_dl = true;
     ctx->trace_det.assign(ctx->d + 2, 0.0);
+    ctx->trace_pending = false;  // a new preconditioner: no derivative traces pending
   });
 }
 
@@ -2118,13 +2165,13 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
       work.ensure(static_cast<size_t>(std::max(lwork, 1)));
       CS(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, k, G.p, k, work.p, lwork, info.p));
       int hinfo = 0;
-      c->d2h(&hinfo, info.p, sizeof(int));
-      if (hinfo != 0)
-        fail(GPK_NUMERICAL_ERROR, "DiagPlusLowRank: inner Cholesky failed (cannot happen for sigma^2 > 0)");
       std::vector<double> diag(k);
+      CK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
       CK(cudaMemcpy2DAsync(diag.data(), sizeof(double), G.p, (k + 1) * sizeof(double), sizeof(double), k,
                            cudaMemcpyDeviceToHost, c->st));
-      c->sync();
+      c->sync();  // one round trip for the factorisation status and the diagonal
+      if (hinfo != 0)
+        fail(GPK_NUMERICAL_ERROR, "DiagPlusLowRank: inner Cholesky failed (cannot happen for sigma^2 > 0)");
       double sl = 0.0;
       for (int a = 0; a < k; ++a) sl += std::log(diag[a]);
       ld += 2.0 * sl - static_cast<double>(k) * std::log(noise);
@@ -2135,12 +2182,13 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
       CB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, k, &one,
                      G.p, k, c->C.p, n));
       c->launches += 4;
-      c->sync();
+      // G and work are released stream-ordered; C is consumed on the same stream
     }
     c->plogdet = ld;
     c->pkind = 2;
     // trace of P^{-1} for the noise derivative: (n - sum C o L) / s2  (:138-145 with dP = I)
     c->trace_det.assign(c->d + 2, 0.0);
+    c->trace_pending = false;  // a new preconditioner: no derivative traces pending
     double cl = 0.0;
     if (k > 0) {
       const int nrb = gpk::num_chunks(n * k);
@@ -2169,6 +2217,24 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
     c->have_dl = false;
     if (k > 0) {
       c->dL.ensure(static_cast<size_t>(nw) * n * k);
+      c->w_trace.ensure(nw);
+      // the build runs on the side stream st2 (fork after L, pivots and dL's allocation on st);
+      // its scratch is allocated and released on st2
+      cudaStream_t ds = c->st;
+      if (c->use_side) {
+        c->ensure_side();
+        ds = c->st2;
+        CK(cudaEventRecord(c->ev_fork, c->st));
+        CK(cudaStreamWaitEvent(ds, c->ev_fork, 0));
+        tl_stream = ds;
+      }
+      struct StreamRestore {
+        gpk_ctx* c;
+        ~StreamRestore() {
+          tl_stream = c->st;
+          if (c->blas) cublasSetStream(c->blas, c->st);
+        }
+      } restore{c};
       DBuf<double> facs;
       facs.ensure(nw);
       std::vector<double> hf(nw);
@@ -2179,7 +2245,7 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
           hf[w] = -2.0 * c->o2 / (lj * lj * lj);
         }
       }
-      c->h2d(facs.p, hf.data(), sizeof(double) * nw);
+      CK(cudaMemcpyAsync(facs.p, hf.data(), sizeof(double) * nw, cudaMemcpyHostToDevice, ds));
       // Left-looking blocks of kB columns: the contribution of all earlier columns to a block is two
       // strided-batched GEMMs over the parameters, the recursion inside the block one kernel per column
       // (same formula as preconditioners.hpp:283-290, summation regrouped by block).
@@ -2191,22 +2257,23 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
       Lp.ensure(static_cast<size_t>(k) * kB);
       dLp.ensure(static_cast<size_t>(nw) * k * kB);
       dpiv.ensure(k);
-      c->h2d(dpiv.p, c->pivots.data(), sizeof(long long) * k);
+      CK(cudaMemcpyAsync(dpiv.p, c->pivots.data(), sizeof(long long) * k, cudaMemcpyHostToDevice, ds));
       DBuf<double> rep;
       rep.ensure(gpk::dl_replay_workspace(nw));
       c->ensure_handles();
+      CB(cublasSetStream(c->blas, ds));
       for (int s0 = 0; s0 < k; s0 += kB) {
         const int bb = std::min(kB, k - s0);
         // DC_w[:, q] = dK_w column of pivot s0+q (all pivots of the block in one launch)
         c->check_launch(gpk::launch_deriv_columns_block(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, dpiv.p + s0, bb,
                                                         nw, facs.p, c->o2, DC.p, static_cast<long long>(n) * kB,
-                                                        c->st),
+                                                        ds),
                         1, "deriv_columns_block");
         if (s0 > 0) {
           // Lp[c][q] = L[piv_q, c], dLp_w[c][q] = dL_w[piv_q, c]   (s0 x bb, column-major)
-          c->check_launch(gpk::launch_gather_pivot_rows(c->L.p, n, 0, 1, dpiv.p + s0, s0, bb, Lp.p, c->st), 1,
+          c->check_launch(gpk::launch_gather_pivot_rows(c->L.p, n, 0, 1, dpiv.p + s0, s0, bb, Lp.p, ds), 1,
                           "gather_pivot_rows");
-          c->check_launch(gpk::launch_gather_pivot_rows(c->dL.p, n, wstride, nw, dpiv.p + s0, s0, bb, dLp.p, c->st),
+          c->check_launch(gpk::launch_gather_pivot_rows(c->dL.p, n, wstride, nw, dpiv.p + s0, s0, bb, dLp.p, ds),
                           1, "gather_pivot_rows");
           const double m1 = -1.0, one = 1.0;
           // DC_w -= dL_w[:, :s0] Lp ;  DC_w -= L[:, :s0] dLp_w
@@ -2219,22 +2286,26 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
         }
         // in-block recursion: one launch per block (every CTA replays the pivot rows' recursion)
         c->check_launch(gpk::launch_dl_block(c->L.p, c->dL.p, wstride, nw, s0, bb, dpiv.p + s0, DC.p,
-                                             static_cast<long long>(n) * kB, n, rep.p, c->st),
+                                             static_cast<long long>(n) * kB, n, rep.p, ds),
                         2, "dl_block");
       }
       // tr(P^{-1} dP_w) = 2 sum(C o dL_w)  (algebraically equal to preconditioners.hpp:138-145)
+      // all nw traces on the device; the host reads them when it needs them (need_trace)
       const int nrb = gpk::num_chunks(n * k);
-      DBuf<double> part, outv;
-      part.ensure(static_cast<size_t>(nrb));
-      outv.ensure(1);
+      DBuf<double> part;
+      part.ensure(static_cast<size_t>(nrb) * nw);
       for (int w = 0; w < nw; ++w) {
         c->check_launch(gpk::launch_dot_partials(0, c->C.p, c->dL.p + static_cast<size_t>(w) * n * k, 0.0, n * k, 0, 1,
-                                                 part.p, c->st),
+                                                 part.p + static_cast<size_t>(w) * nrb, ds),
                         1, "dot");
-        c->check_launch(gpk::launch_reduce_partials(part.p, nrb, 1, outv.p, c->st), 1, "reduce");
-        double v;
-        c->d2h(&v, outv.p, sizeof(double));
-        c->trace_det[w] = 2.0 * v;
+        c->check_launch(gpk::launch_reduce_partials(part.p + static_cast<size_t>(w) * nrb, nrb, 1, c->w_trace.p + w,
+                                                    ds),
+                        1, "reduce");
+      }
+      c->trace_pending = true;
+      if (c->use_side) {
+        CK(cudaEventRecord(c->ev_dl, ds));
+        c->dl_pending = true;
       }
     }
     c->have_dl = true;
@@ -2299,6 +2370,7 @@ gpk_status gpk_precond_trace_inv_deriv(gpk_ctx* ctx, int which, double* out) {
       return;
     }
     if (which <= ctx->d && ctx->k > 0) require(ctx->have_dl, "DiagPlusLowRank: derivative factors not attached");
+    ctx->need_trace();
     *out = ctx->trace_det[which];
   });
 }
@@ -2351,7 +2423,7 @@ gpk_status gpk_mbcg(gpk_ctx* ctx, const double* B, int64_t ldb, int t, const gpk
 
 gpk_status gpk_evaluate_mll_device(gpk_ctx* ctx, const double* dy, const double* dZ, int64_t ldz, int l,
                                    uint64_t probe_seed, const gpk_mll_cfg* cfg, gpk_mll_result* res) {
-  return guard(ctx, [&] { evaluate_impl(ctx, dy, dZ, ldz, l, probe_seed, cfg, res); });
+  return guard(ctx, [&] { evaluate_impl(ctx, dy, dZ, ldz, l, probe_seed, cfg, res); }, true);
 }
 
 gpk_status gpk_evaluate_mll(gpk_ctx* ctx, const double* y, const double* Z, int64_t ldz, int l, uint64_t probe_seed,
@@ -2370,7 +2442,7 @@ gpk_status gpk_evaluate_mll(gpk_ctx* ctx, const double* y, const double* Z, int6
     CK(cudaMemcpy2DAsync(dz.p, n * sizeof(double), Z, ldz * sizeof(double), n * sizeof(double), l,
                          cudaMemcpyHostToDevice, c->st));
     evaluate_impl(c, dy.p, dz.p, n, l, probe_seed, cfg, res);
-  });
+  }, true);
 }
 
 // ---- validation / test metric and predictive mean ------------------
