@@ -645,7 +645,55 @@ struct gpk_ctx {
     for (int w = 0; w < nw; ++w) trace_det[w] = 2.0 * hv[w];
     trace_pending = false;
   }
+  // The backward pass's preconditioner terms need only the probes, L, C and dL, so with
+  // shared probes they are computed on st2 concurrently with the forward solve:
+  // out[w l + i] = t_{w,i} (w <= d, precond_trace_terms_kernel), out[(d+1) l + i] = z_i' P^-1 z_i;
+  // Zc receives the gathered probe block (allocated on st, read there after the join).
+  cudaEvent_t ev_terms = nullptr;
+  void launch_side_terms(const double* Zb, long long ldzb, int l, double* Zc, double* out) {
+    ensure_side();
+    if (!ev_terms) CK(cudaEventCreateWithFlags(&ev_terms, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev_fork, st));  // the probe block, Zc and out exist on st
+    CK(cudaStreamWaitEvent(st2, ev_fork, 0));
+    cudaStream_t s2 = st2;
+    tl_stream = s2;
+    struct Restore {
+      gpk_ctx* c;
+      ~Restore() { tl_stream = c->st; }
+    } restore{this};
+    {
+      const int nw = d + 1, kw = nw * k;
+      DBuf<double> Q, part, W, A, Bq, Bz, partw, dpart;
+      Q.ensure(static_cast<size_t>(l) * ldn);
+      part.ensure(gpk::g1_workspace(nl, k, l));
+      W.ensure(static_cast<size_t>(k) * l);
+      check_launch(gpk::launch_gather_cols(Zb, ldzb, nullptr, 1.0, nl, l, Zc, ldn, s2), 1, "gather");
+      // Q = P^-1 Zc (psolve with its own workspaces)
+      check_launch(gpk::launch_g1(L.p, n, k, Zc, ldn, l, nl, part.p, W.p, k, s2), 2, "g1");
+      check_launch(gpk::launch_woodbury_apply(C.p, n, k, W.p, k, Zc, ldn, pnoise, l, nl, Q.p, ldn, s2), 1,
+                   "woodbury");
+      const int nrb = gpk::num_chunks(nl);
+      dpart.ensure(static_cast<size_t>(l) * nrb);
+      check_launch(gpk::launch_dot_partials(0, Zc, Q.p, 0.0, nl, ldn, l, dpart.p, s2), 1, "dots");
+      check_launch(gpk::launch_reduce_partials(dpart.p, nrb, l, out + static_cast<size_t>(nw) * l, s2), 1, "reduce");
+      A.ensure(static_cast<size_t>(2) * l * k);
+      check_launch(gpk::launch_g1(L.p, n, k, Q.p, ldn, l, nl, part.p, A.p, k, s2), 2, "g1");
+      check_launch(gpk::launch_g1(L.p, n, k, Zc, ldn, l, nl, part.p, A.p + static_cast<size_t>(l) * k, k, s2), 2,
+                   "g1");
+      Bq.ensure(static_cast<size_t>(l) * kw);
+      Bz.ensure(static_cast<size_t>(l) * kw);
+      partw.ensure(gpk::g1_workspace(nl, kw, l));
+      check_launch(gpk::launch_g1(dL.p, n, kw, Q.p, ldn, l, nl, partw.p, Bq.p, kw, s2), 2, "g1");
+      check_launch(gpk::launch_g1(dL.p, n, kw, Zc, ldn, l, nl, partw.p, Bz.p, kw, s2), 2, "g1");
+      precond_trace_terms_kernel<<<static_cast<unsigned>((nw * l * 32 + 255) / 256), 256, 0, s2>>>(
+          Bq.p, Bz.p, A.p, k, kw, l, nw, out);
+      check_launch(cudaGetLastError(), 1, "precond_trace_terms");
+    }
+    CK(cudaEventRecord(ev_terms, s2));
+  }
   void release_side() {
+    if (ev_terms) cudaEventDestroy(ev_terms);
+    ev_terms = nullptr;
     if (st2) {
       cudaStreamSynchronize(st2);
       cudaStreamDestroy(st2);
@@ -1429,6 +1477,15 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   const int nl = c->nl, r0 = c->r0;  // this rank's rows of y, Z and the CG state
   c->check_launch(gpk::launch_gather_cols(dy + r0, n, nullptr, 1.0, nl, 1, B.p, ldn, c->st), 1, "gather");
   c->check_launch(gpk::launch_gather_cols(dZ + r0, ldz, nullptr, 1.0, nl, l, B.p + ldn, ldn, c->st), 1, "gather");
+  // backward preconditioner terms on the side stream, overlapped with the forward solve
+  DBuf<double> Zc, dterms;  // allocated on st: read there after the join
+  const bool side_terms = cfg->with_gradient && cfg->share_probes && cfg->backward_mode == 0 && c->use_side &&
+                          c->pkind == 2 && c->k > 0 && c->world == 1 && c->have_dl;
+  if (cfg->with_gradient) Zc.ensure(static_cast<size_t>(l) * ldn);
+  if (side_terms) {
+    dterms.ensure(static_cast<size_t>(d + 2) * l);
+    c->launch_side_terms(dZ + r0, ldz, l, Zc.p, dterms.p);
+  }
   std::vector<double> ah(static_cast<size_t>(t) * mi), bh(static_cast<size_t>(t) * mi);
   gpk_ctx::CgOut cg;
   try {
@@ -1545,15 +1602,24 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
       ldzb = ldn;
     }
     // ---- preconditioner terms: Q = P^{-1} Zb, t_{w,i} = z_i' P^{-1} dP_w z_i
-    DBuf<double> Zc, Q;
-    Zc.ensure(static_cast<size_t>(l) * ldn);
-    Q.ensure(static_cast<size_t>(l) * ldn);
-    c->check_launch(gpk::launch_gather_cols(Zb, ldzb, nullptr, 1.0, nl, l, Zc.p, ldn, c->st), 1, "gather");
-    c->psolve(Zc.p, l, Q.p);
+    DBuf<double> Q;
     std::vector<std::vector<double>> tw(np, std::vector<double>(l, 0.0));
     std::vector<double> tdet(np, 0.0);
     const bool dplr = c->pkind == 2;
-    if (dplr) {
+    if (side_terms) {  // computed on st2 during the forward solve
+      CK(cudaStreamWaitEvent(c->st, c->ev_terms, 0));
+      std::vector<double> h(static_cast<size_t>(d + 2) * l);
+      c->d2h(h.data(), dterms.p, sizeof(double) * h.size());
+      for (int w = 0; w <= d + 1; ++w) {
+        tdet[w] = c->trace_det[w];
+        for (int i = 0; i < l; ++i) tw[w][i] = h[static_cast<size_t>(w) * l + i];
+      }
+    } else {
+      Q.ensure(static_cast<size_t>(l) * ldn);
+      c->check_launch(gpk::launch_gather_cols(Zb, ldzb, nullptr, 1.0, nl, l, Zc.p, ldn, c->st), 1, "gather");
+      c->psolve(Zc.p, l, Q.p);
+    }
+    if (dplr && !side_terms) {
       tdet[d + 1] = c->trace_det[d + 1];
       const std::vector<double> zq = c->col_dots(Zc.p, Q.p, l, ldn);
       for (int i = 0; i < l; ++i) tw[d + 1][i] = zq[i];  // dP/dsigma^2 = I
