@@ -82,11 +82,10 @@ __global__ void __launch_bounds__(kDThreads, 1)
   constexpr int NA = DP + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Ss = reinterpret_cast<T*>(smem_raw);  // [l][kDA]
-  T* Zs = Ss + l * kDA;                    // [l][kDB]
-  T* Xa = Zs + l * kDB;                    // [kDA][DP]
-  T* Xb = Xa + kDA * DP;                   // [kDB][DP]
-  T* Ua = Xb + kDB * DP;                   // [kDA]
-  T* Ub = Ua + kDA;                        // [kDB]
+  T* Xa = Ss + l * kDA;                    // [kDA][DP]
+  T* Ua = Xa + kDA * DP;                   // [kDA]
+  T* Bbuf = Ua + kDA;                      // 2 x {Zs [l][kDB], Xb [kDB][DP], Ub [kDB]}: double-buffered b-tiles
+  const int bstride = l * kDB + kDB * DP + kDB;
   __shared__ double red[kDThreads / 32];
 
   const int tid = threadIdx.x;
@@ -96,6 +95,27 @@ __global__ void __launch_bounds__(kDThreads, 1)
   const int nbt = n_pad / kDB;
   const int bt0 = blockIdx.y * kDBTilesPerBlock;
   const int bt1 = min(bt0 + kDBTilesPerBlock, nbt);
+
+  // b-tile staging with 16-byte cp.async (every row segment is 16-byte aligned: n_pad % 128 == 0)
+  constexpr int V = 16 / sizeof(T);  // elements per copy
+  auto cp16 = [](T* dst, const T* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  };
+  auto stage = [&](int buf, int bt) {
+    const int b0 = bt * kDB;
+    T* zs = Bbuf + buf * bstride;
+    T* xb = zs + l * kDB;
+    T* ub = xb + kDB * DP;
+    for (int e = tid; e < l * (kDB / V); e += kDThreads) {
+      const int i = e / (kDB / V), r = (e % (kDB / V)) * V;
+      cp16(zs + i * kDB + r, Z + static_cast<long long>(i) * n_pad + b0 + r);
+    }
+    for (int e = tid; e < kDB * DP / V; e += kDThreads) cp16(xb + e * V, X + static_cast<long long>(b0) * DP + e * V);
+    for (int e = tid; e < kDB / V; e += kDThreads) cp16(ub + e * V, U + b0 + e * V);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (bt0 < bt1) stage(0, bt0);
 
   // a-tile operands (once per CTA)
   for (int e = tid; e < l * kDA; e += kDThreads) {
@@ -110,15 +130,17 @@ __global__ void __launch_bounds__(kDThreads, 1)
   for (int q = 0; q < NA; ++q) acc64[q] = 0.0;
 
   for (int bt = bt0; bt < bt1; ++bt) {
-    const int b0 = bt * kDB;
-    __syncthreads();  // previous b-tile fully consumed
-    for (int e = tid; e < l * kDB; e += kDThreads) {
-      const int i = e / kDB, r = e % kDB;
-      Zs[e] = Z[static_cast<long long>(i) * n_pad + b0 + r];
+    const int buf = (bt - bt0) & 1;
+    if (bt + 1 < bt1) {
+      stage(buf ^ 1, bt + 1);  // the other buffer was released by the previous iteration's barrier
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-    for (int e = tid; e < kDB * DP; e += kDThreads) Xb[e] = X[static_cast<long long>(b0) * DP + e];
-    for (int e = tid; e < kDB; e += kDThreads) Ub[e] = U[b0 + e];
-    __syncthreads();
+    __syncthreads();  // tile bt visible to every thread
+    const T* Zs = Bbuf + buf * bstride;
+    const T* Xb = Zs + l * kDB;
+    const T* Ub = Xb + kDB * DP;
 
     // W tile (4 x 4 per thread) = S[a, :] . Z[b, :]
     T w[4][4];
@@ -177,6 +199,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
     }
 #pragma unroll
     for (int q = 0; q < NA; ++q) acc64[q] += static_cast<double>(acc[q]);
+    __syncthreads();  // buffer buf is restaged by the next iteration
   }
 
   // fixed-order block reduction -> one partial row per CTA
@@ -191,7 +214,8 @@ template <typename T, int FAM, int DP>
 static cudaError_t launch_dc_t(const void* X, const void* U, const void* S, const void* Z, int n_pad, int l,
                                int a_begin, int a_rows, double cmix, double* partials, int* nblocks,
                                cudaStream_t st) {
-  const size_t sm = sizeof(T) * (static_cast<size_t>(l) * (kDA + kDB) + (kDA + kDB) * DP + kDA + kDB);
+  const size_t sm = sizeof(T) * (static_cast<size_t>(l) * kDA + kDA * DP + kDA +
+                                 2 * (static_cast<size_t>(l) * kDB + kDB * DP + kDB));
   auto k = deriv_contract_kernel<T, FAM, DP>;
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
