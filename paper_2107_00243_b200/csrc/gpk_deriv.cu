@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(kDThreads, 1)
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) w[r][c] = T(0);
-    for (int i = 0; i < l; ++i) {
+#pragma unroll 5
+    for (int i = 0; i < l; ++i) {  // unrolled: the shared loads of later i are in flight early
       T sa[4], zb[4];
       if constexpr (sizeof(T) == 4) {  // one 128-bit shared load per operand quad
         const float4 va = *reinterpret_cast<const float4*>(Ss + i * kDA + ta * 4);
