@@ -195,6 +195,30 @@ gpk_status gpk_cross_kernel_mvm(gpk_ctx* ctx, const double* A, int64_t na, int64
 gpk_status gpk_predict_mean(gpk_ctx* ctx, const double* y, const double* A, int64_t na, int64_t lda,
                             const gpk_cg_cfg* cfg, double* mean, int* iters);
 
+/* ---- dataset ingestion -------------------------------
+ * gpk_load_csv replaces load_csv (dataset.hpp:155-242) over read_csv_table
+ * (csv.hpp:91-116): header row required, rows shuffled with mt19937_64(seed) +
+ * uniform_int_distribution, split train / validation / test by llround(fraction * n),
+ * optional standardisation with training-split population statistics.  Host code (no
+ * device needed).  Errors: GPK_INPUT_ERROR with the reference's input_error text in err
+ * (errlen bytes, nullable).  Splits are stored column-major fp64, as gpk_set_data takes. */
+typedef struct gpk_dataset gpk_dataset;
+typedef enum { GPK_SPLIT_TRAIN = 0, GPK_SPLIT_VALIDATION = 1, GPK_SPLIT_TEST = 2 } gpk_split;
+gpk_status gpk_load_csv(const char* path, const char* target_column, int standardize, double train_fraction,
+                        double validation_fraction, double test_fraction, uint64_t seed, gpk_dataset** out,
+                        char* err, int64_t errlen);
+void gpk_dataset_free(gpk_dataset* ds);
+gpk_status gpk_dataset_shape(const gpk_dataset* ds, int split, int64_t* n, int* d);
+/* X: n x d column-major (ld ldx >= n), y: n; either nullable */
+gpk_status gpk_dataset_copy(const gpk_dataset* ds, int split, double* X, int64_t ldx, double* y);
+/* Standardizer (dataset.hpp:87-101) statistics; identity (0 / 1) when not standardised */
+gpk_status gpk_dataset_stats(const gpk_dataset* ds, int* standardized, double* feature_mean, double* feature_std,
+                             double* target_mean, double* target_std);
+/* column < 0: the target name; 0..d-1: feature names in file order (DataSplits::feature_names) */
+const char* gpk_dataset_column_name(const gpk_dataset* ds, int column);
+/* Standardizer::invert_x / invert_y in place (no-op when not standardised); X or y nullable */
+gpk_status gpk_dataset_invert(const gpk_dataset* ds, double* X, int64_t n, int64_t ldx, double* y);
+
 /* optimizer.hpp:22-43 OptMethod / OptOptions */
 typedef enum { GPK_OPT_LBFGS = 0, GPK_OPT_ADAM = 1 } gpk_opt_method;
 typedef struct {

@@ -286,6 +286,61 @@ inline std::vector<double> predict_mean(const KernelOperator& k, const std::vect
   return mean;
 }
 
+struct Dataset {  // dataset.hpp:18-26 (x: n x d column-major)
+  std::vector<double> x, y;
+  std::int64_t n = 0;
+  int d = 0;
+  std::int64_t size() const { return n; }
+  int dim() const { return d; }
+};
+
+struct Standardizer {  // dataset.hpp:87-101
+  std::vector<double> feature_mean, feature_std;
+  double target_mean = 0.0, target_std = 1.0;
+};
+
+struct DataSplits {  // dataset.hpp:103-109
+  Dataset train, validation, test;
+  Standardizer stats;
+  bool standardized = false;
+  std::vector<std::string> feature_names;
+  std::string target_name;
+};
+
+struct SplitFractions {  // dataset.hpp:111-113
+  double train = 0.64, validation = 0.16, test = 0.20;
+};
+
+// load_csv (dataset.hpp:155-242) over gpk_load_csv; throws input_error with the reference's text
+inline DataSplits load_csv(const std::string& path, const std::string& target_column, bool standardize,
+                           const SplitFractions& split, std::uint64_t seed) {
+  gpk_dataset* h = nullptr;
+  char err[1024];
+  if (gpk_load_csv(path.c_str(), target_column.c_str(), standardize ? 1 : 0, split.train, split.validation,
+                   split.test, seed, &h, err, sizeof(err)) != GPK_OK)
+    throw input_error(err);
+  std::unique_ptr<gpk_dataset, void (*)(gpk_dataset*)> guard(h, gpk_dataset_free);
+  DataSplits out;
+  Dataset* parts[3] = {&out.train, &out.validation, &out.test};
+  for (int s = 0; s < 3; ++s) {
+    Dataset& p = *parts[s];
+    gpk_dataset_shape(h, s, &p.n, &p.d);
+    p.x.resize(static_cast<size_t>(p.n) * p.d);
+    p.y.resize(static_cast<size_t>(p.n));
+    gpk_dataset_copy(h, s, p.x.data(), p.n > 0 ? p.n : 1, p.y.data());
+  }
+  const int d = out.train.d;
+  int st = 0;
+  out.stats.feature_mean.resize(d);
+  out.stats.feature_std.resize(d);
+  gpk_dataset_stats(h, &st, out.stats.feature_mean.data(), out.stats.feature_std.data(), &out.stats.target_mean,
+                    &out.stats.target_std);
+  out.standardized = st != 0;
+  for (int j = 0; j < d; ++j) out.feature_names.emplace_back(gpk_dataset_column_name(h, j));
+  out.target_name = gpk_dataset_column_name(h, -1);
+  return out;
+}
+
 struct OptOptions {  // optimizer.hpp:24-43
   gpk_opt_method method = GPK_OPT_LBFGS;
   int max_steps = 20, lbfgs_memory = 10;

@@ -12,7 +12,7 @@ from .gpkrylov import (  # noqa: F401
     pivoted_cholesky, pivoted_cholesky_deriv_factors, pivoted_cholesky_with_derivatives,
 )
 from .gpkrylov import (  # noqa: F401  SURVEY §8(f): the callers of the hot path
-    Dataset, ExactMll, IdentityBuilder, OptimizeResult, OptOptions, PivotedCholeskyBuilder, count_model_evaluations,
+    DataSplits, Dataset, ExactMll, SplitFractions, Standardizer, load_csv, IdentityBuilder, OptimizeResult, OptOptions, PivotedCholeskyBuilder, count_model_evaluations,
     cross_kernel_mvm, mll_exact, optimize, predict_mean, run_training_arm,
 )
 

@@ -114,6 +114,14 @@ SIGNATURES = {
     "gpk_mll_exact": (C.c_int, [_V, _D, _D, _D]),
     "gpk_cross_kernel_mvm": (C.c_int, [_V, _D, C.c_int64, C.c_int64, _D, _D]),
     "gpk_predict_mean": (C.c_int, [_V, _D, _D, C.c_int64, C.c_int64, C.POINTER(gpk_cg_cfg), _D, _I]),
+    "gpk_load_csv": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                               C.POINTER(_V), C.c_char_p, C.c_int64]),
+    "gpk_dataset_free": (None, [_V]),
+    "gpk_dataset_shape": (C.c_int, [_V, C.c_int, _L, _I]),
+    "gpk_dataset_copy": (C.c_int, [_V, C.c_int, _D, C.c_int64, _D]),
+    "gpk_dataset_stats": (C.c_int, [_V, _I, _D, _D, _D, _D]),
+    "gpk_dataset_column_name": (C.c_char_p, [_V, C.c_int]),
+    "gpk_dataset_invert": (C.c_int, [_V, _D, C.c_int64, C.c_int64, _D]),
     "gpk_optimize": (C.c_int, [_V, _D, _V, _D, C.c_int, C.c_int, _D, C.c_int, C.c_double, C.c_int,
                                C.POINTER(gpk_opt_options), C.POINTER(gpk_mll_cfg), C.c_uint64, C.c_int64,
                                C.POINTER(gpk_opt_result)]),

@@ -720,6 +720,84 @@ class Dataset:
 
 
 @dataclass
+class Standardizer:
+    """dataset.hpp:87-101: training-split column statistics; exactly invertible transforms."""
+    feature_mean: np.ndarray
+    feature_std: np.ndarray
+    target_mean: float = 0.0
+    target_std: float = 1.0
+
+    def transform_x(self, x):
+        return (np.asarray(x, dtype=np.float64) - self.feature_mean) / self.feature_std
+
+    def transform_y(self, y):
+        return (np.asarray(y, dtype=np.float64) - self.target_mean) / self.target_std
+
+    def invert_x(self, x):
+        return np.asarray(x, dtype=np.float64) * self.feature_std + self.feature_mean
+
+    def invert_y(self, y):
+        return np.asarray(y, dtype=np.float64) * self.target_std + self.target_mean
+
+
+@dataclass
+class SplitFractions:
+    """dataset.hpp:111-113"""
+    train: float = 0.64
+    validation: float = 0.16
+    test: float = 0.20
+
+
+@dataclass
+class DataSplits:
+    """dataset.hpp:103-109"""
+    train: Dataset
+    validation: Dataset
+    test: Dataset
+    stats: Standardizer
+    standardized: bool
+    feature_names: list
+    target_name: str
+
+
+def load_csv(path: str, target_column: str, standardize: bool = True, split: SplitFractions = SplitFractions(),
+             seed: int = 0) -> DataSplits:
+    """load_csv (dataset.hpp:155-242) through gpk_load_csv: header row, mt19937_64 shuffle,
+    llround split, training-split standardisation.  Raises InputError with the reference's
+    messages (non-numeric cell with row/column, constant column naming the column, ...)."""
+    lib = capi.lib()
+    h = C.c_void_p()
+    err = C.create_string_buffer(1024)
+    rc = lib.gpk_load_csv(str(path).encode(), str(target_column).encode(), int(bool(standardize)),
+                          float(split.train), float(split.validation), float(split.test),
+                          int(seed) & 0xFFFFFFFFFFFFFFFF, C.byref(h), err, len(err))
+    if rc != capi.GPK_OK:
+        raise _ERRS.get(rc, GpkError)(err.value.decode())
+    try:
+        parts = []
+        d = C.c_int()
+        for s in (0, 1, 2):
+            n = C.c_int64()
+            lib.gpk_dataset_shape(h, s, C.byref(n), C.byref(d))
+            x = np.zeros((n.value, d.value), dtype=np.float64, order="F")
+            y = np.zeros(n.value, dtype=np.float64)
+            if n.value:
+                lib.gpk_dataset_copy(h, s, _ptr(x), max(1, n.value), _ptr(y))
+            parts.append(Dataset(x, y))
+        st = C.c_int()
+        fm = np.zeros(d.value)
+        fs = np.ones(d.value)
+        tm, ts = C.c_double(), C.c_double()
+        lib.gpk_dataset_stats(h, C.byref(st), _ptr(fm), _ptr(fs), C.byref(tm), C.byref(ts))
+        names = [lib.gpk_dataset_column_name(h, j).decode() for j in range(d.value)]
+        target = lib.gpk_dataset_column_name(h, -1).decode()
+        return DataSplits(parts[0], parts[1], parts[2], Standardizer(fm, fs, tm.value, ts.value), bool(st.value),
+                          names, target)
+    finally:
+        lib.gpk_dataset_free(h)
+
+
+@dataclass
 class OptOptions:
     """optimizer.hpp:24-43"""
     method: str = "lbfgs"  # "lbfgs" | "adam"

@@ -49,3 +49,32 @@ def test_facade_cpp_caller_matches_oracle(tmp_path, orc):
                        seed=17, method=1, max_steps=3)
     assert got["opt_evals"] == len(opt["evaluations"])
     np.testing.assert_allclose(got["opt_best"], opt["best"], rtol=1e-6, atol=1e-7)
+
+
+def test_facade_load_csv_matches_oracle(tmp_path):
+    """gpkrylov::cuda::load_csv from a compiled C++ caller (host only) against oracle/dataset.py."""
+    from oracle import dataset as od
+
+    exe = str(tmp_path / "load_csv_test")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "load_csv_test.cpp"), "-o", exe, "-L" + LIBDIR,
+                    "-lgpkrylov_cuda", "-Wl,-rpath," + LIBDIR], check=True)
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(150, 4))
+    path = tmp_path / "t.csv"
+    path.write_text("u,v,target,w\n" + "\n".join(",".join(repr(float(v)) for v in r) for r in x) + "\n")
+    got = json.loads(subprocess.run([exe, str(path), "target", "1", "99"], check=True, capture_output=True,
+                                    text=True).stdout)
+    want = od.load_csv(str(path), "target", standardize=True, seed=99)
+    assert got["names"] == ["u", "v", "w"] and got["target"] == "target" and got["standardized"]
+    for name in ("train", "validation", "test"):
+        wx, wy = want[name]
+        g = got[name]
+        assert g["n"] == len(wy)
+        np.testing.assert_allclose(np.array(g["x"]).reshape(3, -1).T, wx, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(g["y"], wy, rtol=1e-12, atol=1e-12)
+    bad = tmp_path / "b.csv"
+    bad.write_text("a,target\n1,2\n3,zz\n")
+    r = subprocess.run([exe, str(bad), "target", "1", "1"], capture_output=True, text=True)
+    assert r.returncode == 1
+    assert "non-numeric cell 'zz' at data row 2, column 2" in r.stdout
