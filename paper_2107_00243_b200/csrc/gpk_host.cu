@@ -512,6 +512,15 @@ struct gpk_ctx {
     const int v = e ? std::atoi(e) : 1;
     return v >= 1 && v <= 64 ? v : 1;
   }();
+  // persistent Gram/direct tcgen05 MVM (env GPK_TCG_PERSIST=0: one CTA per (row block, split) unit)
+  int tcg_ctas = [] {
+    const char* e = std::getenv("GPK_TCG_PERSIST");
+    if (e && std::atoi(e) == 0) return 0;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return 0;
+    return sms;
+  }();
   int tc_flush = [] {   // j-tiles per TMEM accumulation group (env GPK_TC_FLUSH, default 2)
     const char* e = std::getenv("GPK_TC_FLUSH");
     const int v = e ? std::atoi(e) : 2;
@@ -799,11 +808,21 @@ struct gpk_ctx {
     const int nt64 = n_pad / 64;
     int best = 1;
     double best_cost = 1e300;
+    const double sms = tcg_ctas > 0 ? tcg_ctas : 148.0;
     for (int s = 1; s <= std::min(32, nt64); ++s) {
       const int per = (nt64 + s - 1) / s;
       const int se = (nt64 + per - 1) / per;
-      const double waves = std::ceil(static_cast<double>(rb) * se / 148.0);
-      const double cost = waves * (per + 8.0) + (se > 1 ? 0.02 * se * rb / 148.0 * per : 0.0);
+      double cost;
+      if (tcg_ctas > 0) {
+        // persistent grid: the busiest CTA runs ceil(U / SMs) units of `per` tiles (+ ~1 tile of
+        // unpipelined drain per unit), one start-up (~8 tiles), a row change (~4) and the split
+        // reduction (fp64 partials, ~0.15 tile-times per split)
+        const double units = std::ceil(static_cast<double>(rb) * se / sms);
+        cost = units * (per + 1.0) + 8.0 + (se > 1 ? 4.0 + 0.15 * se : 0.0);
+      } else {
+        const double waves = std::ceil(static_cast<double>(rb) * se / 148.0);
+        cost = waves * (per + 8.0) + (se > 1 ? 0.02 * se * rb / 148.0 * per : 0.0);
+      }
       if (cost < best_cost - 1e-9) {
         best_cost = cost;
         best = se;
@@ -864,6 +883,7 @@ struct gpk_ctx {
           const int per64 = (nt64 + sg - 1) / sg;
           sp = (nt64 + per64 - 1) / per64;
           a.jtiles_per_split = per64;
+          a.ctas = tcg_ctas;
           a.flush = tc_flush;  // 64-wide tiles: 128 entries per fp32 TMEM accumulation at the default 2
         } else {
           const int npad = gpk::tc_npad(tc);

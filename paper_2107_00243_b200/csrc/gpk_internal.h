@@ -21,6 +21,7 @@ struct MvmArgs {
   int row_begin;             // first output row of this rank's shard (multiple of 128)
   int row_end;               // one past the last output row; outputs are stored at row - row_begin
   int dp;                    // padded coordinate count of the packed fp32 rows (Gram guard path)
+  int ctas;                  // tcg MVM: persistent grid size (0: one CTA per (row block, split) unit)
 };
 
 // Packed-operand geometry for a given column count.

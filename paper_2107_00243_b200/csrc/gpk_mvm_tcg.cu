@@ -143,7 +143,8 @@ cudaError_t launch_fused_kmvm_tcg(int family, int d, int direct_dp, const float*
   const int npad = tcg_npad(a.t);
   if (npad < 0 || d < 1 || d > 32) return cudaErrorInvalidValue;
   const int ks = (d + 7) / 8;
-  dim3 g((a.row_end - a.row_begin + tcg::BM - 1) / tcg::BM, splits);
+  const int units = (a.row_end - a.row_begin + tcg::BM - 1) / tcg::BM * splits;
+  dim3 g(a.ctas > 0 ? std::min(units, a.ctas) : units);  // persistent grid, or one CTA per unit
   const int nc8 = npad / 8;
   const __half* h = static_cast<const __half*>(vhi);
   const __half* l = static_cast<const __half*>(vlo);

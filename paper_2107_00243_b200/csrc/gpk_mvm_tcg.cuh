@@ -160,10 +160,24 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int row0 = a.row_begin + blockIdx.x * BM;
-  const int jt0 = blockIdx.y * a.jtiles_per_split;
-  const int jt1 = min(jt0 + a.jtiles_per_split, a.n_pad / BK);
-  const int nt = jt1 - jt0;
+  // Work units: (row block, split) pairs u = rb * S + sp, the split a FIXED j-tile range (a
+  // function of the global n), each unit's partial stored in its own split slot -- so the
+  // sums never depend on which CTA runs a unit or on the shard.  CTA b runs the contiguous
+  // units [b U / G, (b+1) U / G) of a persistent grid of G CTAs (G = U: one unit per CTA); a
+  // row-block change inside a CTA is one CTA-wide barrier (the row tiles in TMEM / shared
+  // memory are replaced only after every role has finished the previous row).
+  const int ntiles = a.n_pad / BK;
+  const int per = a.jtiles_per_split;
+  const int S = (ntiles + per - 1) / per;
+  const int nrb = (a.row_end - a.row_begin + BM - 1) / BM;
+  const long long U = static_cast<long long>(nrb) * S;
+  const int u0 = static_cast<int>(blockIdx.x * U / gridDim.x);
+  const int u1 = static_cast<int>((blockIdx.x + 1) * U / gridDim.x);
+  auto u_rb = [&](int u) { return u / S; };
+  auto u_jt0 = [&](int u) { return (u - (u / S) * S) * per; };
+  auto u_nt = [&](int u) { return min(u_jt0(u) + per, ntiles) - u_jt0(u); };
+  auto u_newrow = [&](int u) { return u == u0 || u_rb(u) != u_rb(u - 1); };
+  auto row_barrier = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(THREADS) : "memory"); };
   const int F = a.flush > 0 ? a.flush : 1;
   if (threadIdx.x == 0) GPK_TRACE(0, 0);
 
@@ -200,16 +214,23 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer (converged warp, elected lane) ----------------
     const uint32_t xjb = static_cast<uint32_t>(BK * a.dp * 4);
-    if (nt > 0 && elect_one()) {
-      mbar_arrive_expect_tx(xi_full, BM * a.dp * 4);
-      bulk_g2s(sbase + (sXI - base), X32 + static_cast<long long>(row0) * a.dp, BM * a.dp * 4, xi_full);
+    unsigned it = 0;  // unsigned: stage / phase arithmetic without sign fix-ups
+    for (int u = u0; u < u1; ++u) {
+    const int jt0 = u_jt0(u), nt = u_nt(u);
+    if (u_newrow(u)) {
+      if (u != u0) row_barrier();
+      const int row0 = a.row_begin + u_rb(u) * BM;
+      if (elect_one()) {
+        mbar_arrive_expect_tx(xi_full, BM * a.dp * 4);
+        bulk_g2s(sbase + (sXI - base), X32 + static_cast<long long>(row0) * a.dp, BM * a.dp * 4, xi_full);
+      }
+      __syncwarp();
     }
-    __syncwarp();
-    for (int it = 0; it < nt; ++it) {
+    for (int lt = 0; lt < nt; ++lt, ++it) {
       const int s = it % SG;
       mbar_wait_sleep(&xv_empty[s], ((it / SG) & 1) ^ 1);
       if (elect_one()) {
-        const long long jt = jt0 + it;
+        const long long jt = jt0 + lt;
         if constexpr (DIRECT) {
           mbar_arrive_expect_tx(&xv_full[s], 2 * VTILE + xjb);
           bulk_g2s(sbase + (sXJ - base) + s * XJ_TILE, X32 + jt * BK * a.dp, xjb, &xv_full[s]);
@@ -225,13 +246,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
     }
+    }
   } else if (warp == 1) {
     // ---------------- MMA issuer (converged warp, elected lane) ----------------
-    if (nt > 0) {
+    {
       constexpr uint32_t idesc_v = idesc_f16(NPAD);
       constexpr uint32_t idesc_g = tc::idesc_tf32(BK);
-      if constexpr (!DIRECT) mbar_wait_sleep(ax_ready, 0);
-      auto gram = [&](int k) {
+      auto gram = [&](unsigned k) {
         if constexpr (DIRECT) return;
         const int s = k % SG, gb = k & 1;
         mbar_wait_sleep(&xv_full[s], (k / SG) & 1);
@@ -254,12 +275,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         if (lane == 0) GPK_TRACE(7, k);
       };
-      gram(0);
-      for (int it = 0; it < nt; ++it) {
-        if (it + 1 < nt) gram(it + 1);  // the next Gram tile overlaps this tile's kernel-shape evaluation
+      unsigned it = 0, gc = 0, rl = 0;
+      for (int u = u0; u < u1; ++u) {
+      const int nt = u_nt(u);
+      if (u_newrow(u)) {
+        if (u != u0) row_barrier();
+        if constexpr (!DIRECT) mbar_wait_sleep(ax_ready, rl & 1);
+        ++rl;
+        gram(it);
+      }
+      const bool next_same_row = u + 1 < u1 && !u_newrow(u + 1);
+      for (int lt = 0; lt < nt; ++lt, ++it) {
+        // the next Gram tile overlaps this tile's kernel-shape evaluation (not across a row change)
+        if (lt + 1 < nt || next_same_row) gram(it + 1);
         const int s = it % SG, as = it % AS;
-        const int g = it / F, buf = g & 1;
-        if (it % F == 0) mbar_wait_sleep(&acc_empty[buf], ((g >> 1) & 1) ^ 1);
+        const int buf = gc & 1;
+        if (lt % F == 0) mbar_wait_sleep(&acc_empty[buf], ((gc >> 1) & 1) ^ 1);
         mbar_wait_sleep(&a_full[as], (it / AS) & 1);
         if (lane == 0) GPK_TRACE(3, it);
         tc::tc_fence_after();
@@ -271,17 +302,19 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int ks = 0; ks < BK / 16; ++ks) {
             const uint32_t koff = ks * 32;  // 16 fp16 along K
             const uint64_t dbh = tc::smem_desc_sw128(bhi + koff), dbl = tc::smem_desc_sw128(blo + koff);
-            const uint32_t acc = (it % F != 0 || ks > 0) ? 1u : 0u;
+            const uint32_t acc = (lt % F != 0 || ks > 0) ? 1u : 0u;
             mma_ts_f16(d_tmem, tah + ks * 8, dbh, idesc_v, acc);
             mma_ts_f16(d_tmem, tah + ks * 8, dbl, idesc_v, 1u);
             mma_ts_f16(d_tmem, tal + ks * 8, dbh, idesc_v, 1u);
           }
           tc::tc_commit(&a_empty[as]);
           tc::tc_commit(&xv_empty[s]);  // also covers the Gram MMA of this stage and the producers' norm reads
-          if (it % F == F - 1 || it == nt - 1) tc::tc_commit(&acc_full[buf]);
+          if (lt % F == F - 1 || lt == nt - 1) tc::tc_commit(&acc_full[buf]);
         }
         __syncwarp();
+        if (lt % F == F - 1 || lt == nt - 1) ++gc;
         if (lane == 0) GPK_TRACE(6, it);
+      }
       }
     }
   } else {
@@ -290,10 +323,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int lg = warp & 3;   // TMEM lane group
     const int q = pw >> 2;     // 16-column slice of the j-tile, and column-chunk subset of the drain
     const int r = lg * 32 + lane;
-    const int row = row0 + r;
-    const float ni = DIRECT ? 0.0f : Xn[row];
-    const float2 ni2 = make_float2(ni, ni);
     const uint32_t tlane = static_cast<uint32_t>(lg * 32) << 16;
+    double acc64[HC * 8];
+#pragma unroll
+    for (int e = 0; e < HC * 8; ++e) acc64[e] = 0.0;
+    float xi[DIRECT ? DPD : 1];
+    unsigned it = 0, gce = 0, rl = 0;
+    int row = 0;
+    float ni = 0.0f;
+    for (int u = u0; u < u1; ++u) {
+    const int jt0 = u_jt0(u), nt = u_nt(u);
+    if (u_newrow(u)) {
+    if (u != u0) row_barrier();
+    row = a.row_begin + u_rb(u) * BM + r;
+    ni = DIRECT ? 0.0f : Xn[row];
     if constexpr (!DIRECT) {  // this row's centred coordinates (tf32 hi / lo, columns q*8 .. q*8+7) -> A_x in TMEM
       const long long rb = static_cast<long long>(row >> 3) * 256 + (row & 7) * 32;
       uint32_t h8[8], l8[8];
@@ -311,11 +354,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ax_ready);
     }
-    double acc64[HC * 8];
-#pragma unroll
-    for (int e = 0; e < HC * 8; ++e) acc64[e] = 0.0;
-    if (nt > 0) mbar_wait_sleep(xi_full, 0);  // the CTA's fp32 rows (guard path / direct mode)
-    float xi[DIRECT ? DPD : 1];
+    mbar_wait_sleep(xi_full, rl & 1);  // the CTA's fp32 rows (guard path / direct mode)
+    ++rl;
     if constexpr (DIRECT) {
 #pragma unroll
       for (int k4 = 0; k4 < DPD / 4; ++k4) {
@@ -326,7 +366,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         xi[4 * k4 + 3] = v.w;
       }
     }
-    auto drain = [&](int g) {
+    }  // new row block
+    const float2 ni2 = make_float2(ni, ni);
+    auto drain = [&](unsigned g) {
       const int buf = g & 1;
       mbar_wait_sleep(&acc_full[buf], (g >> 1) & 1);
       tc::tc_fence_after();
@@ -345,9 +387,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&acc_empty[buf]);
     };
-    for (int it = 0; it < nt; ++it) {
+    for (int lt = 0; lt < nt; ++lt, ++it) {
       const int s = it % SG, as = it % AS, gb = it & 1;
-      const int jb = (jt0 + it) * BK + q * JPT;  // global index of this thread's first column
       if (threadIdx.x == 64) GPK_TRACE(1, it);
       if constexpr (!DIRECT) mbar_wait_sleep(&g_full[gb], (it >> 1) & 1);
       if (threadIdx.x == 64) GPK_TRACE(2, it);
@@ -461,12 +502,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&a_full[as]);
       if (lane == 0 && it < 64) GPK_TRACE(4, it * 16 + pw);
-      if (it % F == 0 && it > 0) drain(it / F - 1);
+      if (lt % F == 0 && lt > 0) drain(gce++);
     }
-    if (nt > 0) drain((nt - 1) / F);
+    drain(gce++);
     if (threadIdx.x == 64) GPK_TRACE(0, 2);
     if (row < a.row_end) {
-      double* o = out + static_cast<long long>(blockIdx.y) * a.split_stride;
+      double* o = out + static_cast<long long>(u - u_rb(u) * S) * a.split_stride;
 #pragma unroll
       for (int h = 0; h < HC; ++h) {
         const int c8 = q + h * RPT;
@@ -478,6 +519,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+#pragma unroll
+    for (int e = 0; e < HC * 8; ++e) acc64[e] = 0.0;
+    (void)jt0;
+    }  // units
   }
   tc::tc_fence_before();
   __syncthreads();
