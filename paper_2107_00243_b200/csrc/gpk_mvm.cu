@@ -81,10 +81,37 @@ __global__ void reduce_splits_kernel(const double* __restrict__ part, int splits
   out[c * ldo + i] = s;
 }
 
+// Same sums, two rows per thread with 16-byte loads of the (L2-resident) partials: the
+// partial leading dimension and split stride are even, so (c, 2i) is 16-byte aligned.
+__global__ void reduce_splits2_kernel(const double* __restrict__ part, int splits, long long sstride, int t, int n,
+                                      long long ldp, double* __restrict__ out, long long ldo) {
+  const int n2 = (n + 1) >> 1;
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<long long>(t) * n2) return;
+  const int c = static_cast<int>(idx / n2);
+  const int i = 2 * static_cast<int>(idx % n2);
+  double s0 = 0.0, s1 = 0.0;
+  const double* p = part + c * ldp + i;
+#pragma unroll 4
+  for (int k = 0; k < splits; ++k) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(p + k * sstride));
+    s0 += v.x;
+    s1 += v.y;
+  }
+  out[c * ldo + i] = s0;
+  if (i + 1 < n) out[c * ldo + i + 1] = s1;
+}
+
 cudaError_t launch_reduce_splits(const double* part, int splits, long long sstride, int t, int n, long long ldpart,
                                  double* out, long long ldo, cudaStream_t st) {
-  const long long total = static_cast<long long>(t) * n;
   const int thr = 256;
+  if ((ldpart & 1) == 0 && (sstride & 1) == 0 && (reinterpret_cast<uintptr_t>(part) & 15) == 0 && ldpart >= n + (n & 1)) {
+    const long long total2 = static_cast<long long>(t) * ((n + 1) >> 1);
+    reduce_splits2_kernel<<<static_cast<unsigned>((total2 + thr - 1) / thr), thr, 0, st>>>(part, splits, sstride, t,
+                                                                                         n, ldpart, out, ldo);
+    return cudaGetLastError();
+  }
+  const long long total = static_cast<long long>(t) * n;
   reduce_splits_kernel<<<static_cast<unsigned>((total + thr - 1) / thr), thr, 0, st>>>(part, splits, sstride, t, n,
                                                                                        ldpart, out, ldo);
   return cudaGetLastError();
