@@ -62,6 +62,8 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
 
     def __enter__(self):
+        if self.device < 0:  # not the sampling rank
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
@@ -102,12 +104,92 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def run_ours(args, rank_env):
+class SingleComm:
+    """N = 1: one process, one GPU."""
+    rank, world, device = 0, 1, 0
+
+    def create_ctx(self, lib, ctx):
+        assert lib.gpk_create(self.device, C.byref(ctx)) == 0, "gpk_create failed"
+
+    def barrier(self):
+        pass
+
+    def max(self, vals):
+        return list(vals)
+
+
+class DistComm:
+    """One process per GPU (torchrun / the self-spawn below): the library's own NCCL
+    communicator for the row-sharded evaluation, torch.distributed for barrier / max."""
+
+    def __init__(self, rank, world, local):
+        self.rank, self.world, self.device = rank, world, local
+
+    def create_ctx(self, lib, ctx):
+        import torch.distributed as dist
+
+        uid = [None]
+        if self.rank == 0:
+            buf = C.create_string_buffer(128)
+            assert lib.gpk_nccl_unique_id(buf) == 0
+            uid[0] = buf.raw
+        dist.broadcast_object_list(uid, src=0)
+        ub = C.create_string_buffer(uid[0], 128)
+        rc = lib.gpk_create_sharded(self.device, self.rank, self.world, ub, C.byref(ctx))
+        assert rc == 0, f"gpk_create_sharded failed ({rc})"
+
+    def barrier(self):
+        import torch.distributed as dist
+
+        dist.barrier()
+
+    def max(self, vals):
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor(list(vals), dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+
+class GroupComm:
+    """TEST-ONLY (--comm group): the N ranks as host threads of one process on one GPU, the
+    library's host-staged rank group (gpk_create_in_group) as the transport.  Exercises the
+    same spawn / sharding / rank-ordered reduction / max-over-ranks logic as the NCCL path;
+    its timings mean nothing (N ranks share one GPU)."""
+
+    class Shared:
+        def __init__(self, world, lib):
+            g = C.c_void_p()
+            assert lib.gpk_group_create(world, C.byref(g)) == 0
+            self.g, self.world = g, world
+            self.bar = threading.Barrier(world)
+            self.slots = [None] * world
+
+    def __init__(self, shared, rank):
+        self.sh, self.rank, self.world, self.device = shared, rank, shared.world, 0
+
+    def create_ctx(self, lib, ctx):
+        rc = lib.gpk_create_in_group(0, self.sh.g, self.rank, C.byref(ctx))
+        assert rc == 0, f"gpk_create_in_group failed ({rc})"
+
+    def barrier(self):
+        self.sh.bar.wait()
+
+    def max(self, vals):
+        self.sh.slots[self.rank] = list(vals)
+        self.sh.bar.wait()
+        out = [max(s[i] for s in self.sh.slots) for i in range(len(vals))]
+        self.sh.bar.wait()
+        return out
+
+
+def run_ours(args, comm):
     import torch
 
     from paper_2107_00243_b200 import capi
 
-    rank, world, local = rank_env
+    rank, world, local = comm.rank, comm.world, comm.device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = capi.lib()
@@ -131,24 +213,13 @@ def run_ours(args, rank_env):
 
     ctx = C.c_void_p()
     if world > 1 and args.mode == "sharded":
-        # one evaluation row-sharded over all ranks: NCCL communicator inside the library
-        import torch.distributed as dist
-
-        uid = [None]
-        if rank == 0:
-            buf = C.create_string_buffer(128)
-            assert lib.gpk_nccl_unique_id(buf) == 0
-            uid[0] = buf.raw
-        dist.broadcast_object_list(uid, src=0)
-        ub = C.create_string_buffer(uid[0], 128)
-        rc = lib.gpk_create_sharded(local, rank, world, ub, C.byref(ctx))
-        assert rc == 0, f"gpk_create_sharded failed ({rc})"
+        comm.create_ctx(lib, ctx)  # one evaluation row-sharded over all ranks
     else:
         assert lib.gpk_create(local, C.byref(ctx)) == 0, "gpk_create failed"
     stream = torch.cuda.ExternalStream(lib.gpk_stream(ctx), device=dev)
     prec = {"fp64": capi.GPK_PREC_FP64, "fp32": capi.GPK_PREC_FP32, "tf32x3": capi.GPK_PREC_TF32X3}[args.precision]
     cfg = capi.gpk_mll_cfg(capi.gpk_cg_cfg(w.max_iters, w.rel_tol, 0, prec, args.refine), 1, 1,
-                           0 if args.backward == "fused" else 1)
+                           {"fused": 0, "faithful": 1, "auto": 2}[args.backward])
     grad = np.zeros(d + 2)
     fg = np.zeros(l)
     fi = np.zeros(l, dtype=np.int32)
@@ -185,8 +256,7 @@ def run_ours(args, rank_env):
         for _ in range(warmup):
             fn(rank_k)
         torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
+        comm.barrier()
         times = []
         l0 = lib.gpk_launch_count(ctx)
         check(lib.gpk_profile_reset(ctx))
@@ -200,12 +270,13 @@ def run_ours(args, rank_env):
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         torch.cuda.synchronize()
+        comm.barrier()
         launches = (lib.gpk_launch_count(ctx) - l0) // steps
         return times, launches
 
     # ---- headline: device-resident value, with live per-launch kernel timing
     check(lib.gpk_profile_enable(ctx, 0 if os.environ.get("GPK_BENCH_NOPROF") else 1))
-    with ClockSampler(local) as clk:
+    with ClockSampler(local if rank == 0 else -1) as clk:
         times, launches = timed(step_device, args.steps, args.warmup, w.rank)
     ms = C.c_double()
     cnt = C.c_longlong()
@@ -230,8 +301,11 @@ def run_ours(args, rank_env):
     telemetry = {"value": res.value, "gradient": grad.tolist(), "logdet": res.logdet,
                  "solve_iterations": res.solve_iterations, "total_cg_iterations": res.total_cg_iterations,
                  "forward_cg_iterations_mean": float(np.mean(fi)), "refine_passes": res.refine_passes,
-                 "max_true_rel_residual": res.max_true_rel_residual, "seconds_solve": res.seconds_solve,
-                 "seconds_backward": res.seconds_backward}
+                 "max_true_rel_residual": res.max_true_rel_residual,
+                 "max_cg_rel_residual": res.max_cg_rel_residual, "unconverged_columns": res.unconverged_columns,
+                 "seconds_solve": res.seconds_solve,
+                 "seconds_backward": res.seconds_backward,
+                 "backward_mode_used": ("fused", "faithful")[res.backward_mode_used]}
     # ---- e2e through the host C-ABI
     e2e_times, _ = timed(step_host, max(1, args.steps), 1, w.rank)
     sweep = {}
@@ -245,7 +319,8 @@ def run_ours(args, rank_env):
     lib.gpk_destroy(ctx)
     h2d = X_h.numel() * 8 + y_h.numel() * 8 + Z_h.numel() * 8
     d2h = 8 * (d + 2) + 8 * l + 4 * l + 8 * 8
-    return dict(times=times, e2e_times=e2e_times, launches=launches, mvm=mvm, dc=dc, f64=f64, vec=vec,
+    return dict(times=times, e2e_times=e2e_times, mean_step=float(np.mean(times)),
+                mean_e2e=float(np.mean(e2e_times)), launches=launches, mvm=mvm, dc=dc, f64=f64, vec=vec,
                 clocks=clk.summary(),
                 mvm_variant=mvm_variant,
                 telemetry=telemetry, sweep=sweep, h2d=h2d, d2h=d2h, w=w)
@@ -254,10 +329,35 @@ def run_ours(args, rank_env):
 # ---------------------------------------------------------------------------
 # CPU arm: the reference algorithm's restatement (oracle/) on the host cores
 # ---------------------------------------------------------------------------
-def cpu_sample(w, iters_fwd, budget_s=20.0):
+def reference_iterations(w, gpu_fwd_mean=None):
+    """CG iteration counts of the REFERENCE evaluation of workload w (evaluate_mll,
+    gp_likelihood.hpp:51-103): the oracle's own counts from the committed golden fixture when
+    there is one (C2 ranks 0/100/500, tests/golden/c2_oracle_rank*.json); otherwise the GPU
+    run's measured forward mean for every solve (C3-C5 hit the 200-iteration cap), labelled."""
+    g = os.path.join(ROOT, "tests", "golden", f"{w.name.lower()}_oracle_rank{w.rank}.json")
+    l, d = w.probes, w.d
+    if os.path.exists(g):
+        gj = json.load(open(g))
+        fwd = gj["forward_cg_iterations"]
+        return {"y": gj["solve_iterations"], "fwd_total": int(sum(fwd)),
+                "bwd_total": int(gj["total_cg_iterations"] - gj["solve_iterations"] - sum(fwd)),
+                "source": f"oracle golden {os.path.relpath(g, ROOT)} (the reference algorithm's own counts)"}
+    table = os.path.join(ROOT, "profiles", "iteration_counts.json")
+    m = None
+    if gpu_fwd_mean:
+        m, src = float(gpu_fwd_mean), "this run's GPU forward mean (every solve assumed alike)"
+    elif os.path.exists(table) and w.name in json.load(open(table)):
+        m, src = float(json.load(open(table))[w.name]["forward_mean"]), "profiles/iteration_counts.json (GPU-measured)"
+    else:
+        m, src = float(w.max_iters), "max_iters (no measured count available)"
+    return {"y": m, "fwd_total": m * l, "bwd_total": m * (d + 1) * l, "source": src}
+
+
+def cpu_sample(w, its, budget_s=20.0):
     """Times MatrixFree applies (kernels.hpp:184-195, 1024-row blocks) with OpenMP over
     columns (the reference's probe parallelism, krylov.hpp:141 / trace_estimation.hpp:163)
-    and extrapolates the reference's apply count for one evaluate_mll."""
+    and extrapolates the reference's apply count for one evaluate_mll from its CG iteration
+    counts `its` (reference_iterations)."""
     import oracle
 
     cores = oracle.num_threads()
@@ -267,7 +367,6 @@ def cpu_sample(w, iters_fwd, budget_s=20.0):
     # bounded sample: rows subset so that one apply on each core takes ~budget/2
     t_cols = cores
     v = np.asfortranarray(np.random.default_rng(0).standard_normal((n, t_cols)))
-    # probe one small apply to size the sample
     rows = min(n, 2048)
     xs = x[:rows]
     t0 = time.perf_counter()
@@ -282,14 +381,38 @@ def cpu_sample(w, iters_fwd, budget_s=20.0):
         t_apply = time.perf_counter() - t0
         sample = f"{t_cols} concurrent full-size MatrixFree applies (n={n}, oracle port)"
     l, d = w.probes, w.d
-    m = iters_fwd
-    # wall-clock apply rounds of evaluate_mll (gp_likelihood.hpp:51-103): the y solve runs alone,
-    # probe solves run `cores` at a time, then (d+1) backward batches of l solves, plus the
-    # (d+1) deriv_applies on u and (d+1) l on the probes.
-    rounds = m + math.ceil(l / cores) * m + (d + 1) * (math.ceil(l / cores) * (m + 1) + 1)
+    par = min(cores, l)
+    # wall-clock apply rounds of evaluate_mll: the y solve runs alone; the probe solves of a phase
+    # run `par` at a time (OpenMP over probes); every trace_residual also applies dK_w to its l
+    # probes, and deriv_apply(w, u) runs alone, for the d+1 non-noise parameters
+    rounds = (its["y"] + its["fwd_total"] / par + its["bwd_total"] / par
+              + (d + 1) * (math.ceil(l / par) + 1))
     return {"value": rounds * t_apply, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": sample + f"; extrapolated x{rounds} apply rounds (m={m} CG iterations)",
-            "seconds_per_apply_round": t_apply, "extrapolated": True}
+            "sample": sample + f"; extrapolated x{rounds:.0f} apply rounds",
+            "iterations": its, "seconds_per_apply_round": t_apply, "extrapolated": True}
+
+
+def cpu_c1_measured():
+    """The BASELINE C1 evaluation (configs[0], the reference's CPU-runnable case) run IN FULL by
+    the oracle port on the host cores: pivoted Cholesky + derivative factors + evaluate_mll,
+    MatrixFree (the reference's operator, optimizer.hpp:427 picks Dense for n <= 4096; both
+    modes are in the oracle), max 100 iterations as configured."""
+    import oracle
+
+    w = workloads.config("C1")
+    x, y = workloads.generate(w)
+    p = oracle.Params(w.d, w.outputscale, lengthscales=w.lengthscales, noise=w.noise)
+    seed = oracle.mix_seed(workloads.PROBE_SEED, 1)
+    z = oracle.make_probes(w.n, w.probes, seed)
+    out = {}
+    for mode, name in ((oracle.DENSE, "dense"), (oracle.MATRIX_FREE, "matrix_free")):
+        t0 = time.perf_counter()
+        r = oracle.evaluate_mll(w.family, x, p, y, z, seed=seed, prec="pivchol", rank=w.rank, mode=mode,
+                                max_iters=w.max_iters, rel_tol=w.rel_tol)
+        out[name] = {"seconds": time.perf_counter() - t0, "value": r["value"],
+                     "total_cg_iterations": r["total_cg_iterations"]}
+    return {"workload": "C1 (n=2048 d=3 rbf l=8 rank=16 max_iters=100)", "measured": True,
+            "cores": oracle.num_threads(), "kind": "port", **out}
 
 
 def cpu_model():
@@ -303,6 +426,25 @@ def cpu_model():
 
 
 # ---------------------------------------------------------------------------
+def spawn(args):
+    """--gpus N without a launcher: re-exec this script under torch.distributed.run, one rank
+    per GPU (the driver's own launch form), after checking N GPUs are visible."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -312,63 +454,91 @@ def main():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--rank", type=int, default=None)
     ap.add_argument("--precision", default="tf32x3", choices=["tf32x3", "fp32", "fp64"])
-    ap.add_argument("--backward", default="fused", choices=["fused", "faithful"])
+    ap.add_argument("--backward", default="auto", choices=["auto", "fused", "faithful"])
     ap.add_argument("--refine", type=int, default=2)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                     help="N>1: one row-sharded evaluation over N GPUs (NCCL) or N independent replicas")
-    ap.add_argument("--cpu-iters", type=int, default=None, help="CG iterations for the CPU extrapolation")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "group"],
+                    help="TEST ONLY 'group': the N ranks as threads on one GPU over the host-staged rank group")
+    ap.add_argument("--cpu-c1", action="store_true", help="reference arm: also run the full C1 evaluation")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
+    env_world = os.environ.get("WORLD_SIZE")
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(env_world or "1")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     peaks, peaks_src = load_peaks()
     w = workloads.config(args.workload, rank=args.rank)
-    config = {"workload": f"{w.name}: n={w.n} d={w.d} {['rbf', 'matern12', 'matern32', 'matern52'][w.family]} "
-                          f"l={w.probes} rank={w.rank} max_iters={w.max_iters} tol={w.rel_tol}",
-              "n": w.n, "d": w.d, "probes": w.probes, "precond_rank": w.rank, "precision": args.precision,
-              "backward": args.backward, "l2": "flushed between timed steps (256 MB write)",
-              "step": "set_data + set_params + pivoted_cholesky(+deriv factors) + evaluate_mll(value+grad)",
-              "parallelism": (f"row-sharded x{world} (NCCL)" if args.mode == "sharded" else f"replicas x{world}")
-              if world > 1 else "1 GPU"}
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        iters = args.cpu_iters or w.max_iters
-        cb = cpu_sample(w, iters)
+        if rank != 0:  # under torchrun rank 0 alone runs the CPU reference arm
+            return 0
+        its = reference_iterations(w)
+        cb = cpu_sample(w, its)
         cb["cpu_model"] = cpu_model()
+        if args.cpu_c1 or w.name == "C1":
+            cb["c1_full_evaluation"] = cpu_c1_measured()
+        cfg = config_of(w, args, world if env_world else args.gpus)
         line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": 0,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["value"] * 1e3,
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded stand-in for the BASELINE config)", "config": config,
+                "data": "synthetic (seeded stand-in for the BASELINE config)", "config": cfg,
                 "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                                             "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
-        return
+        return 0
 
-    if world > 1:
+    if env_world is None and args.gpus > 1 and args.comm == "nccl":
+        return spawn(args)
+    if env_world is not None and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+
+    if args.comm == "group" and args.gpus > 1:
+        import torch  # noqa: F401  (before the library: torch's bundled NCCL must load first)
+
+        from paper_2107_00243_b200 import capi
+
+        shared = GroupComm.Shared(args.gpus, capi.lib())
+        results, errs = [None] * args.gpus, []
+
+        def body(r):
+            try:
+                results[r] = run_ours(args, GroupComm(shared, r))
+            except Exception as e:  # noqa: BLE001
+                errs.append(e)
+                shared.bar.abort()
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(args.gpus)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        comm = GroupComm(shared, 0)
+        world = args.gpus
+        r = results[0]
+        r["max_times"] = [max(res["mean_step"] for res in results), max(res["mean_e2e"] for res in results)]
+    elif world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-    r = run_ours(args, (rank, world, local))
-    import torch
-
-    per_step = max(r["times"]) if False else float(np.mean(r["times"]))
-    e2e = float(np.mean(r["e2e_times"]))
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([per_step, e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        per_step, e2e = float(t[0]), float(t[1])
+        comm = DistComm(rank, world, local)
+        r = run_ours(args, comm)
+        r["max_times"] = comm.max([r["mean_step"], r["mean_e2e"]])
+    else:
+        comm = SingleComm()
+        r = run_ours(args, comm)
+        r["max_times"] = [r["mean_step"], r["mean_e2e"]]
+    per_step, e2e = r["max_times"]  # max over ranks of each rank's device-timed mean
     # replicas: N independent evaluations per step -> whole-job seconds per evaluation
-    # sharded: one evaluation across all GPUs (strong scaling); replicas: N evaluations per step
+    # sharded: one evaluation across all GPUs (strong scaling)
     div = world if args.mode == "replicas" else 1
     value = per_step / div
     e2e_value = e2e / div
@@ -456,25 +626,41 @@ def main():
             "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": False,
             "scaling": "weak" if (world == 1 or args.mode == "replicas") else "strong", "vs_baseline": None,
             "dtype": {"fp64": "f64", "fp32": "f32 entries+contraction / f64 CG state",
-                      "tf32x3": "f32 entries, 3xTF32 tensor-core contraction / f64 CG state"}[args.precision],
+                      "tf32x3": "f32 entries; tcgen05 contraction in 3xF16 hi/lo (22 significant bits, Gram "
+                                "path; 3xTF32 on the direct path) / f64 CG state"}[args.precision],
             "data": "synthetic (seeded stand-in for the BASELINE config; UCI data unavailable offline)",
-            "config": config, "gpu_launches": r["launches"],
+            "config": config_of(w, args, world), "gpu_launches": r["launches"],
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
             "roofline": roofline, "clocks": {"sm_mhz": clk.get("sm_mhz"), "sm_max_mhz": clk.get("sm_max_mhz"),
                                              "reasons": clk.get("reasons", [])},
             "telemetry": r["telemetry"], "sweep": r["sweep"]}
+    if args.comm == "group":
+        line["comm"] = "group (TEST ONLY: ranks are threads on one GPU, host-staged collectives)"
     if rank == 0 and world == 1 and not args.no_cpu:
-        iters = args.cpu_iters or int(round(r["telemetry"]["forward_cg_iterations_mean"])) or w.max_iters
-        cb = cpu_sample(w, iters)
+        its = reference_iterations(w, None if os.path.exists(os.path.join(
+            ROOT, "tests", "golden", f"{w.name.lower()}_oracle_rank{w.rank}.json")) else
+            r["telemetry"]["forward_cg_iterations_mean"])
+        cb = cpu_sample(w, its)
         cb["cpu_model"] = cpu_model()
         line["cpu_baseline"] = cb
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if world > 1 and args.comm == "nccl":
         import torch.distributed as dist
 
         dist.destroy_process_group()
+    return 0
+
+
+def config_of(w, args, world):
+    return {"workload": f"{w.name}: n={w.n} d={w.d} {['rbf', 'matern12', 'matern32', 'matern52'][w.family]} "
+                        f"l={w.probes} rank={w.rank} max_iters={w.max_iters} tol={w.rel_tol}",
+            "n": w.n, "d": w.d, "probes": w.probes, "precond_rank": w.rank, "precision": args.precision,
+            "backward": args.backward, "l2": "flushed between timed steps (256 MB write)",
+            "step": "set_data + set_params + pivoted_cholesky(+deriv factors) + evaluate_mll(value+grad)",
+            "parallelism": (f"row-sharded x{world} (NCCL)" if args.mode == "sharded" else f"replicas x{world}")
+            if world > 1 else "1 GPU"}
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -72,8 +72,10 @@ typedef struct {
   gpk_cg_cfg solver;
   int share_probes;    /* reuse the forward probe batch in the backward pass (reference default 1) */
   int with_gradient;   /* evaluate_mll's with_gradient flag */
-  int backward_mode;   /* 0: fused bilinear derivative pass over the forward solves (default)
-                          1: reference-faithful: mBCG over the (d+1) l right-hand sides dK_w z_i */
+  int backward_mode;   /* 0: fused bilinear derivative pass over the forward solves
+                          1: reference-faithful: mBCG over the (d+1) l right-hand sides dK_w z_i
+                          2: auto (default): fused when every forward solve converged, else faithful
+                             (the fused identity needs converged probe solves) */
 } gpk_mll_cfg;
 
 /* gp_likelihood.hpp:35-46 MllEvaluation, caller-allocated arrays. */
@@ -91,11 +93,17 @@ typedef struct {
   double logdet_precond;        /* log det P_hat */
   double quad;                  /* y^T u */
   int refine_passes;            /* fp64 defect-correction passes used */
-  double max_true_rel_residual; /* max over columns of ||P^-1(b - K_hat x)|| / ||P^-1 b|| in fp64 (or -1) */
+  double max_true_rel_residual; /* fp64 audit (precision != FP64, refine > 0): max over ALL solve columns of
+                                   ||P^-1(b - K_hat x)|| / ||P^-1 b||, capped columns included; -1 when not
+                                   audited (FP64 mode, refine = 0, or no column converged: nothing to certify) */
   double seconds_solve, seconds_backward, seconds_total;
   long long kernel_entries;     /* kernel-matrix entries evaluated by the fused kernels */
   long long mvm_flops;          /* algorithmic fused-MVM flops */
   int gpu_launches;             /* kernels this library launched in the call */
+  double max_cg_rel_residual;   /* max over solve columns of the CG recurrence's last ||P^-1 r_k|| / ||P^-1 b||
+                                   (krylov.hpp:102-106; what the stopping rule saw, every precision) */
+  int unconverged_columns;      /* solve columns that hit max_iters (converged = false, krylov.hpp:120) */
+  int backward_mode_used;       /* 0 fused, 1 faithful (what backward_mode 2 resolved to) */
 } gpk_mll_result;
 
 /* ---- context ----------------------------------------------------------- */

@@ -69,7 +69,7 @@ struct CgConfig {  // krylov.hpp:15-24 (+ GPU fields)
 struct MllConfig {  // gp_likelihood.hpp:26-32
   CgConfig solver;
   bool share_probes = true;
-  int backward_mode = 0;  // 0 fused derivative pass, 1 reference-faithful per-RHS solves
+  int backward_mode = 2;  // 0 fused derivative pass, 1 reference-faithful per-RHS solves, 2 auto
 };
 
 struct MllEvaluation {  // gp_likelihood.hpp:35-46

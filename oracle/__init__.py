@@ -18,10 +18,11 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_LIB_NAME = "liboracle_native.so" if os.environ.get("ORC_NATIVE") == "1" else "liboracle.so"
+_LIB_PATH = os.path.join(_HERE, _LIB_NAME)
 
 RBF, MATERN12, MATERN32, MATERN52, RATQUAD = 0, 1, 2, 3, 4
-DENSE, MATRIX_FREE = 0, 1
+DENSE, MATRIX_FREE, CACHED = 0, 1, 2
 FAMILIES = {"rbf": RBF, "matern12": MATERN12, "matern32": MATERN32, "matern52": MATERN52, "ratquad": RATQUAD}
 
 
@@ -48,7 +49,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(
         os.path.join(_HERE, "gpkrylov_oracle.cpp")
     ):
-        subprocess.run(["make", "-C", _HERE, "-B" if force else "liboracle.so"], check=True,
+        subprocess.run(["make", "-C", _HERE, "-B" if force else _LIB_NAME], check=True,
                        stdout=subprocess.DEVNULL)
     return _LIB_PATH
 
@@ -140,6 +141,33 @@ def kernel_apply(family, x, p: Params, v, which=-1, mode=MATRIX_FREE, block_rows
     _check(lib().orc_kernel_apply(C.c_int(family), C.c_double(alpha), _p(x), C.c_int64(n), C.c_int(d),
                                   C.c_double(p.log_o), _p(p.log_ls), C.c_double(p.log_noise), C.c_int(mode),
                                   C.c_int64(block_rows), C.c_int(which), _p(v), C.c_int(v.shape[1]), _p(out)))
+    return out
+
+
+def kernel_apply_block(family, x, p: Params, v, mode=CACHED, alpha=1.0):
+    """KernelOperator::apply_block over all columns of v (oracle-internal block apply)."""
+    x = _f(x)
+    v = _f(v)
+    n, d = x.shape
+    out = np.empty_like(v, order="F")
+    _check(lib().orc_kernel_apply_block(C.c_int(family), C.c_double(alpha), _p(x), C.c_int64(n), C.c_int(d),
+                                        C.c_double(p.log_o), _p(p.log_ls), C.c_double(p.log_noise), C.c_int(mode),
+                                        _p(v), C.c_int(v.shape[1]), _p(out)))
+    return out
+
+
+def kernel_apply_rows(family, x, p: Params, rows, v, alpha=1.0):
+    """Rows ``rows`` of (K + sigma^2 I) V with the MatrixFree entries and sums (kernels.hpp:184-195,
+    :296-306): a (len(rows), t) array.  For MVM row-subset parity at the large BASELINE shapes."""
+    x = _f(x)
+    v = _f(v if np.ndim(v) == 2 else np.asarray(v)[:, None])
+    n, d = x.shape
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty((len(rows), v.shape[1]), order="F")
+    _check(lib().orc_kernel_apply_rows(C.c_int(family), C.c_double(alpha), _p(x), C.c_int64(n), C.c_int(d),
+                                       C.c_double(p.log_o), _p(p.log_ls), C.c_double(p.log_noise),
+                                       rows.ctypes.data_as(_L), C.c_int64(len(rows)), _p(v), C.c_int(v.shape[1]),
+                                       _p(out)))
     return out
 
 
@@ -288,9 +316,14 @@ def dplr_trace_inv_deriv(noise, L, dL, shift=0.0):
 
 
 def evaluate_mll(family, x, p: Params, y, probes, seed=0, prec="pivchol", rank=0, diag_tol=0.0, mode=MATRIX_FREE,
-                 max_iters=100, rel_tol=1e-6, share_probes=True, with_gradient=True, alpha=1.0):
+                 max_iters=100, rel_tol=1e-6, share_probes=True, with_gradient=True, alpha=1.0, lockstep=False):
     """evaluate_mll (gp_likelihood.hpp:51-103) with the preconditioner built as
-    build_preconditioner's pivoted-Cholesky branch (experiments.hpp:37-38, :59-61)."""
+    build_preconditioner's pivoted-Cholesky branch (experiments.hpp:37-38, :59-61).
+
+    ``lockstep=True`` runs every solve of a phase as one lock-step batch (the batched_pcg
+    contract, krylov.hpp:131-153); with ``mode=CACHED`` the operator keeps its MatrixFree
+    kernel block and applies it to the whole block per iteration — bitwise the MatrixFree
+    per-column result (tests/test_oracle_lockstep.py), fast enough for the C2 fixtures."""
     x = _f(x)
     n, d = x.shape
     z = _f(probes)
@@ -303,15 +336,17 @@ def evaluate_mll(family, x, p: Params, y, probes, seed=0, prec="pivchol", rank=0
     fi = np.zeros(l, dtype=np.int32)
     sc = np.zeros(8)
     u = np.zeros(n)
-    _check(lib().orc_evaluate_mll(C.c_int(family), C.c_double(alpha), _p(x), C.c_int64(n), C.c_int(d),
-                                  C.c_double(p.log_o), _p(p.log_ls), C.c_double(p.log_noise), _p(y), _p(z),
-                                  C.c_int(l), C.c_uint64(seed), C.c_int(kind), C.c_int(rank), C.c_double(diag_tol),
-                                  C.c_int(mode), C.c_int(max_iters), C.c_double(rel_tol), C.c_int(int(share_probes)),
-                                  C.c_int(int(with_gradient)), _p(grad), _p(fg), _p(bg), fi.ctypes.data_as(_I),
-                                  _p(sc), _p(u)))
+    piv = np.zeros(max(rank, 1), dtype=np.int64)
+    _check(lib().orc_evaluate_mll2(C.c_int(family), C.c_double(alpha), _p(x), C.c_int64(n), C.c_int(d),
+                                   C.c_double(p.log_o), _p(p.log_ls), C.c_double(p.log_noise), _p(y), _p(z),
+                                   C.c_int(l), C.c_uint64(seed), C.c_int(kind), C.c_int(rank), C.c_double(diag_tol),
+                                   C.c_int(mode), C.c_int(max_iters), C.c_double(rel_tol), C.c_int(int(share_probes)),
+                                   C.c_int(int(with_gradient)), C.c_int(int(lockstep)), _p(grad), _p(fg), _p(bg),
+                                   fi.ctypes.data_as(_I), _p(sc), _p(u), piv.ctypes.data_as(_L)))
     return dict(value=sc[0], logdet=sc[1], quad=sc[2], value_sample_variance=sc[3], solve_iterations=int(sc[4]),
                 total_cg_iterations=int(sc[5]), logdet_precond=sc[6], gradient=grad, forward_gammas=fg,
-                backward_gammas=bg.reshape(d + 2, l), forward_cg_iterations=fi, u=u)
+                backward_gammas=bg.reshape(d + 2, l), forward_cg_iterations=fi, u=u,
+                pivots=piv[:rank].copy() if kind == 1 else None)
 
 
 def mll_exact(family, x, p: Params, y, alpha=1.0):

@@ -145,7 +145,11 @@ struct MllPrecond : SolveOp {
   virtual double trace_inv_deriv(int w) const = 0;
 };
 
-enum Mode { Dense = 0, MatrixFree = 1 };
+// Cached (oracle-only, for large golden fixtures): MatrixFree semantics with the noise-free
+// kernel block assembled ONCE (the same entries assemble_kernel_rows produces) and kept, so a
+// block of columns is applied per CG iteration; every output is the MatrixFree apply's own
+// sequential sum, so results are bitwise those of MatrixFree mode (tests/test_oracle_lockstep.py).
+enum Mode { Dense = 0, MatrixFree = 1, Cached = 2 };
 
 // kernels.hpp:157-336
 class KernelOperator : public ApplyOp {
@@ -173,6 +177,16 @@ class KernelOperator : public ApplyOp {
       dense_hat_ = assemble_kernel_rows(0, n);
       for (Index i = 0; i < n; ++i) dense_hat_(i, i) += p_.noise();
     }
+    if (mode_ == Cached) {
+      kcache_ = Mat(n, n);
+#pragma omp parallel for schedule(static)
+      for (Index r0 = 0; r0 < n; r0 += 256) {
+        const Index r1 = std::min(n, r0 + 256);
+        const Mat blk = assemble_kernel_rows(r0, r1);
+        for (Index j = 0; j < n; ++j)
+          for (Index i = 0; i < r1 - r0; ++i) kcache_(r0 + i, j) = blk(i, j);
+      }
+    }
   }
 
   Index rows() const override { return x_.rows; }
@@ -197,6 +211,10 @@ class KernelOperator : public ApplyOp {
       }
       return out;
     }
+    if (mode_ == Cached) {
+      apply_block(v.data(), n, 1, out.data(), n);
+      return out;
+    }
     for (Index r0 = 0; r0 < n; r0 += block_rows_) {
       const Index nb = std::min(block_rows_, n - r0);
       const Mat blk = assemble_kernel_rows(r0, r0 + nb);
@@ -209,6 +227,82 @@ class KernelOperator : public ApplyOp {
     const double nv = p_.noise();
     for (Index i = 0; i < n; ++i) out[static_cast<size_t>(i)] += nv * v[static_cast<size_t>(i)];
     return out;
+  }
+
+  // Block form of apply() for t columns (P, out column-major with leading dimensions ldp / ldo).
+  // Cached mode: out(i,c) = (sum_j K(i,j) P(j,c), j ascending from 0.0) + sigma^2 P(i,c) —
+  // exactly the MatrixFree apply's per-row sum (kernels.hpp:191-195 as restated above), so
+  // every column is bitwise what apply() returns.  Other modes: apply() per column.
+  void apply_block(const double* P, Index ldp, int t, double* out, Index ldo) const {
+    const Index n = rows();
+    if (mode_ != Cached) {
+#pragma omp parallel for schedule(dynamic)
+      for (int c = 0; c < t; ++c) {
+        Vec vc(P + c * ldp, P + c * ldp + n);
+        const Vec r = apply(vc);
+        std::memcpy(out + c * ldo, r.data(), sizeof(double) * static_cast<size_t>(n));
+      }
+      return;
+    }
+    for (int c = 0; c < t; ++c)  // check_input per column (kernels.hpp:285-288)
+      for (Index i = 0; i < n; ++i)
+        if (!std::isfinite(P[i + c * ldp])) throw input_error("KernelOperator: non-finite entries in input vector");
+    gemm_seq(kcache_, P, ldp, t, out, ldo);
+    const double nv = p_.noise();
+#pragma omp parallel for schedule(static)
+    for (int c = 0; c < t; ++c)
+      for (Index i = 0; i < n; ++i) out[i + c * ldo] += nv * P[i + c * ldp];
+  }
+
+  // Block form of deriv_apply(which, .) for t columns: the 1024-row MatrixFree blocks of
+  // dK/dtheta are assembled once per call and applied to every column (row blocks run in
+  // parallel); each output is deriv_apply's own sequential sum, so bitwise equal per column.
+  void deriv_apply_block(int which, const double* P, Index ldp, int t, double* out, Index ldo) const {
+    check_which(which);
+    const Index n = rows();
+    if (which == dim() + 1) {
+      for (int c = 0; c < t; ++c) std::memcpy(out + c * ldo, P + c * ldp, sizeof(double) * static_cast<size_t>(n));
+      return;
+    }
+    const Index nblk = (n + block_rows_ - 1) / block_rows_;
+#pragma omp parallel for schedule(dynamic)
+    for (Index b = 0; b < nblk; ++b) {
+      const Index r0 = b * block_rows_, nb = std::min(block_rows_, n - r0);
+      const Mat blk = assemble_deriv_rows(which, r0, r0 + nb);
+      for (int c = 0; c < t; ++c) {
+        const double* v = P + c * ldp;
+        for (Index i = 0; i < nb; ++i) {
+          double s = 0.0;
+          for (Index j = 0; j < n; ++j) s += blk(i, j) * v[j];
+          out[r0 + i + c * ldo] = s;
+        }
+      }
+    }
+  }
+
+  // Selected rows of apply(): out(r, c) = (K_hat v_c)[rows[r]] with the MatrixFree entry and sum
+  // order (kernels.hpp:296-306); rows run in parallel.  For MVM row-subset parity at large n.
+  void apply_rows(const Index* rws, Index nr, const double* P, Index ldp, int t, double* out) const {
+    const Index n = rows(), d = x_.cols;
+    const double o2 = std::pow(p_.outputscale(), 2), nv = p_.noise();
+#pragma omp parallel for schedule(dynamic)
+    for (Index r = 0; r < nr; ++r) {
+      const Index i = rws[r];
+      Vec krow(static_cast<size_t>(n));
+      for (Index j = 0; j < n; ++j) {
+        double g = 0.0;
+        for (Index k = 0; k < d; ++k) g += sx_(i, k) * sx_(j, k);
+        double s = (-2.0 * g + sq_[static_cast<size_t>(i)]) + sq_[static_cast<size_t>(j)];
+        s = std::max(s, 0.0);
+        krow[static_cast<size_t>(j)] = o2 * shape(fam_, alpha_, s);
+      }
+      for (int c = 0; c < t; ++c) {
+        const double* v = P + c * ldp;
+        double s = 0.0;
+        for (Index j = 0; j < n; ++j) s += krow[static_cast<size_t>(j)] * v[j];
+        out[r + c * nr] = s + nv * v[i];
+      }
+    }
   }
 
   // kernels.hpp:205-215: (d K_hat / d theta_which) v, raw parameter.
@@ -241,6 +335,7 @@ class KernelOperator : public ApplyOp {
     const double o2 = std::pow(p_.outputscale(), 2);
     const Index n = rows(), d = x_.cols;
     Vec out(static_cast<size_t>(n));
+#pragma omp parallel for schedule(static) if (n >= 65536)
     for (Index r = 0; r < n; ++r) {
       double g = 0.0;
       for (Index k = 0; k < d; ++k) g += sx_(r, k) * sx_(i, k);
@@ -367,6 +462,64 @@ class KernelOperator : public ApplyOp {
     return out;
   }
 
+  // out(i,c) = sum_j A(i,j) P(j,c) with j ascending from 0.0 (plain mul + add, -ffp-contract=off).
+  // Cache-blocked (row blocks of 256 per thread, j chunks of 256, 16x6 register tiles whose
+  // running sums are stored and reloaded between chunks — storing a double does not round it),
+  // so every output is the same sequential sum as the MatrixFree apply's.
+  static void gemm_seq(const Mat& a, const double* P, Index ldp, int t, double* out, Index ldo) {
+    const Index n = a.rows, m = a.cols;
+    constexpr int MR = 16, NR = 6;
+    constexpr Index MC = 256, KC = 256;
+    const Index tp = (t + NR - 1) / NR * NR;
+    std::vector<double> pt(static_cast<size_t>(m * tp), 0.0);  // P^T, row j = P(j, 0..t)
+#pragma omp parallel for schedule(static)
+    for (Index j = 0; j < m; ++j)
+      for (int c = 0; c < t; ++c) pt[static_cast<size_t>(j * tp + c)] = P[j + c * ldp];
+    const Index nblk = (n + MC - 1) / MC;
+#pragma omp parallel for schedule(dynamic)
+    for (Index blk = 0; blk < nblk; ++blk) {
+      const Index i0 = blk * MC, i1 = std::min(n, i0 + MC);
+      std::vector<double> acc(static_cast<size_t>((i1 - i0) * tp), 0.0);  // [c][i - i0]
+      const Index mb = i1 - i0;
+      for (Index j0 = 0; j0 < m; j0 += KC) {
+        const Index j1 = std::min(m, j0 + KC);
+        for (Index c0 = 0; c0 < tp; c0 += NR) {
+          Index ii = 0;
+          for (; ii + MR <= mb; ii += MR) {
+            // 16 rows = two 8-wide vectors per column (GCC vector extension; element-wise mul and
+            // add, so each lane is the scalar sum)
+            typedef double v8 __attribute__((vector_size(64)));
+            v8 r[NR][2];
+            for (int c = 0; c < NR; ++c)
+              for (int h = 0; h < 2; ++h) std::memcpy(&r[c][h], &acc[static_cast<size_t>((c0 + c) * mb + ii + 8 * h)], 64);
+            for (Index j = j0; j < j1; ++j) {
+              const double* ak = a.a.data() + (i0 + ii) + j * n;
+              const double* pj = pt.data() + j * tp + c0;
+              v8 a0, a1;
+              std::memcpy(&a0, ak, 64);
+              std::memcpy(&a1, ak + 8, 64);
+              for (int c = 0; c < NR; ++c) {
+                const double b = pj[c];
+                r[c][0] += a0 * b;
+                r[c][1] += a1 * b;
+              }
+            }
+            for (int c = 0; c < NR; ++c)
+              for (int h = 0; h < 2; ++h) std::memcpy(&acc[static_cast<size_t>((c0 + c) * mb + ii + 8 * h)], &r[c][h], 64);
+          }
+          for (; ii < mb; ++ii)
+            for (int c = 0; c < NR; ++c) {
+              double s = acc[static_cast<size_t>((c0 + c) * mb + ii)];
+              for (Index j = j0; j < j1; ++j) s += a(i0 + ii, j) * pt[static_cast<size_t>(j * tp + c0 + c)];
+              acc[static_cast<size_t>((c0 + c) * mb + ii)] = s;
+            }
+        }
+      }
+      for (int c = 0; c < t; ++c)
+        for (Index ii = 0; ii < mb; ++ii) out[i0 + ii + c * ldo] = acc[static_cast<size_t>(c * mb + ii)];
+    }
+  }
+
   int fam_;
   double alpha_;
   Mat x_;
@@ -376,6 +529,7 @@ class KernelOperator : public ApplyOp {
   Mat sx_;
   Vec sq_;
   Mat dense_hat_;
+  Mat kcache_;
 };
 
 // Dense symmetric matrix as an operator (common.hpp:73-79; lower triangle read).
@@ -818,10 +972,18 @@ inline DiagPlusLowRank pivoted_cholesky(const KernelAccessor& k, int rank, doubl
     if (d[static_cast<size_t>(p)] <= diag_tol) break;
     Vec c = k.column(p);
     if (step > 0) {
-      for (Index i = 0; i < n; ++i) {
-        double g = 0.0;
-        for (Index s = 0; s < step; ++s) g += l(i, s) * l(p, s);
-        c[static_cast<size_t>(i)] -= g;
+      // g_i = sum_{s < step} l(i,s) l(p,s), s ascending per row (the reference's row GEMV order);
+      // swept column by column so each pass over L is contiguous — per-row sums are unchanged.
+#pragma omp parallel for schedule(static) if (n >= 65536)
+      for (Index i0 = 0; i0 < n; i0 += 4096) {
+        const Index i1 = std::min(n, i0 + 4096);
+        double g[4096] = {};
+        for (Index s = 0; s < step; ++s) {
+          const double lp = l(p, s);
+          const double* ls = l.col(s);
+          for (Index i = i0; i < i1; ++i) g[i - i0] += ls[i] * lp;
+        }
+        for (Index i = i0; i < i1; ++i) c[static_cast<size_t>(i)] -= g[i - i0];
       }
     }
     const double root = std::sqrt(d[static_cast<size_t>(p)]);
@@ -850,15 +1012,24 @@ inline std::vector<Mat> pivoted_cholesky_deriv_factors(const KernelOperator& op,
       const Index pv = piv[static_cast<size_t>(s)];
       Vec dc = op.kernel_deriv_column(w, pv);
       if (s > 0) {
-        for (Index i = 0; i < n; ++i) {
-          double g = 0.0;
-          for (Index c = 0; c < s; ++c) g += dl(i, c) * l(pv, c);
-          dc[static_cast<size_t>(i)] -= g;
-        }
-        for (Index i = 0; i < n; ++i) {
-          double g = 0.0;
-          for (Index c = 0; c < s; ++c) g += l(i, c) * dl(pv, c);
-          dc[static_cast<size_t>(i)] -= g;
+        // the reference's two row GEMVs, c ascending per row, swept column by column (same sums)
+#pragma omp parallel for schedule(static) if (n >= 16384)
+        for (Index i0 = 0; i0 < n; i0 += 2048) {
+          const Index i1 = std::min(n, i0 + 2048);
+          double g1[2048] = {}, g2[2048] = {};
+          for (Index c = 0; c < s; ++c) {
+            const double a1 = l(pv, c), a2 = dl(pv, c);
+            const double* dlc = dl.col(c);
+            const double* lc = l.col(c);
+            for (Index i = i0; i < i1; ++i) {
+              g1[i - i0] += dlc[i] * a1;
+              g2[i - i0] += lc[i] * a2;
+            }
+          }
+          for (Index i = i0; i < i1; ++i) {
+            dc[static_cast<size_t>(i)] -= g1[i - i0];
+            dc[static_cast<size_t>(i)] -= g2[i - i0];
+          }
         }
       }
       const double root = l(pv, s);
@@ -1077,6 +1248,227 @@ inline MllEvaluation evaluate_mll(const Vec& y, const KernelOperator& k, const M
     const Vec dku = k.deriv_apply(w, u);
     const double q = dot(u.data(), dku.data(), n);
     out.gradient[static_cast<size_t>(w)] = 0.5 * (q - tau) * k.params().raw_value(w);
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Lock-step batched PCG (the batched_pcg contract, krylov.hpp:131-153: columns are
+// independent and each column is bitwise pcg_solve).  All active columns advance one
+// iteration together so the operator is applied to the whole block at once
+// (KernelOperator::apply_block); every per-column step below is pcg_solve's own
+// statement sequence (:559-611 above), so with a bitwise-equal block apply each column
+// reproduces pcg_solve exactly (tests/test_oracle_lockstep.py).  Oracle-only: this is how
+// the large golden fixtures (tests/golden/make_golden_big.py) are made in minutes.
+// ---------------------------------------------------------------------------
+struct LockstepOut {
+  std::vector<CgResult> res;
+  std::vector<std::string> err;  // pcg_solve's exception text per column ("" = none)
+};
+
+inline LockstepOut pcg_lockstep(const KernelOperator& a, const Mat& b, const SolveOp& prec, const CgConfig& cfg,
+                                const std::vector<char>& collect) {
+  cfg.validate();
+  const Index n = a.rows();
+  const int t = static_cast<int>(b.cols);
+  require(b.rows == n, "pcg_solve: rhs length does not match operator");
+  LockstepOut o;
+  o.res.resize(static_cast<size_t>(t));
+  o.err.resize(static_cast<size_t>(t));
+  std::vector<Vec> r(t), z(t), p(t);
+  std::vector<double> rz(t, 0.0), norm0(t, 0.0), alpha_prev(t, 0.0), beta_prev(t, 0.0);
+  std::vector<char> active(t, 0);
+#pragma omp parallel for schedule(dynamic)
+  for (int c = 0; c < t; ++c) {
+    CgResult& res = o.res[static_cast<size_t>(c)];
+    res.solution.assign(static_cast<size_t>(n), 0.0);
+    r[c].assign(b.col(c), b.col(c) + n);
+    z[c] = prec.solve(r[c]);
+    norm0[c] = norm(z[c].data(), n);
+    res.has_tridiag = collect[static_cast<size_t>(c)] != 0;
+    if (norm0[c] == 0.0) { res.converged = true; continue; }
+    p[c] = z[c];
+    rz[c] = dot(r[c].data(), z[c].data(), n);
+    active[c] = 1;
+  }
+  Mat pb, apb;
+  for (int k = 1; k <= cfg.max_iters; ++k) {
+    std::vector<int> act;
+    for (int c = 0; c < t; ++c)
+      if (active[c]) act.push_back(c);
+    if (act.empty()) break;
+    const int na = static_cast<int>(act.size());
+    pb = Mat(n, na);
+    apb = Mat(n, na);
+    for (int q = 0; q < na; ++q) std::memcpy(pb.col(q), p[act[q]].data(), sizeof(double) * static_cast<size_t>(n));
+    a.apply_block(pb.a.data(), n, na, apb.a.data(), n);
+#pragma omp parallel for schedule(dynamic)
+    for (int q = 0; q < na; ++q) {
+      const int c = act[q];
+      CgResult& res = o.res[static_cast<size_t>(c)];
+      const double* ap = apb.col(q);
+      Vec& pc = p[c];
+      Vec& rc = r[c];
+      const double pap = dot(pc.data(), ap, n);
+      const double alpha = rz[c] / pap;
+      if (!std::isfinite(alpha) || alpha <= 0.0) {
+        o.err[static_cast<size_t>(c)] = "pcg_solve: breakdown at iteration " + std::to_string(k) + " (alpha = " +
+                                        std::to_string(alpha) + "); operator or preconditioner not positive definite";
+        active[c] = 0;
+        continue;
+      }
+      if (res.has_tridiag) {
+        double d = 1.0 / alpha;
+        if (k > 1) {
+          d += beta_prev[c] / alpha_prev[c];
+          res.tsub.push_back(std::sqrt(beta_prev[c]) / alpha_prev[c]);
+        }
+        res.tdiag.push_back(d);
+      }
+      for (Index i = 0; i < n; ++i) res.solution[static_cast<size_t>(i)] += alpha * pc[static_cast<size_t>(i)];
+      for (Index i = 0; i < n; ++i) rc[static_cast<size_t>(i)] -= alpha * ap[i];
+      z[c] = prec.solve(rc);
+      const double rz_new = dot(rc.data(), z[c].data(), n);
+      if (!std::isfinite(rz_new) || rz_new < 0.0) {
+        o.err[static_cast<size_t>(c)] = "pcg_solve: breakdown at iteration " + std::to_string(k) + " (r'z = " +
+                                        std::to_string(rz_new) + ")";
+        active[c] = 0;
+        continue;
+      }
+      const double pres = norm(z[c].data(), n);
+      res.residual_history.push_back(pres);
+      res.iterations_used = k;
+      if (pres <= cfg.rel_tol * norm0[c]) { res.converged = true; active[c] = 0; continue; }
+      if (rz_new == 0.0) { res.converged = true; active[c] = 0; continue; }
+      const double beta = rz_new / rz[c];
+      for (Index i = 0; i < n; ++i) pc[static_cast<size_t>(i)] = z[c][static_cast<size_t>(i)] + beta * pc[static_cast<size_t>(i)];
+      beta_prev[c] = beta;
+      alpha_prev[c] = alpha;
+      rz[c] = rz_new;
+    }
+  }
+  return o;
+}
+
+// evaluate_mll (gp_likelihood.hpp:51-103) with every solve of one phase in ONE lock-step
+// batch: forward [y, z_1..z_l] (pcg_solve(k, y) + vr_logdet's probe solves), backward all
+// (d+1) l right-hand sides dK_w z_i (trace_residual, :190-224).  Same statements, same
+// per-column arithmetic and the same error precedence as evaluate_mll above.
+inline MllEvaluation evaluate_mll_lockstep(const Vec& y, const KernelOperator& k, const MllPrecond& prec,
+                                           const Mat& probes, std::uint64_t seed, const MllConfig& cfg,
+                                           bool with_gradient = true) {
+  const Index n = k.rows();
+  require(static_cast<Index>(y.size()) == n, "evaluate_mll: label length does not match operator");
+  const int l = static_cast<int>(probes.cols);
+  require(probes.rows == n, "vr_logdet: probe length does not match operator");
+  MllEvaluation out;
+  out.probe_seed = seed;
+  Mat fb(n, l + 1);
+  std::memcpy(fb.col(0), y.data(), sizeof(double) * static_cast<size_t>(n));
+  std::memcpy(fb.col(1), probes.a.data(), sizeof(double) * static_cast<size_t>(n * l));
+  std::vector<char> coll(static_cast<size_t>(l + 1), 1);
+  coll[0] = 0;
+  const LockstepOut fw = pcg_lockstep(k, fb, prec, cfg.solver, coll);
+  if (!fw.err[0].empty()) throw solver_error(fw.err[0]);
+  const CgResult& ur = fw.res[0];
+  out.solve_iterations = ur.iterations_used;
+  out.total_cg_iterations = ur.iterations_used;
+  const Vec& u = ur.solution;
+  out.u = u;
+  VrEstimate fwd;  // vr_logdet (:148-183)
+  fwd.deterministic = prec.logdet();
+  fwd.per_probe.assign(static_cast<size_t>(l), 0.0);
+  fwd.cg_iterations.assign(static_cast<size_t>(l), 0);
+  fwd.probe_solutions = Mat(n, l);
+  std::vector<std::string> errors(static_cast<size_t>(l));
+  std::vector<int> clamped(static_cast<size_t>(l), 0);
+#pragma omp parallel for schedule(dynamic)
+  for (int i = 0; i < l; ++i) {
+    if (!fw.err[static_cast<size_t>(i + 1)].empty()) { errors[static_cast<size_t>(i)] = fw.err[static_cast<size_t>(i + 1)]; continue; }
+    try {
+      const CgResult& res = fw.res[static_cast<size_t>(i + 1)];
+      const SlqTerm term = slq_quadrature(res.tdiag, res.tsub, [](double x) { return std::log(x); });
+      fwd.per_probe[static_cast<size_t>(i)] = term.value;
+      fwd.cg_iterations[static_cast<size_t>(i)] = res.iterations_used;
+      std::copy(res.solution.begin(), res.solution.end(), fwd.probe_solutions.col(i));
+      clamped[static_cast<size_t>(i)] = term.clamped;
+    } catch (const std::exception& e) {
+      errors[static_cast<size_t>(i)] = e.what();
+    }
+  }
+  for (int i = 0; i < l; ++i)
+    if (!errors[static_cast<size_t>(i)].empty())
+      throw numerical_error("vr_logdet: probe " + std::to_string(i) + ": " + errors[static_cast<size_t>(i)]);
+  for (int c : clamped) fwd.clamped += c;
+  finish_estimate(fwd, n, l);
+  out.forward_gammas = fwd.per_probe;
+  out.forward_cg_iterations = fwd.cg_iterations;
+  for (int it : fwd.cg_iterations) out.total_cg_iterations += it;
+  out.value_sample_variance = fwd.sample_variance;
+  out.quad = dot(y.data(), u.data(), n);
+  out.logdet = fwd.estimate;
+  out.value = -0.5 * (out.quad + fwd.estimate + static_cast<double>(n) * std::log(2.0 * M_PI));
+  if (!with_gradient) return out;
+
+  Mat bwd_store;
+  const Mat* bwd = &probes;
+  if (!cfg.share_probes) {
+    bwd_store = make_probes(n, l, mix_seed(seed, 0xb2dULL));
+    bwd = &bwd_store;
+  }
+  const int np = k.num_params();
+  const int noise_w = k.dim() + 1;
+  // dK_w [z_1..z_l, u] for every w, one block pass per w
+  Mat zu(n, l + 1);
+  std::memcpy(zu.a.data(), bwd->a.data(), sizeof(double) * static_cast<size_t>(n * l));
+  std::memcpy(zu.col(l), u.data(), sizeof(double) * static_cast<size_t>(n));
+  std::vector<Mat> dkzu(static_cast<size_t>(np));
+  std::vector<int> solved;  // parameters whose trace residual needs solves
+  for (int w = 0; w < np; ++w) {
+    dkzu[static_cast<size_t>(w)] = Mat(n, l + 1);
+    k.deriv_apply_block(w, zu.a.data(), n, l + 1, dkzu[static_cast<size_t>(w)].a.data(), n);
+    if (!(w == noise_w && cfg.share_probes)) solved.push_back(w);
+  }
+  const int ns = static_cast<int>(solved.size());
+  Mat bb(n, static_cast<Index>(ns) * l);
+  for (int q = 0; q < ns; ++q)
+    std::memcpy(bb.col(static_cast<Index>(q) * l), dkzu[static_cast<size_t>(solved[q])].a.data(),
+                sizeof(double) * static_cast<size_t>(n * l));
+  const LockstepOut bw = pcg_lockstep(k, bb, prec, cfg.solver, std::vector<char>(static_cast<size_t>(ns * l), 0));
+  out.gradient.assign(static_cast<size_t>(np), 0.0);
+  out.backward_gammas.resize(static_cast<size_t>(np));
+  for (int w = 0; w < np; ++w) {  // trace_residual for parameter w, then the gradient entry (:84-101)
+    const bool cached = (w == noise_w && cfg.share_probes);
+    const int q = cached ? -1 : static_cast<int>(std::find(solved.begin(), solved.end(), w) - solved.begin());
+    VrEstimate est;
+    est.per_probe.assign(static_cast<size_t>(l), 0.0);
+    est.cg_iterations.assign(static_cast<size_t>(l), 0);
+    std::vector<std::string> errs(static_cast<size_t>(l));
+#pragma omp parallel for schedule(dynamic)
+    for (int i = 0; i < l; ++i) {
+      const size_t col = cached ? 0 : static_cast<size_t>(q * l + i);
+      if (!cached && !bw.err[col].empty()) { errs[static_cast<size_t>(i)] = bw.err[col]; continue; }
+      try {
+        const Vec zi(bwd->col(i), bwd->col(i) + n);
+        const Vec& wv = cached ? Vec(fwd.probe_solutions.col(i), fwd.probe_solutions.col(i) + n) : bw.res[col].solution;
+        if (!cached) est.cg_iterations[static_cast<size_t>(i)] = bw.res[col].iterations_used;
+        const Vec wt = prec.solve(prec.deriv_apply(w, zi));
+        Vec diff(static_cast<size_t>(n));
+        for (Index r = 0; r < n; ++r) diff[static_cast<size_t>(r)] = wv[static_cast<size_t>(r)] - wt[static_cast<size_t>(r)];
+        est.per_probe[static_cast<size_t>(i)] = dot(zi.data(), diff.data(), n);
+      } catch (const std::exception& e) {
+        errs[static_cast<size_t>(i)] = e.what();
+      }
+    }
+    for (int i = 0; i < l; ++i)
+      if (!errs[static_cast<size_t>(i)].empty())
+        throw numerical_error("trace residual: probe " + std::to_string(i) + ": " + errs[static_cast<size_t>(i)]);
+    finish_estimate(est, n, l);
+    for (int it : est.cg_iterations) out.total_cg_iterations += it;
+    out.backward_gammas[static_cast<size_t>(w)] = est.per_probe;
+    const double tau = prec.trace_inv_deriv(w) + est.stochastic;
+    const double qd = dot(u.data(), dkzu[static_cast<size_t>(w)].col(l), n);
+    out.gradient[static_cast<size_t>(w)] = 0.5 * (qd - tau) * k.params().raw_value(w);
   }
   return out;
 }
@@ -1779,11 +2171,12 @@ int orc_dplr_trace_inv_deriv(double noise, const double* lfac, const double* dlf
 // bwd_gammas ((d+2) x l, row-major by parameter), fwd_iters (l), scalars[8] =
 // {value, logdet, quad, value_sample_variance, solve_iterations,
 //  total_cg_iterations, logdet_P, 0}; u (n, optional).
-int orc_evaluate_mll(int family, double alpha, const double* x, std::int64_t n, int d, double log_o,
-                     const double* log_ls, double log_noise, const double* y, const double* probes, int l,
-                     std::uint64_t seed, int prec_kind, int rank, double diag_tol, int mode, int max_iters,
-                     double rel_tol, int share_probes, int with_gradient, double* grad, double* fwd_gammas,
-                     double* bwd_gammas, int* fwd_iters, double* scalars, double* u) {
+int orc_evaluate_mll2(int family, double alpha, const double* x, std::int64_t n, int d, double log_o,
+                      const double* log_ls, double log_noise, const double* y, const double* probes, int l,
+                      std::uint64_t seed, int prec_kind, int rank, double diag_tol, int mode, int max_iters,
+                      double rel_tol, int share_probes, int with_gradient, int lockstep, double* grad,
+                      double* fwd_gammas, double* bwd_gammas, int* fwd_iters, double* scalars, double* u,
+                      std::int64_t* pivots_out) {
   return guard([&] {
     orc::Hyper h = to_hyper(log_o, log_ls, d, log_noise);
     orc::KernelOperator op(family, alpha, to_mat(x, n, d), h, mode);
@@ -1803,7 +2196,12 @@ int orc_evaluate_mll(int family, double alpha, const double* x, std::int64_t n, 
     cfg.share_probes = share_probes != 0;
     const orc::Mat z = to_mat(probes, n, l);
     const orc::Vec yv(y, y + n);
-    const orc::MllEvaluation e = orc::evaluate_mll(yv, op, *prec, z, seed, cfg, with_gradient != 0);
+    const orc::MllEvaluation e = lockstep ? orc::evaluate_mll_lockstep(yv, op, *prec, z, seed, cfg, with_gradient != 0)
+                                          : orc::evaluate_mll(yv, op, *prec, z, seed, cfg, with_gradient != 0);
+    if (pivots_out && prec_kind == 1) {
+      const auto& pv = static_cast<const orc::DiagPlusLowRank&>(*prec).pivots();
+      for (size_t i = 0; i < pv.size(); ++i) pivots_out[i] = pv[i];
+    }
     scalars[0] = e.value;
     scalars[1] = e.logdet;
     scalars[2] = e.quad;
@@ -1824,6 +2222,34 @@ int orc_evaluate_mll(int family, double alpha, const double* x, std::int64_t n, 
           for (int i = 0; i < l; ++i) bwd_gammas[w * l + i] = e.backward_gammas[static_cast<size_t>(w)][static_cast<size_t>(i)];
       }
     }
+  });
+}
+
+int orc_evaluate_mll(int family, double alpha, const double* x, std::int64_t n, int d, double log_o,
+                     const double* log_ls, double log_noise, const double* y, const double* probes, int l,
+                     std::uint64_t seed, int prec_kind, int rank, double diag_tol, int mode, int max_iters,
+                     double rel_tol, int share_probes, int with_gradient, double* grad, double* fwd_gammas,
+                     double* bwd_gammas, int* fwd_iters, double* scalars, double* u) {
+  return orc_evaluate_mll2(family, alpha, x, n, d, log_o, log_ls, log_noise, y, probes, l, seed, prec_kind, rank,
+                           diag_tol, mode, max_iters, rel_tol, share_probes, with_gradient, 0, grad, fwd_gammas,
+                           bwd_gammas, fwd_iters, scalars, u, nullptr);
+}
+
+int orc_kernel_apply_block(int family, double alpha, const double* x, std::int64_t n, int d, double log_o,
+                           const double* log_ls, double log_noise, int mode, const double* v, int t, double* out) {
+  return guard([&] {
+    orc::KernelOperator op(family, alpha, to_mat(x, n, d), to_hyper(log_o, log_ls, d, log_noise), mode);
+    op.apply_block(v, n, t, out, n);
+  });
+}
+
+// Selected rows of (K + sigma^2 I) V (MatrixFree entries and sums): out is nr x t column-major.
+int orc_kernel_apply_rows(int family, double alpha, const double* x, std::int64_t n, int d, double log_o,
+                          const double* log_ls, double log_noise, const std::int64_t* rows, std::int64_t nr,
+                          const double* v, int t, double* out) {
+  return guard([&] {
+    orc::KernelOperator op(family, alpha, to_mat(x, n, d), to_hyper(log_o, log_ls, d, log_noise), orc::MatrixFree);
+    op.apply_rows(rows, nr, v, n, t, out);
   });
 }
 

@@ -37,7 +37,9 @@ class gpk_mll_result(C.Structure):
                 ("total_cg_iterations", C.c_int), ("logdet", C.c_double), ("logdet_precond", C.c_double),
                 ("quad", C.c_double), ("refine_passes", C.c_int), ("max_true_rel_residual", C.c_double),
                 ("seconds_solve", C.c_double), ("seconds_backward", C.c_double), ("seconds_total", C.c_double),
-                ("kernel_entries", C.c_longlong), ("mvm_flops", C.c_longlong), ("gpu_launches", C.c_int)]
+                ("kernel_entries", C.c_longlong), ("mvm_flops", C.c_longlong), ("gpu_launches", C.c_int),
+                ("max_cg_rel_residual", C.c_double), ("unconverged_columns", C.c_int),
+                ("backward_mode_used", C.c_int)]
 
 
 class gpk_opt_options(C.Structure):

@@ -60,6 +60,7 @@ GPK_DEV void beta_step(SlotState& x, double rz_new, double zz, int k, double rel
   const long long base = static_cast<long long>(x.col) * max_iters + (k - 1);
   if (resid_hist) resid_hist[base] = pres;
   x.iters = k;
+  x.pres = pres;
   if (pres <= rel_tol * x.norm0 || rz_new == 0.0) {
     x.flag = kFlagConverged;
     x.beta = 0.0;

@@ -474,6 +474,9 @@ struct gpk_ctx {
     const char* e = std::getenv("GPK_WOOD");
     return !(e && std::atoi(e) == 0);
   }();
+  // the single-rank vector phase as one cooperative launch (env GPK_COOP=0: the five-launch path)
+  bool use_coop = gpk::cg_iter_coop_available();
+  DBuf<double> w_ppap;
   bool use_persistent_pchol = [] {  // env GPK_PCHOL_STEPS=1 selects the per-step kernels (A/B checks)
     const char* e = std::getenv("GPK_PCHOL_STEPS");
     return !(e && std::atoi(e) == 1);
@@ -1042,6 +1045,19 @@ struct gpk_ctx {
   struct CgOut {
     std::vector<int> iters, converged, status;
     std::vector<double> bad, norm0;
+    std::vector<double> pres;  // last preconditioned residual norm of the CG recurrence (krylov.hpp:102)
+    // max over columns with b != 0 of pres / norm0, and the number of columns that hit max_iters
+    double max_rel_pres() const {
+      double m = 0.0;
+      for (size_t c = 0; c < pres.size(); ++c)
+        if (norm0[c] > 0.0) m = std::max(m, pres[c] / norm0[c]);
+      return m;
+    }
+    int unconverged() const {
+      int u = 0;
+      for (size_t c = 0; c < converged.size(); ++c) u += converged[c] ? 0 : 1;
+      return u;
+    }
   };
   CgOut mbcg(const double* B, long long ldb, int t, int max_iters, double rel_tol, bool fp64, double* Xout,
              long long ldx, double* alpha_h, double* beta_h, double* resid_h,
@@ -1054,6 +1070,7 @@ struct gpk_ctx {
     out.status.assign(t, 0);
     out.bad.assign(t, 0.0);
     out.norm0.assign(t, 0.0);
+    out.pres.assign(t, 0.0);
     if (t <= 0) return out;
     const int nrb = gpk::num_chunks(nl);
     for (int b = 0; b < 2; ++b) {
@@ -1182,6 +1199,7 @@ struct gpk_ctx {
       for (int s = 0; s < ta; ++s) {
         if (hs[s].flag == gpk::kFlagConverged) {
           out.iters[hs[s].col] = hs[s].iters;
+          out.pres[hs[s].col] = hs[s].pres;
           out.converged[hs[s].col] = 1;
           done.push_back(s);
         } else {
@@ -1211,6 +1229,7 @@ struct gpk_ctx {
         w_pzz.ensure(gpk::wood_g2_partials(t));
         w_cnt2.ensure(t);
         CK(cudaMemsetAsync(w_cnt2.p, 0, sizeof(unsigned) * t, st));
+        if (use_coop) w_ppap.ensure(gpk::wood_g2_partials(t));
       }
     }
     // pipelined read-back: snapshot of iteration it (async), then the decision on the
@@ -1247,10 +1266,17 @@ struct gpk_ctx {
         auto evv = prof_begin(3);
         const double vbytes = 8.0 * nl * (13.0 * ta + 2.0 * k);
         unsigned long long* vm = (!fp64 && use_tc && (gram_ok || tcg_direct) && ta <= 96) ? w_vmax.p : nullptr;
-        check_launch(gpk::launch_cg_pap_alpha(Ps, w_kx.p, noise, nl, ldn, ta, ppap, w_cnt.p, it, ss, dh_a, max_iters,
-                                              st, use_wood_s ? vm : nullptr),
-                     1, "cg_pap_alpha");
-        if (use_wood_s) {  // gpk_wood.cu: x/r update fused into the staged G1, staged G2 + dots, beta + p
+        if (!(use_wood_s && use_coop))
+          check_launch(gpk::launch_cg_pap_alpha(Ps, w_kx.p, noise, nl, ldn, ta, ppap, w_cnt.p, it, ss, dh_a,
+                                                max_iters, st, use_wood_s ? vm : nullptr),
+                       1, "cg_pap_alpha");
+        if (use_wood_s && use_coop) {  // gpk_wood.cu: the whole vector phase in one cooperative launch
+          check_launch(gpk::launch_cg_iter_coop(L.p, n, C.p, n, k, Xs, Rs, Ps, Zs, w_kx.p, ldn, ta, nl, noise, pnoise,
+                                                w_ppap.p, w_g1.p, w_W.p, w_prz.p, w_pzz.p, ss, it, rel_tol, dh_a, dh_b,
+                                                dh_r, max_iters, vm,
+                                                use_pipe ? snaps + static_cast<size_t>(it & 1) * t : nullptr, st),
+                       1, "cg_iter_coop");
+        } else if (use_wood_s) {  // gpk_wood.cu: x/r update fused into the staged G1, staged G2 + dots, beta + p
           check_launch(gpk::launch_g1s(L.p, n, k, Rs, ldn, ta, nl, w_g1.p, w_W.p, k, Xs, Ps, w_kx.p, noise, ss, st),
                        2, "g1s");
           check_launch(gpk::launch_g2s_dots_beta(C.p, n, k, w_W.p, k, ta, nl, Zs, Rs, ldn, pnoise, w_prz.p, w_pzz.p,
@@ -1308,6 +1334,7 @@ struct gpk_ctx {
       std::vector<int> all;
       for (int s = 0; s < ta; ++s) {
         out.iters[hs[s].col] = hs[s].iters;
+        out.pres[hs[s].col] = hs[s].pres;
         all.push_back(s);
       }
       finish_slots(all);
@@ -1324,18 +1351,25 @@ struct gpk_ctx {
   }
 
   // FP32 defect correction: audit the fp64 preconditioned true residual of
-  // every converged column and correct the ones above tolerance.  The fp64
+  // every column and correct the converged ones above tolerance.  The fp64
   // residual R = B - K_hat X is formed ONCE (fp64 fused MVM); after a correction
   // X += E it is updated as R -= K_hat E with the solve's own (reduced-precision)
   // operator: E is the small defect, so that product's relative error (<= ~5e-7)
   // perturbs R by ~5e-7 |R|, far below the tolerance being certified.
+  // *max_ratio = max over all columns with b != 0 (converged or not: a column that hit
+  // max_iters shows its true residual); -1 when no column converged — nothing can be
+  // certified then, and the fp64 residual MVM is skipped (the CG recurrence's own residual
+  // is reported by the caller instead, CgOut::max_rel_pres).
   int refine(const double* B, long long ldb, int t, double* Xd, long long ldx, const CgOut& cg, int max_iters,
              double rel_tol, int passes, double* max_ratio) {
+    int nconv = 0;
+    for (int c = 0; c < t; ++c) nconv += (cg.converged[c] && cg.norm0[c] > 0.0) ? 1 : 0;
+    *max_ratio = -1.0;
+    if (nconv == 0) return 0;
     w_tmp.ensure(static_cast<size_t>(t) * ldn);
     w_tmp2.ensure(static_cast<size_t>(t) * ldn);
     w_B.ensure(static_cast<size_t>(t) * ldn);
     int used = 0;
-    *max_ratio = 0.0;
     // R = B - (K X + s2 X)  in fp64
     w_kx.ensure(static_cast<size_t>(t) * ldn);
     apply_kernel(Xd, ldx, t, w_kx.p, ldn, true, -1);
@@ -1352,10 +1386,10 @@ struct gpk_ctx {
       std::vector<double> scale;
       double mr = 0.0;
       for (int c = 0; c < t; ++c) {
-        if (!cg.converged[c] || cg.norm0[c] == 0.0) continue;
+        if (cg.norm0[c] == 0.0) continue;
         const double ratio = std::sqrt(zz[c]) / cg.norm0[c];
         mr = std::max(mr, ratio);
-        if (ratio > rel_tol) {
+        if (ratio > rel_tol && cg.converged[c]) {  // a capped column cannot be certified by correction
           bad.push_back(c);
           scale.push_back(cg.norm0[c] / std::sqrt(zz[c]));
         }
@@ -1469,10 +1503,17 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   const long long launches0 = c->launches;
   c->entries = 0;
   c->flops = 0;
-  cudaEvent_t e0, e1, e2;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  CK(cudaEventCreate(&e2));
+  struct Events {  // destroyed on every exit path (the solver errors above are recoverable)
+    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+    ~Events() {
+      for (cudaEvent_t& x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } ev;
+  CK(cudaEventCreate(&ev.e[0]));
+  CK(cudaEventCreate(&ev.e[1]));
+  CK(cudaEventCreate(&ev.e[2]));
+  cudaEvent_t e0 = ev.e[0], e1 = ev.e[1], e2 = ev.e[2];
   CK(cudaEventRecord(e0, c->st));
   // unshared backward batch (gp_likelihood.hpp:79-84): its host mt19937_64 stream is drawn on a
   // host thread while the device runs the forward solve
@@ -1499,7 +1540,8 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   c->check_launch(gpk::launch_gather_cols(dZ + r0, ldz, nullptr, 1.0, nl, l, B.p + ldn, ldn, c->st), 1, "gather");
   // backward preconditioner terms on the side stream, overlapped with the forward solve
   DBuf<double> Zc, dterms;  // allocated on st: read there after the join
-  const bool side_terms = cfg->with_gradient && cfg->share_probes && cfg->backward_mode == 0 && c->use_side &&
+  require(cfg->backward_mode >= 0 && cfg->backward_mode <= 2, "MllConfig: unknown backward mode");
+  const bool side_terms = cfg->with_gradient && cfg->share_probes && cfg->backward_mode != 1 && c->use_side &&
                           c->pkind == 2 && c->k > 0 && c->world == 1 && c->have_dl;
   if (cfg->with_gradient) Zc.ensure(static_cast<size_t>(l) * ldn);
   if (side_terms) {
@@ -1519,9 +1561,20 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   }
   res->refine_passes = 0;
   res->max_true_rel_residual = -1.0;
+  res->max_cg_rel_residual = cg.max_rel_pres();
+  res->unconverged_columns = cg.unconverged();
+  res->backward_mode_used = cfg->backward_mode == 1 ? 1 : 0;
   if (!fp64 && cfg->solver.refine > 0) {
-    double mr = 0.0;
-    res->refine_passes = c->refine(B.p, ldn, t, Xs.p, ldn, cg, mi, tol, cfg->solver.refine, &mr);
+    double mr = -1.0;
+    try {  // a breakdown inside a correction solve maps like the solve it corrects
+      res->refine_passes = c->refine(B.p, ldn, t, Xs.p, ldn, cg, mi, tol, cfg->solver.refine, &mr);
+    } catch (const GpkError& e) {
+      if (e.code != GPK_SOLVER_ERROR) throw;
+      int col;
+      const std::string m = strip_col(e.msg, &col);
+      if (col <= 0) fail(GPK_SOLVER_ERROR, m);
+      fail(GPK_NUMERICAL_ERROR, "vr_logdet: probe " + std::to_string(col - 1) + ": " + m);
+    }
     res->max_true_rel_residual = mr;
   }
   const double* U = Xs.p;
@@ -1694,9 +1747,18 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         fail(GPK_NUMERICAL_ERROR, "trace residual: probe " + std::to_string(std::max(col, 0)) + ": " + m);
       }
       for (int i = 0; i < l; ++i) res->total_cg_iterations += cgb.iters[i];
+      res->max_cg_rel_residual = std::max(res->max_cg_rel_residual, cgb.max_rel_pres());
+      res->unconverged_columns += cgb.unconverged();
       if (!fp64 && cfg->solver.refine > 0) {
-        double mr;
-        c->refine(Zc.p, ldn, l, Sx.p, ldn, cgb, mi, tol, cfg->solver.refine, &mr);
+        double mr = -1.0;
+        try {
+          c->refine(Zc.p, ldn, l, Sx.p, ldn, cgb, mi, tol, cfg->solver.refine, &mr);
+        } catch (const GpkError& e) {
+          int col;
+          const std::string m = strip_col(e.msg, &col);
+          fail(GPK_NUMERICAL_ERROR, "trace residual: probe " + std::to_string(std::max(col, 0)) + ": " + m);
+        }
+        res->max_true_rel_residual = std::max(res->max_true_rel_residual, mr);
       }
       Sb = Sx.p;
       ldsb = ldn;
@@ -1708,7 +1770,13 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
       const std::vector<double> zs = c->col_dots(Zc.p, Sb, l, ldn);
       for (int i = 0; i < l; ++i) zw[d + 1][i] = zs[i];
     }
-    if (cfg->backward_mode == 0) {
+    // auto (2): the fused identity z' K^-1 dK z = s' dK z holds for converged solves; when a
+    // forward column hit max_iters the reference's truncated estimator (per-RHS solves) is
+    // reproduced instead (C1 as configured: the fused gradient's truncation error is ~3x the
+    // faithful one, profiles/r2_c1_fused_truncation.txt)
+    const bool fused_bwd = cfg->backward_mode == 0 || (cfg->backward_mode == 2 && cg.unconverged() == 0);
+    res->backward_mode_used = fused_bwd ? 0 : 1;
+    if (fused_bwd) {
       // fused bilinear derivative pass over all n^2 pairs
       const int n_pad = c->n_pad;
       const size_t elem = fp64 ? 8 : 4;
@@ -1807,9 +1875,18 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         const std::string m = strip_col(e.msg, &col);
         fail(GPK_NUMERICAL_ERROR, "trace residual: probe " + std::to_string(std::max(col, 0) % l) + ": " + m);
       }
+      res->max_cg_rel_residual = std::max(res->max_cg_rel_residual, cgw.max_rel_pres());
+      res->unconverged_columns += cgw.unconverged();
       if (!fp64 && cfg->solver.refine > 0) {
-        double mr;
-        c->refine(RH.p, ldn, tb, Wsol.p, ldn, cgw, mi, tol, cfg->solver.refine, &mr);
+        double mr = -1.0;
+        try {
+          c->refine(RH.p, ldn, tb, Wsol.p, ldn, cgw, mi, tol, cfg->solver.refine, &mr);
+        } catch (const GpkError& e) {
+          int col;
+          const std::string m = strip_col(e.msg, &col);
+          fail(GPK_NUMERICAL_ERROR, "trace residual: probe " + std::to_string(std::max(col, 0) % l) + ": " + m);
+        }
+        res->max_true_rel_residual = std::max(res->max_true_rel_residual, mr);
       }
       for (int q = 0; q < tb; ++q) res->total_cg_iterations += cgw.iters[q];
       DBuf<double> du;
@@ -1856,9 +1933,6 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   float ms1 = 0, ms2 = 0;
   CK(cudaEventElapsedTime(&ms1, e0, e1));
   CK(cudaEventElapsedTime(&ms2, e1, e2));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(e2);
   res->seconds_solve = ms1 * 1e-3;
   res->seconds_backward = ms2 * 1e-3;
   res->seconds_total = (ms1 + ms2) * 1e-3;

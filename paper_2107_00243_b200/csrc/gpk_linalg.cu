@@ -81,6 +81,7 @@ __global__ void cg_init_kernel(const double* __restrict__ part_rz, const double*
     SlotState& x = ss[s];
     x.rz = rz;
     x.norm0 = sqrt(zz);  // ||P^{-1} b|| (krylov.hpp:59-60)
+    x.pres = x.norm0;
     x.iters = 0;
     x.status = 0;
     x.alpha_prev = 0.0;
@@ -140,6 +141,7 @@ __global__ void cg_beta_kernel(const double* __restrict__ part_rz, const double*
     const long long base = static_cast<long long>(x.col) * max_iters + (k - 1);
     if (resid_hist) resid_hist[base] = pres;
     x.iters = k;
+    x.pres = pres;
     if (pres <= rel_tol * x.norm0 || rz_new == 0.0) {  // :106-113
       x.flag = kFlagConverged;
       x.beta = 0.0;

@@ -11,6 +11,7 @@ enum { kStatusOk = 0, kStatusAlpha = 1, kStatusRz = 2 };
 // Per-column CG scalars (krylov.hpp:66-68), resident on the device.
 struct SlotState {
   double rz, norm0, alpha, beta, alpha_prev, beta_prev, bad;
+  double pres;  // last recorded preconditioned residual norm ||P^-1 r_k|| (krylov.hpp:102)
   int col, iters, status, flag;
 };
 
@@ -70,6 +71,14 @@ cudaError_t launch_cg_p_vmax(double* P, const double* Z, int n, long long ldn, i
 int wood_grid();
 size_t wood_g1_workspace(int ka, int tb);
 size_t wood_g2_partials(int tb);
+// the whole single-rank CG vector phase of one iteration in ONE cooperative launch (gpk_wood.cu)
+bool cg_iter_coop_available();
+cudaError_t launch_cg_iter_coop(const double* L, long long ldl, const double* Cm, long long ldc, int ka, double* X,
+                                double* R, double* P, double* Z, const double* Y, long long ldn, int tb, int n,
+                                double sig2, double psig2, double* ppap, double* pg1, double* W, double* prz,
+                                double* pzz, SlotState* ss, int k, double rel_tol, double* ahist, double* bhist,
+                                double* rhist, int max_iters, unsigned long long* vmax, SlotState* snap,
+                                cudaStream_t st);
 // W = A^T R_new (A: ka columns, ld lda); with X != null, R_new = R - alpha (Y + s2 P) for live
 // slots is written back to R and X += alpha P (krylov.hpp:94-95)
 cudaError_t launch_g1s(const double* A, long long lda, int ka, double* R, long long ldr, int tb, int n,

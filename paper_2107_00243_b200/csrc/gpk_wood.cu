@@ -20,6 +20,8 @@
 #include <cfloat>
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "gpk_common.cuh"
 #include "gpk_linalg.h"
 
@@ -89,26 +91,25 @@ int sm_count() {
 // XR: Rn = R - alpha_s (Y + s2 P) for live slots, written back to R (and X += alpha P) by
 // the CTA that owns the rows (no other CTA reads them).  NT = 8-column tiles of the group.
 // Copy thread map: pair p = tid & 31 (elements 2p, 2p+1 of a 64-long row), rows tid / 32 + 8e.
+// One 64-column group [s0, s0 + ns) of CTA b out of G (the body of g1s_kernel, also run as a
+// phase of the cooperative CG iteration, gpk_cgcoop.cu).  The slot states are read through
+// L2 (they may have been written earlier in the same cooperative launch).
 template <bool XR, bool VEC, int NT>
-__global__ void __launch_bounds__(kWT, 2)
-    g1s_kernel(const double* __restrict__ A, long long lda, int ka, double* __restrict__ R, long long ldr, int tb,
-               int s_off, int n, double* __restrict__ part, double* __restrict__ X, const double* __restrict__ P,
-               const double* __restrict__ Y, double sig2, const SlotState* __restrict__ ss) {
-  extern __shared__ __align__(16) double wsm[];
+GPK_DEV void g1s_group(int b, int G, int s0, const double* __restrict__ A, long long lda, int ka,
+                       double* __restrict__ R, long long ldr, int tb, int n, double* __restrict__ part,
+                       double* __restrict__ X, const double* __restrict__ P, const double* __restrict__ Y, double sig2,
+                       const SlotState* ss, double* wsm, double* s_al) {
   double* As = wsm;              // [kk][kpos(i)]
   double* Bs = wsm + kWS * kSR;  // [s][kpos(i)]
-  __shared__ double s_al[kWS];   // alpha of live slots, 0 for frozen ones (XR)
-  const int G = gridDim.x, b = blockIdx.x;
   int r0, r1;
   rows_of(b, G, n, r0, r1);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, r = lane & 3, m = lane >> 2;
   const int cp = tid & 31, crow = tid >> 5, cpos = kpos(2 * cp);
-  const int s0 = s_off + blockIdx.y * kWS;
   const int ns = min(kWS, tb - s0);
   if (XR) {
     if (tid < ns) {
-      const SlotState& x = ss[s0 + tid];
-      s_al[tid] = x.flag == 0 ? x.alpha : 0.0;
+      const SlotState* x = ss + s0 + tid;
+      s_al[tid] = __ldcg(&x->flag) == 0 ? __ldcg(&x->alpha) : 0.0;
     }
   }
   for (int k0 = 0; k0 < ka; k0 += kWS) {
@@ -206,14 +207,24 @@ __global__ void __launch_bounds__(kWT, 2)
   }
 }
 
+template <bool XR, bool VEC, int NT>
+__global__ void __launch_bounds__(kWT, 2)
+    g1s_kernel(const double* __restrict__ A, long long lda, int ka, double* __restrict__ R, long long ldr, int tb,
+               int s_off, int n, double* __restrict__ part, double* __restrict__ X, const double* __restrict__ P,
+               const double* __restrict__ Y, double sig2, const SlotState* __restrict__ ss) {
+  extern __shared__ __align__(16) double wsm[];
+  __shared__ double s_al[kWS];  // alpha of live slots, 0 for frozen ones (XR)
+  g1s_group<XR, VEC, NT>(blockIdx.x, gridDim.x, s_off + blockIdx.y * kWS, A, lda, ka, R, ldr, tb, n, part, X, P, Y,
+                         sig2, ss, wsm, s_al);
+}
+
 // W[s][kk] = sum over the G CTA partials in fixed order.  A CTA owns 32 consecutive outputs
 // (coalesced 256-byte rows of the partial array); warp q sums partials q, q + 8, ... (16
 // loads in flight per thread), and the 8 warp sums are combined in warp order.
-__global__ void __launch_bounds__(256) g1s_reduce_kernel(const double* __restrict__ part, int G, int ka, int tb,
-                                                         double* __restrict__ W, long long ldw) {
-  __shared__ double red[8][32];
+GPK_DEV void g1s_reduce_chunk(long long chunk, const double* part, int G, int ka, int tb, double* W, long long ldw,
+                              double (*red)[32]) {
   const int o = threadIdx.x & 31, q = threadIdx.x >> 5;
-  const long long idx = static_cast<long long>(blockIdx.x) * 32 + o;
+  const long long idx = chunk * 32 + o;
   const long long tot = static_cast<long long>(ka) * tb;
   double acc = 0.0;
   if (idx < tot) {
@@ -239,6 +250,12 @@ __global__ void __launch_bounds__(256) g1s_reduce_kernel(const double* __restric
   }
 }
 
+__global__ void __launch_bounds__(256) g1s_reduce_kernel(const double* __restrict__ part, int G, int ka, int tb,
+                                                         double* __restrict__ W, long long ldw) {
+  __shared__ double red[8][32];
+  g1s_reduce_chunk(blockIdx.x, part, G, ka, tb, W, ldw, red);
+}
+
 // ---- G2s: Z = R / s2 - (C W) / s2 on CTA b's rows, per-CTA r.z / z.z partials, then a
 // two-level last-arrival reduction (groups of 32 CTAs, then the groups) runs beta_step.
 GPK_DEV void beta_step_s(SlotState& x, double rz_new, double zz, int k, double rel_tol, double* beta_hist,
@@ -259,6 +276,7 @@ GPK_DEV void beta_step_s(SlotState& x, double rz_new, double zz, int k, double r
   const long long base = static_cast<long long>(x.col) * max_iters + (k - 1);
   if (resid_hist) resid_hist[base] = pres;
   x.iters = k;
+  x.pres = pres;
   if (pres <= rel_tol * x.norm0 || rz_new == 0.0) {
     x.flag = kFlagConverged;
     x.beta = 0.0;
@@ -338,15 +356,12 @@ GPK_DEV int cswz(int kk) { return ((kk >> 4) & 3) * 4; }
 // One column group [s0, s0 + ns) of G2s (the launcher runs one launch per group; group
 // launches use disjoint counters and partial columns).
 template <bool VEC, int NT>
-__global__ void __launch_bounds__(kWT, 2)
-    g2s_dots_beta_kernel(const double* __restrict__ C, long long ldc, int ka, const double* __restrict__ W,
-                         long long ldw, int s0, int ns, int n, double* __restrict__ Z, const double* __restrict__ R,
-                         long long ldn, double sig2, double* __restrict__ prz, double* __restrict__ pzz) {
-  extern __shared__ __align__(16) double wsm[];
+GPK_DEV void g2s_group(int b, int G, const double* __restrict__ C, long long ldc, int ka, const double* W,
+                       long long ldw, int s0, int ns, int n, double* __restrict__ Z, const double* R, long long ldn,
+                       double sig2, double* __restrict__ prz, double* __restrict__ pzz, double* wsm,
+                       double (*srz)[kWS], double (*szz)[kWS]) {
   double* Cs = wsm;              // [kk][i ^ cswz(kk)], stride 64
   double* Ws = wsm + kWS * kSR;  // [s][kpos(kk)], stride 72
-  __shared__ double srz[8][kWS], szz[8][kWS];
-  const int G = gridDim.x, b = blockIdx.x;
   int r0, r1;
   rows_of(b, G, n, r0, r1);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, r = lane & 3, m = lane >> 2;
@@ -447,6 +462,16 @@ __global__ void __launch_bounds__(kWT, 2)
     prz[static_cast<long long>(s0 + tid) * G + b] = crun;
     pzz[static_cast<long long>(s0 + tid) * G + b] = zrun;
   }
+}
+
+template <bool VEC, int NT>
+__global__ void __launch_bounds__(kWT, 2)
+    g2s_dots_beta_kernel(const double* __restrict__ C, long long ldc, int ka, const double* __restrict__ W,
+                         long long ldw, int s0, int ns, int n, double* __restrict__ Z, const double* __restrict__ R,
+                         long long ldn, double sig2, double* __restrict__ prz, double* __restrict__ pzz) {
+  extern __shared__ __align__(16) double wsm[];
+  __shared__ double srz[8][kWS], szz[8][kWS];
+  g2s_group<VEC, NT>(blockIdx.x, gridDim.x, C, ldc, ka, W, ldw, s0, ns, n, Z, R, ldn, sig2, prz, pzz, wsm, srz, szz);
 }
 
 int wood_grid() {  // CTAs per SM: 2 (env GPK_WOOD_CPS=1 for A/B checks)
@@ -575,6 +600,220 @@ cudaError_t launch_cg_beta_p(double* P, const double* Z, int n, long long ldn, i
   cg_beta_p_kernel<<<dim3(bx, t), kWT, 0, st>>>(P, Z, n, ldn, ss, prz, pzz, wood_grid(), cnt, k, rel_tol, beta_hist,
                                                 resid_hist, max_iters, vmax, snap);
   return cudaGetLastError();
+}
+
+// ===========================================================================
+// The whole CG vector phase of one iteration as ONE cooperative launch (single rank,
+// Woodbury preconditioner; krylov.hpp:76-119 + preconditioners.hpp:114-118):
+//   1 pap partials over the CTA's rows      | grid barrier
+//   2 alpha of column s in CTA s mod G      | grid barrier
+//   3 x/r update fused into G1s (W = L^T r) | grid barrier
+//   4 G1s partial reduction -> W            | grid barrier
+//   5 G2s: z = (r - C W)/s2, r.z, z.z       | grid barrier
+//   6 beta of column s in CTA s mod G, the slot state (+ pinned host snapshot)
+//                                           | grid barrier
+//   7 p = z + beta p on the CTA's rows, |p| column maxima for the next fp16 pack
+// instead of five launches (pap+alpha, G1s, G1s reduce, G2s, beta+p) whose boundaries
+// drained the GPU between phases (C2: 66 us per iteration, the work itself ~15 us of L2
+// traffic).  Every phase keeps a fixed partition (rows_of over the G CTAs) and fixed-order
+// reductions, so a column's arithmetic never depends on the other columns (batched ==
+// independent, krylov.hpp:131-132) and reruns are bitwise reproducible.
+// ===========================================================================
+namespace cgrp = cooperative_groups;
+
+GPK_DEV void alpha_step_c(SlotState& x, double pap, int k, double* alpha_hist, int max_iters) {
+  if (x.flag != 0) {  // krylov.hpp:78-83 (cg_alpha_kernel's semantics)
+    x.alpha = 0.0;
+    return;
+  }
+  const double alpha = x.rz / pap;
+  x.alpha = alpha;
+  if (!isfinite(alpha) || alpha <= 0.0) {
+    x.status = kStatusAlpha;
+    x.bad = alpha;
+    x.iters = k;
+    x.flag = kFlagError;
+    x.alpha = 0.0;
+    return;
+  }
+  if (alpha_hist) alpha_hist[static_cast<long long>(x.col) * max_iters + (k - 1)] = alpha;
+}
+
+struct CoopArgs {
+  const double* L;
+  const double* Cm;
+  long long ldl, ldc;
+  int ka;
+  double *X, *R, *P, *Z;
+  const double* Y;
+  long long ldn;
+  int tb, n;
+  double sig2, psig2;
+  double *ppap, *pg1, *W, *prz, *pzz;
+  SlotState* ss;
+  int k;
+  double rel_tol;
+  double *ahist, *bhist, *rhist;
+  int max_iters;
+  unsigned long long* vmax;
+  SlotState* snap;
+};
+
+template <bool VEC>
+__global__ void __launch_bounds__(kWT, 2) cg_iter_coop_kernel(CoopArgs a) {
+  extern __shared__ __align__(16) double wsm[];
+  __shared__ double s_al[kWS];
+  __shared__ double srz[8][kWS], szz[8][kWS];
+  __shared__ double red8[8][32];
+  __shared__ double red[kWT / 32];
+  cgrp::grid_group grid = cgrp::this_grid();
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  int r0, r1;
+  rows_of(b, G, a.n, r0, r1);
+  // 1. p.(Kp + s2 p) over the CTA's rows: warp per column, lane-strided rows + butterfly
+  for (int s = w; s < a.tb; s += kWT / 32) {
+    const double* p = a.P + s * a.ldn;
+    const double* y = a.Y + s * a.ldn;
+    double acc = 0.0;
+    for (int i = r0 + lane; i < r1; i += 32) {
+      const double pv = p[i];
+      acc += pv * (y[i] + a.sig2 * pv);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) a.ppap[static_cast<long long>(s) * G + b] = acc;
+  }
+  grid.sync();
+  // 2. alpha (krylov.hpp:78-83); the fp16 pack's column maxima are re-armed here
+  for (int s = b; s < a.tb; s += G) {
+    double acc = 0.0;
+    for (int c = tid; c < G; c += kWT) acc += __ldcg(a.ppap + static_cast<long long>(s) * G + c);
+    const double pap = block_sum(acc, red);
+    if (tid == 0) {
+      SlotState x = a.ss[s];
+      alpha_step_c(x, pap, a.k, a.ahist, a.max_iters);
+      a.ss[s] = x;
+      if (a.vmax) a.vmax[s] = 0ull;
+    }
+  }
+  grid.sync();
+  // 3. x += alpha p, r -= alpha (Kp + s2 p) fused into G1s partials of W = L^T r
+  for (int s0 = 0; s0 < a.tb; s0 += kWS) {
+    const int nt = (min(kWS, a.tb - s0) + 7) / 8;
+    __syncthreads();
+#define GPK_G1C(NTV)                                                                                          \
+  case NTV:                                                                                                   \
+    g1s_group<true, VEC, NTV>(b, G, s0, a.L, a.ldl, a.ka, a.R, a.ldn, a.tb, a.n, a.pg1, a.X, a.P, a.Y, a.sig2, \
+                              a.ss, wsm, s_al);                                                               \
+    break;
+    switch (nt) { GPK_G1C(1) GPK_G1C(2) GPK_G1C(3) GPK_G1C(4) GPK_G1C(5) GPK_G1C(6) GPK_G1C(7) GPK_G1C(8) }
+#undef GPK_G1C
+  }
+  grid.sync();
+  // 4. W = sum of the G partials in fixed order
+  {
+    const long long tot = static_cast<long long>(a.ka) * a.tb, nch = (tot + 31) / 32;
+    for (long long c = b; c < nch; c += G) {
+      __syncthreads();
+      g1s_reduce_chunk(c, a.pg1, G, a.ka, a.tb, a.W, a.ka, red8);
+    }
+  }
+  grid.sync();
+  // 5. z = (r - C W) / s2 and the CTA's r.z / z.z partials
+  for (int s0 = 0; s0 < a.tb; s0 += kWS) {
+    const int ns = min(kWS, a.tb - s0), nt = (ns + 7) / 8;
+    __syncthreads();
+#define GPK_G2C(NTV)                                                                                            \
+  case NTV:                                                                                                     \
+    g2s_group<VEC, NTV>(b, G, a.Cm, a.ldc, a.ka, a.W, a.ka, s0, ns, a.n, a.Z, a.R, a.ldn, a.psig2, a.prz, a.pzz, \
+                        wsm, srz, szz);                                                                         \
+    break;
+    switch (nt) { GPK_G2C(1) GPK_G2C(2) GPK_G2C(3) GPK_G2C(4) GPK_G2C(5) GPK_G2C(6) GPK_G2C(7) GPK_G2C(8) }
+#undef GPK_G2C
+  }
+  grid.sync();
+  // 6. beta (krylov.hpp:96-119) and the slot state (+ the host's pinned snapshot)
+  for (int s = b; s < a.tb; s += G) {
+    double ar = 0.0, az = 0.0;
+    for (int c = tid; c < G; c += kWT) {
+      ar += __ldcg(a.prz + static_cast<long long>(s) * G + c);
+      az += __ldcg(a.pzz + static_cast<long long>(s) * G + c);
+    }
+    const double rz_new = block_sum(ar, red);
+    const double zz = block_sum(az, red);
+    if (tid == 0) {
+      SlotState x = a.ss[s];
+      beta_step_s(x, rz_new, zz, a.k, a.rel_tol, a.bhist, a.rhist, a.max_iters);
+      a.ss[s] = x;
+      if (a.snap) a.snap[s] = x;
+    }
+  }
+  grid.sync();
+  // 7. p = z + beta p on the CTA's rows (krylov.hpp:116) and |p| column maxima
+  for (int s = w; s < a.tb; s += kWT / 32) {
+    const SlotState* x = a.ss + s;
+    const bool live = __ldcg(&x->flag) == 0;
+    const double beta = __ldcg(&x->beta);
+    double* p = a.P + s * a.ldn;
+    const double* z = a.Z + s * a.ldn;
+    double mx = 0.0;
+    for (int i = r0 + lane; i < r1; i += 32) {
+      double pv = p[i];
+      if (live) {
+        pv = z[i] + beta * pv;
+        p[i] = pv;
+      }
+      mx = fmax(mx, fabs(pv));
+    }
+    if (a.vmax) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0 && mx > 0.0) atomicMax(a.vmax + s, static_cast<unsigned long long>(__double_as_longlong(mx)));
+    }
+  }
+}
+
+namespace {
+template <bool VEC>
+int coop_grid() {
+  static int g = [] {
+    cudaFuncSetAttribute(cg_iter_coop_kernel<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kWSmem));
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_iter_coop_kernel<VEC>, kWT, kWSmem);
+    return std::min(per, 2) * sm_count();
+  }();
+  return g;
+}
+}  // namespace
+
+bool cg_iter_coop_available() {
+  static bool ok = [] {
+    // opt-in (GPK_COOP=1): measured SLOWER than the five-launch path at C2 (0.102 vs 0.079 ms per
+    // iteration, profiles/r2_coop_vector_phase.txt): the warp-per-column phases and the five grid
+    // barriers of 296 CTAs cost more than the kernel boundaries they replace
+    const char* e = std::getenv("GPK_COOP");
+    if (!(e && e[0] == '1')) return false;
+    return coop_grid<true>() >= sm_count() && coop_grid<false>() >= sm_count();
+  }();
+  return ok;
+}
+
+cudaError_t launch_cg_iter_coop(const double* L, long long ldl, const double* Cm, long long ldc, int ka, double* X,
+                                double* R, double* P, double* Z, const double* Y, long long ldn, int tb, int n,
+                                double sig2, double psig2, double* ppap, double* pg1, double* W, double* prz,
+                                double* pzz, SlotState* ss, int k, double rel_tol, double* ahist, double* bhist,
+                                double* rhist, int max_iters, unsigned long long* vmax, SlotState* snap,
+                                cudaStream_t st) {
+  if (tb <= 0) return cudaSuccess;
+  CoopArgs a{L, Cm, ldl, ldc, ka, X, R, P, Z, Y, ldn, tb, n, sig2, psig2, ppap, pg1, W, prz, pzz, ss, k,
+             rel_tol, ahist, bhist, rhist, max_iters, vmax, snap};
+  const bool vec = aligned16(L) && aligned16(R) && aligned16(Cm) && aligned16(W) && ldl % 2 == 0 && ldn % 2 == 0 &&
+                   ldc % 2 == 0 && ka % 2 == 0;
+  void* args[] = {&a};
+  const int G = vec ? coop_grid<true>() : coop_grid<false>();
+  const void* fn = vec ? reinterpret_cast<const void*>(cg_iter_coop_kernel<true>)
+                       : reinterpret_cast<const void*>(cg_iter_coop_kernel<false>);
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kWT), args, kWSmem, st);
 }
 
 }  // namespace gpk

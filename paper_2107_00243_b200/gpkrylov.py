@@ -548,14 +548,17 @@ def make_probes(n: int, count: int, seed: int) -> ProbeBatch:
 # ---------------------------------------------------------------------------
 @dataclass
 class MllConfig:
-    """gp_likelihood.hpp:26-32 (+ backward: 'fused' bilinear derivative pass or 'faithful' per-RHS solves)."""
+    """gp_likelihood.hpp:26-32 (+ backward: 'fused' bilinear derivative pass, 'faithful' per-RHS
+    solves, or 'auto' = fused when every forward solve converged, else faithful)."""
     solver: CgConfig = field(default_factory=CgConfig)
     share_probes: bool = True
-    backward: str = "fused"
+    backward: str = "auto"
 
     def c(self, with_gradient):
-        return capi.gpk_mll_cfg(self.solver.c(), int(self.share_probes), int(with_gradient),
-                                0 if self.backward == "fused" else 1)
+        modes = {"fused": 0, "faithful": 1, "auto": 2}
+        if self.backward not in modes:
+            raise InputError(f"MllConfig: unknown backward mode {self.backward!r}")
+        return capi.gpk_mll_cfg(self.solver.c(), int(self.share_probes), int(with_gradient), modes[self.backward])
 
 
 @dataclass
@@ -581,6 +584,9 @@ class MllEvaluation:
     kernel_entries: int = 0
     mvm_flops: int = 0
     gpu_launches: int = 0
+    max_cg_rel_residual: float = 0.0
+    unconverged_columns: int = 0
+    backward_mode_used: str = ""
 
 
 def _result_struct(n_params, l):
@@ -605,7 +611,9 @@ def _to_eval(r, arrs, seed, with_gradient):
                          quad=r.quad, refine_passes=r.refine_passes, max_true_rel_residual=r.max_true_rel_residual,
                          seconds_solve=r.seconds_solve, seconds_backward=r.seconds_backward,
                          seconds_total=r.seconds_total, kernel_entries=r.kernel_entries, mvm_flops=r.mvm_flops,
-                         gpu_launches=r.gpu_launches)
+                         gpu_launches=r.gpu_launches, max_cg_rel_residual=r.max_cg_rel_residual,
+                         unconverged_columns=r.unconverged_columns,
+                         backward_mode_used=("fused", "faithful")[r.backward_mode_used] if with_gradient else "")
 
 
 def evaluate_mll(y, k: KernelOperator, prec, batch: ProbeBatch, cfg: MllConfig, with_gradient: bool = True):

@@ -1,0 +1,153 @@
+"""Parity at the BASELINE configurations themselves (C2-C5), against the oracle fixtures of
+tests/golden/make_golden_big.py, through the C-ABI (north-star gates: identical pivot
+sequence; solves to relative residual 1e-6; log-det, mLL and each gradient component within
+1e-4 relative).
+
+* C2 evaluate_mll (gp_likelihood.hpp:51-103) at preconditioner ranks 0 / 100 / 500, in the
+  bench's default mode (tf32x3 operator + fused bilinear backward) and the reference-faithful
+  fp64 mode (fp64 operator + (d+1) l backward solves), against the reference algorithm run in
+  full by the oracle (MatrixFree operator, reference default solver: max_iters 200, tol 1e-6).
+* The pivot sequence of the pivoted Cholesky (preconditioners.hpp:236-264) at C2-C5.
+* Rows of the fused kernel MVM (kernels.hpp:184-195) at the C2-C5 shapes.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2107_00243_b200 as gk
+from paper_2107_00243_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+FAMS = ["rbf", "matern12", "matern32", "matern52"]
+
+
+def checksum(x):
+    x = np.asarray(x, dtype=np.float64).ravel(order="C")
+    return float(np.dot(x, np.cos(np.arange(x.size, dtype=np.float64) * 1e-3)))
+
+
+def operator(w, x, precision="fp64"):
+    hp = gk.Hyperparameters.from_raw(w.d, w.outputscale, lengthscales=w.lengthscales, noise=w.noise)
+    return gk.KernelOperator(gk.KernelSpec(FAMS[w.family]), x, hp, precision=precision)
+
+
+# ---------------------------------------------------------------------------
+# C2 evaluate_mll (the benchmarked evaluation)
+# ---------------------------------------------------------------------------
+_C2 = {}
+
+
+def c2_case(rank):
+    if rank not in _C2:
+        g = json.load(open(os.path.join(GOLD, f"c2_oracle_rank{rank}.json")))
+        w = workloads.config("C2", rank=rank)
+        x, y = workloads.generate(w)
+        assert checksum(x) == pytest.approx(g["x_checksum"], rel=1e-12)
+        assert checksum(y) == pytest.approx(g["y_checksum"], rel=1e-12)
+        _C2[rank] = (g, w, x, y)
+    return _C2[rank]
+
+
+@pytest.mark.parametrize("rank", [0, 100, 500])
+@pytest.mark.parametrize("precision,backward", [("tf32x3", "fused"), ("fp64", "faithful"), ("fp64", "fused"),
+                                                ("tf32x3", "faithful")])
+def test_c2_evaluate_mll_matches_oracle(rank, precision, backward):
+    g, w, x, y = c2_case(rank)
+    op = operator(w, x)
+    pc = gk.pivoted_cholesky_with_derivatives(op, rank)
+    assert pc.pivots() == g["pivots"]  # identical pivot sequence
+    z = gk.make_probes(w.n, w.probes, g["probe_seed"])
+    cfg = gk.MllConfig(gk.CgConfig(w.max_iters, w.rel_tol, False, precision, 2), True, backward)
+    r = gk.evaluate_mll(y, op, pc, z, cfg)
+    # every solve converged (the oracle's did) and, in the reduced-precision operator modes,
+    # the fp64-audited true preconditioned residual of every column meets the tolerance
+    assert r.unconverged_columns == 0
+    assert max(g["forward_cg_iterations"]) < w.max_iters
+    if precision != "fp64":
+        assert 0.0 <= r.max_true_rel_residual <= w.rel_tol
+    assert r.max_cg_rel_residual <= w.rel_tol
+    # north-star gate: mLL, log-det and every gradient component within 1e-4 relative
+    assert r.value == pytest.approx(g["value"], rel=1e-4)
+    assert r.logdet == pytest.approx(g["logdet"], rel=1e-4)
+    np.testing.assert_allclose(r.gradient, g["gradient"], rtol=1e-4, atol=0)
+    np.testing.assert_allclose(r.forward_gammas, g["forward_gammas"], rtol=1e-4,
+                               atol=1e-4 * np.abs(g["forward_gammas"]).max())
+    assert abs(np.mean(r.forward_cg_iterations) - np.mean(g["forward_cg_iterations"])) <= 0.1 * np.mean(
+        g["forward_cg_iterations"])
+    if backward == "faithful":
+        # per-probe backward gammas of the reference-faithful mode (trace_estimation.hpp:190-224)
+        bg = np.array(g["backward_gammas"])
+        np.testing.assert_allclose(r.backward_gammas, bg, rtol=1e-3, atol=1e-4 * np.abs(bg).max())
+        assert abs(r.total_cg_iterations - g["total_cg_iterations"]) <= 0.1 * g["total_cg_iterations"]
+
+
+@pytest.mark.parametrize("precision", ["fp64", "tf32x3"])
+def test_c2_solve_matches_oracle(precision):
+    """u = K_hat^{-1} y at C2 (rank 100) against the oracle's solution: both stop at relative
+    preconditioned residual 1e-6 (krylov.hpp:106), so they agree to that level times the
+    conditioning of the preconditioned system."""
+    g, w, x, y = c2_case(100)
+    u_ref = np.load(os.path.join(GOLD, "c2_oracle_rank100_u.npy"))
+    op = operator(w, x)
+    pc = gk.pivoted_cholesky(op, 100)
+    r = gk.pcg_solve(op, y, pc, gk.CgConfig(w.max_iters, w.rel_tol, False, precision, 2))
+    assert r.converged
+    # the reduced-precision operator costs a few more iterations (~5%)
+    assert abs(r.iterations_used - g["solve_iterations"]) <= max(2, g["solve_iterations"] // 10)
+    assert np.linalg.norm(r.solution - u_ref) / np.linalg.norm(u_ref) < 1e-4
+
+
+# ---------------------------------------------------------------------------
+# pivot sequences at C2-C5
+# ---------------------------------------------------------------------------
+PIVOT_KEYS = ["C2_100", "C2_500", "C3_200", "C4_500", "C5_500"]
+
+
+@pytest.mark.parametrize("key", PIVOT_KEYS)
+def test_pivots_identical_at_baseline_configs(key):
+    g = json.load(open(os.path.join(GOLD, "big_pivots.json")))[key]
+    w = workloads.config(g["workload"], rank=g["rank"])
+    x, _ = workloads.generate(w)
+    assert checksum(x) == pytest.approx(g["x_checksum"], rel=1e-12)
+    op = operator(w, x)
+    pc, rem = gk.pivoted_cholesky(op, g["rank"], want_remaining=True)
+    assert pc.rank() == len(g["pivots"])
+    assert pc.pivots() == g["pivots"]
+    assert float(rem.max()) == pytest.approx(g["remaining_max"], rel=1e-8)
+
+
+# ---------------------------------------------------------------------------
+# fused MVM rows at the C2-C5 shapes
+# ---------------------------------------------------------------------------
+_MVM = {}
+
+
+def mvm_fixture():
+    if not _MVM:
+        f = np.load(os.path.join(GOLD, "big_mvm_rows.npz"))
+        _MVM.update({k: f[k] for k in f.files})
+        _MVM["meta"] = json.loads(str(f["meta"]))
+    return _MVM
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("precision", ["tf32x3", "fp64"])
+def test_mvm_rows_at_baseline_configs(name, precision):
+    fx = mvm_fixture()
+    meta = fx["meta"][name]
+    w = workloads.config(name)
+    x, _ = workloads.generate(w)
+    assert checksum(x) == pytest.approx(meta["x_checksum"], rel=1e-12)
+    t = meta["t"]
+    v = np.asfortranarray(np.random.default_rng(777 + w.data_seed).standard_normal((w.n, t)))
+    assert checksum(v[:4096]) == pytest.approx(meta["v_checksum"], rel=1e-12)
+    rows, want = fx[f"{name}_rows"], fx[f"{name}_out"]
+    op = operator(w, x, precision=precision)
+    got = op.apply(v, precision=precision)[rows]
+    tol = 1e-12 if precision == "fp64" else 3e-6
+    for c in range(t):
+        err = np.linalg.norm(got[:, c] - want[:, c]) / np.linalg.norm(want[:, c])
+        assert err < tol, (c, err)
