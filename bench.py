@@ -41,6 +41,14 @@ METRIC = "s per mLL+gradient eval"
 UNIT = "s/eval"
 
 
+def fp64_peak():
+    """Measured DMMA peak (tools/fp64_peak.py -> profiles/fp64_peak.json), else B200's nominal 40."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_tflops"]), "measured"
+    except Exception:
+        return 40.0, "nominal B200 FP64 tensor (no measurement committed)"
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
@@ -293,7 +301,7 @@ def run_ours(args, comm):
     check(lib.gpk_profile_read(ctx, 2, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en)))
     f64 = {"ms": ms.value, "launches": cnt.value, "flops": fl.value, "entries": en.value}
     check(lib.gpk_profile_read(ctx, 3, C.byref(ms), C.byref(cnt), C.byref(fl), C.byref(en)))
-    vec = {"ms": ms.value, "launches": cnt.value, "bytes": fl.value}
+    vec = {"ms": ms.value, "launches": cnt.value, "bytes": fl.value, "cols": en.value}
     check(lib.gpk_profile_enable(ctx, 0))
     var, maxnorm = C.c_int(), C.c_double()
     check(lib.gpk_get_mvm_variant(ctx, C.byref(var), C.byref(maxnorm)))
@@ -617,9 +625,19 @@ def main():
         # column + L and C per iteration (the operands are L2-resident at C2: latency-bound there)
         hbm = float(peaks.get("hbm_gbs", 6538.3))
         ach = vec["bytes"] / (vec["ms"] / 1e3) / 1e9
+        # the Woodbury products G1 = L^T r and G2 = C W are 4 n k t fp64 flops per iteration on
+        # the DMMA pipe; at large k they bind before HBM does (C4: 44 GFLOP vs 5.3 GB)
+        f64p, f64src = fp64_peak()
+        wflops = 4.0 * w.n * w.rank * vec.get("cols", 0.0)
+        t_hbm = vec["bytes"] / (hbm * 1e9)
+        t_f64 = wflops / (f64p * 1e12)
         roofline["cg_vector_phase"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                                        "frac": ach / hbm, "avg_ms_per_iteration": vec["ms"] / vec["launches"],
                                        "bytes_per_iteration": vec["bytes"] / vec["launches"],
+                                       "woodbury_fp64_flops_per_iteration": wflops / vec["launches"],
+                                       "fp64_tensor_peak_tflops": f64p, "fp64_peak_source": f64src,
+                                       "binding": "fp64_tensor" if t_f64 > t_hbm else "hbm",
+                                       "frac_of_binding_roofline": max(t_hbm, t_f64) / (vec["ms"] / 1e3),
                                        "iterations_per_step": vec["launches"] / max(args.steps, 1),
                                        "share_of_step": (vec["ms"] / 1e3) / max(sum(r["times"]), 1e-12)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

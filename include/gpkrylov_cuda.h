@@ -75,7 +75,9 @@ typedef struct {
   int backward_mode;   /* 0: fused bilinear derivative pass over the forward solves
                           1: reference-faithful: mBCG over the (d+1) l right-hand sides dK_w z_i
                           2: auto (default): fused when every forward solve converged, else faithful
-                             (the fused identity needs converged probe solves) */
+                             (the fused identity needs converged probe solves)
+                          3: fused + per-probe backward gammas s_i' dK_w z_i - z_i' P^-1 dP_w z_i
+                             from (d+1) derivative MVMs of the probe block (no backward solves) */
 } gpk_mll_cfg;
 
 /* gp_likelihood.hpp:35-46 MllEvaluation, caller-allocated arrays. */

@@ -134,6 +134,21 @@ class ExtensionMissing(RuntimeError):
     pass
 
 
+class _Stubbed:
+    """An experiment build (GPK_LIB_PATH) missing some exports: the missing names raise
+    ExtensionMissing naming the symbol at the call, every other attribute is the library's."""
+
+    def __init__(self, handle, missing):
+        self._h, self._missing = handle, set(missing)
+
+    def __getattr__(self, name):
+        if name in self._missing:
+            def stub(*_a, **_k):
+                raise ExtensionMissing(f"{LIB_PATH} does not export {name}")
+            return stub
+        return getattr(self._h, name)
+
+
 _lib = None
 
 
@@ -145,14 +160,21 @@ def lib():
             raise ExtensionMissing(
                 f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
         handle = C.CDLL(LIB_PATH)
+        missing = []
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(handle, name, None)
             if fn is None:
-                if os.environ.get("GPK_LIB_PATH"):  # an older experiment build: bind what it has
-                    continue
-                raise ExtensionMissing(f"{LIB_PATH} does not export {name}")
+                if not os.environ.get("GPK_LIB_PATH"):
+                    raise ExtensionMissing(f"{LIB_PATH} does not export {name}")
+                missing.append(name)  # an older experiment build: bound to a stub that raises
+                continue
             fn.restype = res
             fn.argtypes = args
+        if missing:
+            import warnings
+
+            warnings.warn(f"GPK_LIB_PATH={LIB_PATH} lacks {len(missing)} exports: {', '.join(missing)}")
+            handle = _Stubbed(handle, missing)
         _lib = handle
     return _lib
 

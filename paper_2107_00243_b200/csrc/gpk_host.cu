@@ -450,6 +450,14 @@ struct gpk_ctx {
   int k = 0;
   double pnoise = 0.0, plogdet = 0.0;
   DBuf<double> L, C, dL;
+  // L, C, dL storage: unsharded, all n rows (leading dimension n); row-sharded (world > 1),
+  // the own rows [r0, r1) followed by the k pivot rows (leading dimension nl + k) -- the
+  // preconditioner is built and stored per rank, never replicated
+  bool pshard = false;
+  long long ldP = 0;
+  double* Lloc() const { return pshard ? L.p : L.p + r0; }
+  double* Cloc() const { return pshard ? C.p : C.p + r0; }
+  double* dLloc() const { return pshard ? dL.p : dL.p + r0; }
   std::vector<long long> pivots;
   bool have_dl = false;
   std::vector<double> trace_det;  // tr(P^-1 dP_w), w = 0..d+1
@@ -523,6 +531,14 @@ struct gpk_ctx {
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       return 0;
     return sms;
+  }();
+  // TEST HOOK (env GPK_TCG_CTAS=c): cap the persistent MVM grid at c CTAs without changing the
+  // unit decomposition (splits_for_tcg keeps the SM count), so every CTA runs several units --
+  // row-block changes and same-row split changes -- with results bitwise those of the full grid
+  int tcg_grid_cap = [] {
+    const char* e = std::getenv("GPK_TCG_CTAS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 0;
   }();
   int tc_flush = [] {   // j-tiles per TMEM accumulation group (env GPK_TC_FLUSH, default 2)
     const char* e = std::getenv("GPK_TC_FLUSH");
@@ -750,13 +766,13 @@ struct gpk_ctx {
                  1, "pack_x");
     gram_ok = false;
     tcg_direct = false;
-    // Gram variant: RBF / Matern-3/2 / Matern-5/2, d <= 32, and centred pre-scaled
+    // Gram variant: RBF / Matern-3/2 / Matern-5/2, d <= 30, and centred pre-scaled
     // coordinates small enough that the expanded-distance cancellation stays at the
     // fp32 level (max |x~|^2 <= kGramMaxNorm; see gpk_mvm_tcg.cuh).
-    if (mvm_variant != GPK_MVM_DIRECT && family != gpk::kMatern12 && d <= 32) {
-      Xgh.ensure(static_cast<size_t>(n_pad) * 32);
-      Xgl.ensure(static_cast<size_t>(n_pad) * 32);
-      Xgn.ensure(n_pad);
+    if (mvm_variant != GPK_MVM_DIRECT && family != gpk::kMatern12 && d <= gpk::kGramMaxDim) {
+      Xgh.ensure(static_cast<size_t>(n_pad) * 64);  // B-side then A-side augmented images
+      Xgl.ensure(static_cast<size_t>(n_pad) * 64);
+      Xgn.ensure(static_cast<size_t>(n_pad) + n_pad / 64);  // norms, then per-j-tile maxima
       Xgmu.ensure(d);
       check_launch(gpk::launch_gram_pack(X.p, n, n, d, n_pad, ls_dev.p, gpk::prescale_c(family), Xgmu.p, Xgh.p, Xgl.p,
                                          Xgn.p, st),
@@ -886,7 +902,7 @@ struct gpk_ctx {
           const int per64 = (nt64 + sg - 1) / sg;
           sp = (nt64 + per64 - 1) / per64;
           a.jtiles_per_split = per64;
-          a.ctas = tcg_ctas;
+          a.ctas = (tcg_grid_cap > 0 && tcg_ctas > 0) ? std::min(tcg_ctas, tcg_grid_cap) : tcg_ctas;
           a.flush = tc_flush;  // 64-wide tiles: 128 entries per fp32 TMEM accumulation at the default 2
         } else {
           const int npad = gpk::tc_npad(tc);
@@ -1005,9 +1021,9 @@ struct gpk_ctx {
     w_g1.ensure(gpk::g1_workspace(nl, k, t));
     w_W.ensure(static_cast<size_t>(k) * t);
     w_T.ensure(static_cast<size_t>(t) * ldn);
-    check_launch(gpk::launch_g1(L.p + r0, n, k, R, ldn, t, nl, w_g1.p, w_W.p, k, st), 2, "g1");
+    check_launch(gpk::launch_g1(Lloc(), ldP, k, R, ldn, t, nl, w_g1.p, w_W.p, k, st), 2, "g1");
     allreduce_sum(w_W.p, static_cast<long long>(k) * t);
-    check_launch(gpk::launch_woodbury_apply(C.p + r0, n, k, w_W.p, k, R, ldn, pnoise, t, nl, Z, ldn, st), 1,
+    check_launch(gpk::launch_woodbury_apply(Cloc(), ldP, k, w_W.p, k, R, ldn, pnoise, t, nl, Z, ldn, st), 1,
                  "woodbury");
   }
 
@@ -1540,7 +1556,7 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
   c->check_launch(gpk::launch_gather_cols(dZ + r0, ldz, nullptr, 1.0, nl, l, B.p + ldn, ldn, c->st), 1, "gather");
   // backward preconditioner terms on the side stream, overlapped with the forward solve
   DBuf<double> Zc, dterms;  // allocated on st: read there after the join
-  require(cfg->backward_mode >= 0 && cfg->backward_mode <= 2, "MllConfig: unknown backward mode");
+  require(cfg->backward_mode >= 0 && cfg->backward_mode <= 3, "MllConfig: unknown backward mode");
   const bool side_terms = cfg->with_gradient && cfg->share_probes && cfg->backward_mode != 1 && c->use_side &&
                           c->pkind == 2 && c->k > 0 && c->world == 1 && c->have_dl;
   if (cfg->with_gradient) Zc.ensure(static_cast<size_t>(l) * ldn);
@@ -1703,8 +1719,8 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         DBuf<double> A, part;
         A.ensure(static_cast<size_t>(2) * l * k);
         part.ensure(gpk::g1_workspace(nl, k, l));
-        c->check_launch(gpk::launch_g1(c->L.p + r0, n, k, Q.p, ldn, l, nl, part.p, A.p, k, c->st), 2, "g1");
-        c->check_launch(gpk::launch_g1(c->L.p + r0, n, k, Zc.p, ldn, l, nl, part.p, A.p + static_cast<size_t>(l) * k,
+        c->check_launch(gpk::launch_g1(c->Lloc(), c->ldP, k, Q.p, ldn, l, nl, part.p, A.p, k, c->st), 2, "g1");
+        c->check_launch(gpk::launch_g1(c->Lloc(), c->ldP, k, Zc.p, ldn, l, nl, part.p, A.p + static_cast<size_t>(l) * k,
                                        k, c->st),
                         2, "g1");
         c->allreduce_sum(A.p, 2LL * l * k);
@@ -1714,8 +1730,8 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         Bq.ensure(static_cast<size_t>(l) * kw);
         Bz.ensure(static_cast<size_t>(l) * kw);
         partw.ensure(gpk::g1_workspace(nl, kw, l));
-        c->check_launch(gpk::launch_g1(c->dL.p + r0, n, kw, Q.p, ldn, l, nl, partw.p, Bq.p, kw, c->st), 2, "g1");
-        c->check_launch(gpk::launch_g1(c->dL.p + r0, n, kw, Zc.p, ldn, l, nl, partw.p, Bz.p, kw, c->st), 2, "g1");
+        c->check_launch(gpk::launch_g1(c->dLloc(), c->ldP, kw, Q.p, ldn, l, nl, partw.p, Bq.p, kw, c->st), 2, "g1");
+        c->check_launch(gpk::launch_g1(c->dLloc(), c->ldP, kw, Zc.p, ldn, l, nl, partw.p, Bz.p, kw, c->st), 2, "g1");
         c->allreduce_sum(Bq.p, static_cast<long long>(l) * kw);
         c->allreduce_sum(Bz.p, static_cast<long long>(l) * kw);
         dtw.ensure(static_cast<size_t>(d + 1) * l);
@@ -1774,7 +1790,8 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
     // forward column hit max_iters the reference's truncated estimator (per-RHS solves) is
     // reproduced instead (C1 as configured: the fused gradient's truncation error is ~3x the
     // faithful one, profiles/r2_c1_fused_truncation.txt)
-    const bool fused_bwd = cfg->backward_mode == 0 || (cfg->backward_mode == 2 && cg.unconverged() == 0);
+    const bool fused_bwd =
+        cfg->backward_mode == 0 || cfg->backward_mode == 3 || (cfg->backward_mode == 2 && cg.unconverged() == 0);
     res->backward_mode_used = fused_bwd ? 0 : 1;
     if (fused_bwd) {
       // fused bilinear derivative pass over all n^2 pairs
@@ -1856,8 +1873,21 @@ void evaluate_impl(gpk_ctx* c, const double* dy, const double* dZ, int64_t ldz, 
         for (int i = 0; i < l; ++i) tsum += tw[w][i];
         const double num = mix[w] - tdet[w] + static_cast<double>(n) / static_cast<double>(l) * tsum;
         res->gradient[w] = 0.5 * num * (w == 0 ? c->o : c->ls[w - 1]);
-        if (res->backward_gammas)
+        if (res->backward_gammas && cfg->backward_mode != 3)
           for (int i = 0; i < l; ++i) res->backward_gammas[static_cast<size_t>(w) * l + i] = std::nan("");
+      }
+      if (res->backward_gammas && cfg->backward_mode == 3) {
+        // per-probe backward gammas without the (d+1) l solves: z_i' K^-1 dK_w z_i = s_i' (dK_w z_i)
+        // (K_hat^-1 symmetric, s_i the converged probe solves), one derivative MVM of the l
+        // probes per parameter; gamma_i = s_i' dK_w z_i - z_i' P^-1 dP_w z_i
+        // (trace_estimation.hpp:216-218)
+        DBuf<double> RHw;
+        RHw.ensure(static_cast<size_t>(l) * ldn);
+        for (int w = 0; w <= d; ++w) {
+          c->apply_kernel(Zc.p, ldn, l, RHw.p, ldn, fp64, w);
+          const std::vector<double> zs = c->col_dots(Sb, RHw.p, l, ldn);
+          for (int i = 0; i < l; ++i) res->backward_gammas[static_cast<size_t>(w) * l + i] = zs[i] - tw[w][i];
+        }
       }
     } else {
       // reference-faithful: mBCG over the (d+1) l right-hand sides dK_w z_i (trace_estimation.hpp:209)
@@ -2251,11 +2281,15 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
     c->pkind = 0;
     c->have_dl = false;
     c->pivots.clear();
+    const bool shard = c->world > 1;
+    const int nrow = shard ? c->nl : n;  // rows of the diagonal / factor this rank computes
+    c->pshard = shard;
+    c->ldP = shard ? static_cast<long long>(c->nl) + rank : n;  // sharded: own rows, then the pivot rows
     DBuf<double> dg, col;
-    dg.ensure(n);
+    dg.ensure(nrow);
     col.ensure(n);
-    c->L.ensure(static_cast<size_t>(n) * std::max(rank, 1));
-    const long long cnt = n;
+    c->L.ensure(static_cast<size_t>(c->ldP) * std::max(rank, 1));
+    const long long cnt = nrow;
     fill_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, c->st>>>(dg.p, cnt, c->o * c->o);  // :230-233
     c->check_launch(cudaGetLastError(), 1, "fill");
     const double kmax = c->o * c->o;
@@ -2265,7 +2299,64 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
     // the whole factorisation is enqueued at once; the pivot (argmax, lowest index on
     // ties) and the stopping rules (:250-253) live in a device-resident state
     int step = 0;
-    if (rank > 0 && !(kmax <= diag_tol)) {  // step 0: diagonal o^2, pivot 0
+    if (shard && rank > 0 && !(kmax <= diag_tol)) {
+      // row-sharded: per-step kernels on the own rows, candidates and pivot rows all-gathered
+      // (gpk_pchol.cu); no host round trip until the end
+      DBuf<gpk::PivotState> ps;
+      DBuf<long long> dpiv;
+      DBuf<double> lp, cand, cands, rows, rowsr;
+      ps.ensure(1);
+      dpiv.ensure(rank);
+      lp.ensure(rank);
+      cand.ensure(2);
+      cands.ensure(2 * static_cast<size_t>(c->world));
+      rows.ensure(rank);
+      rowsr.ensure(static_cast<size_t>(rank) * c->world);
+      gpk::PivotState h0{};
+      h0.dp = kmax;
+      h0.p = 0;
+      c->h2d(ps.p, &h0, sizeof(h0));
+      const int grid = gpk::pchol_shard_grid(c->nl);
+      c->w_argval.ensure(grid);
+      c->w_argidx.ensure(grid);
+      for (int st_ = 0; st_ < rank; ++st_) {
+        c->check_launch(gpk::launch_pchol_shard_step(c->family, c->sx.p, c->sq.p, n, c->d, c->o2, c->L.p, c->ldP,
+                                                     c->r0, c->nl, st_, lp.p, ps.p, dg.p, c->w_argval.p,
+                                                     c->w_argidx.p, grid, cand.p, c->st),
+                        2, "pchol_shard_step");
+        c->comm->allgather(cand.p, cands.p, 2 * sizeof(double), c->st);
+        c->check_launch(gpk::launch_pchol_shard_select(cands.p, c->world, st_, diag_tol, kmax, ps.p, dpiv.p, c->L.p,
+                                                       c->ldP, c->r0, c->nl, rank, rows.p, c->st),
+                        2, "pchol_shard_select");
+        if (st_ + 1 < rank) {
+          c->comm->allgather(rows.p, rowsr.p, sizeof(double) * rank, c->st);
+          c->check_launch(gpk::launch_pchol_shard_rowtake(rowsr.p, c->world, rank, c->d_r0.p, c->d_rows.p, ps.p, lp.p,
+                                                          c->st),
+                          1, "pchol_shard_rowtake");
+        }
+      }
+      gpk::PivotState hs{};
+      c->d2h(&hs, ps.p, sizeof(hs));
+      step = hs.done;
+      if (hs.negative)
+        fail(GPK_NUMERICAL_ERROR, "pivoted_cholesky: negative pivot " + num(hs.dp) + " at step " +
+                                      std::to_string(step) + "; matrix not PSD");
+      c->pivots.resize(step);
+      if (step > 0) c->d2h(c->pivots.data(), dpiv.p, sizeof(long long) * step);
+      // the pivot rows L[p_q, :] (owned by one rank each) appended as rows nl .. nl + k - 1
+      if (step > 0) {
+        DBuf<double> pr, prr;
+        pr.ensure(static_cast<size_t>(rank) * rank);
+        prr.ensure(static_cast<size_t>(rank) * rank * c->world);
+        c->check_launch(gpk::launch_pchol_pivot_rows(0, c->L.p, pr.p, c->ldP, c->r0, c->nl, rank, dpiv.p, c->world,
+                                                     c->d_r0.p, c->d_rows.p, c->st),
+                        1, "pivot_rows");
+        c->comm->allgather(pr.p, prr.p, sizeof(double) * rank * rank, c->st);
+        c->check_launch(gpk::launch_pchol_pivot_rows(1, prr.p, c->L.p, c->ldP, c->r0, c->nl, rank, dpiv.p, c->world,
+                                                     c->d_r0.p, c->d_rows.p, c->st),
+                        1, "pivot_rows");
+      }
+    } else if (!shard && rank > 0 && !(kmax <= diag_tol)) {  // step 0: diagonal o^2, pivot 0
       DBuf<gpk::PivotState> ps;
       DBuf<long long> dpiv;
       ps.ensure(1);
@@ -2303,7 +2394,16 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
     if (achieved) *achieved = step;
     if (pivots_out)
       for (int s = 0; s < step; ++s) pivots_out[s] = c->pivots[s];
-    if (remaining_diag) c->d2h(remaining_diag, dg.p, sizeof(double) * n);
+    if (remaining_diag) {
+      if (shard) {
+        DBuf<double> full;
+        full.ensure(n);
+        c->allgather_cols(dg.p, nrow, 1, full.p, n);
+        c->d2h(remaining_diag, full.p, sizeof(double) * n);
+      } else {
+        c->d2h(remaining_diag, dg.p, sizeof(double) * n);
+      }
+    }
     // DiagPlusLowRank (:84-95): inner = L'L + s2 I, Cholesky inner = R R', C = L inner^{-1}
     // = (L R^-T) R^-1, log det P (:127-133) -- k x k work on the device (cuBLAS/cuSOLVER)
     c->pnoise = noise;
@@ -2316,7 +2416,8 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
       G.ensure(static_cast<size_t>(k) * k);
       info.ensure(1);
       const double one = 1.0, zero = 0.0;
-      CB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, k, n, &one, c->L.p, n, &zero, G.p, k));
+      CB(cublasDsyrk(c->blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, k, nrow, &one, c->L.p, c->ldP, &zero, G.p, k));
+      if (shard) c->allreduce_sum(G.p, static_cast<long long>(k) * k);  // L'L over all rows, rank order
       add_diag_kernel<<<(k + 255) / 256, 256, 0, c->st>>>(G.p, k, noise);
       c->check_launch(cudaGetLastError(), 2, "gram");
       int lwork = 0;
@@ -2335,12 +2436,13 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
       double sl = 0.0;
       for (int a = 0; a < k; ++a) sl += std::log(diag[a]);
       ld += 2.0 * sl - static_cast<double>(k) * std::log(noise);
-      c->C.ensure(static_cast<size_t>(n) * k);
-      CK(cudaMemcpyAsync(c->C.p, c->L.p, sizeof(double) * static_cast<size_t>(n) * k, cudaMemcpyDeviceToDevice, c->st));
-      CB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, n, k, &one,
-                     G.p, k, c->C.p, n));
-      CB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n, k, &one,
-                     G.p, k, c->C.p, n));
+      c->C.ensure(static_cast<size_t>(c->ldP) * k);
+      CK(cudaMemcpyAsync(c->C.p, c->L.p, sizeof(double) * static_cast<size_t>(c->ldP) * k, cudaMemcpyDeviceToDevice,
+                         c->st));
+      CB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, nrow, k,
+                     &one, G.p, k, c->C.p, c->ldP));
+      CB(cublasDtrsm(c->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, nrow, k,
+                     &one, G.p, k, c->C.p, c->ldP));
       c->launches += 4;
       // G and work are released stream-ordered; C is consumed on the same stream
     }
@@ -2350,7 +2452,10 @@ gpk_status gpk_pivoted_cholesky(gpk_ctx* ctx, int rank, double diag_tol, double 
     c->trace_det.assign(c->d + 2, 0.0);
     c->trace_pending = false;  // a new preconditioner: no derivative traces pending
     double cl = 0.0;
-    if (k > 0) {
+    if (k > 0 && shard) {
+      const std::vector<double> cd = c->col_dots(c->C.p, c->L.p, k, c->ldP);  // own rows, rank-order sum
+      for (int q = 0; q < k; ++q) cl += cd[q];
+    } else if (k > 0) {
       const int nrb = gpk::num_chunks(n * k);
       DBuf<double> part, outv;
       part.ensure(nrb);
@@ -2376,12 +2481,19 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
             "pivoted_cholesky_deriv_factors: preconditioner has no pivot record");
     c->have_dl = false;
     if (k > 0) {
-      c->dL.ensure(static_cast<size_t>(nw) * n * k);
+      // rows of the recursion: all n (unsharded), or -- row-sharded -- the own rows followed by
+      // the k pivot rows (the only rows another row's recursion reads), so every rank builds
+      // the factors of exactly the rows it owns: the reference's algorithm on that row set
+      const bool shard = c->pshard;
+      const int N = shard ? static_cast<int>(c->ldP) : n;
+      DBuf<double> xs_e, x_e, sq_e;
+      DBuf<long long> piv_e;
+      c->dL.ensure(static_cast<size_t>(nw) * N * k);
       c->w_trace.ensure(nw);
       // the build runs on the side stream st2 (fork after L, pivots and dL's allocation on st);
-      // its scratch is allocated and released on st2
+      // its scratch is allocated and released on st2 (sharded: on st, its traces are all-reduced)
       cudaStream_t ds = c->st;
-      if (c->use_side) {
+      if (c->use_side && !shard) {
         c->ensure_side();
         ds = c->st2;
         CK(cudaEventRecord(c->ev_fork, c->st));
@@ -2410,14 +2522,35 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
       // strided-batched GEMMs over the parameters, the recursion inside the block one kernel per column
       // (same formula as preconditioners.hpp:283-290, summation regrouped by block).
       constexpr int kB = 32;
-      const long long wstride = static_cast<long long>(n) * k;
+      const long long wstride = static_cast<long long>(N) * k;
       DBuf<double> DC, Lp, dLp;
       DBuf<long long> dpiv;
-      DC.ensure(static_cast<size_t>(nw) * n * kB);
+      DC.ensure(static_cast<size_t>(nw) * N * kB);
       Lp.ensure(static_cast<size_t>(k) * kB);
       dLp.ensure(static_cast<size_t>(nw) * k * kB);
       dpiv.ensure(k);
       CK(cudaMemcpyAsync(dpiv.p, c->pivots.data(), sizeof(long long) * k, cudaMemcpyHostToDevice, ds));
+      const double* sxp = c->sx.p;
+      const double* xp = c->X.p;
+      const double* sqp = c->sq.p;
+      const long long* pivp = dpiv.p;
+      if (shard) {  // coordinates of the extended rows; pivot q is row nl + q
+        xs_e.ensure(static_cast<size_t>(c->d) * N);
+        x_e.ensure(static_cast<size_t>(c->d) * N);
+        sq_e.ensure(N);
+        piv_e.ensure(k);
+        c->check_launch(gpk::launch_gather_ext_rows(c->sx.p, n, c->d, c->r0, c->nl, dpiv.p, k, xs_e.p, N, ds), 1,
+                        "ext_rows");
+        c->check_launch(gpk::launch_gather_ext_rows(c->X.p, n, c->d, c->r0, c->nl, dpiv.p, k, x_e.p, N, ds), 1,
+                        "ext_rows");
+        c->check_launch(gpk::launch_gather_ext_rows(c->sq.p, n, 1, c->r0, c->nl, dpiv.p, k, sq_e.p, N, ds), 1,
+                        "ext_rows");
+        c->check_launch(gpk::launch_iota_ll(piv_e.p, k, c->nl, ds), 1, "iota");
+        sxp = xs_e.p;
+        xp = x_e.p;
+        sqp = sq_e.p;
+        pivp = piv_e.p;
+      }
       DBuf<double> rep;
       rep.ensure(gpk::dl_replay_workspace(nw));
       c->ensure_handles();
@@ -2425,32 +2558,43 @@ gpk_status gpk_precond_deriv_factors(gpk_ctx* ctx) {
       for (int s0 = 0; s0 < k; s0 += kB) {
         const int bb = std::min(kB, k - s0);
         // DC_w[:, q] = dK_w column of pivot s0+q (all pivots of the block in one launch)
-        c->check_launch(gpk::launch_deriv_columns_block(c->family, c->sx.p, c->X.p, c->sq.p, n, c->d, dpiv.p + s0, bb,
-                                                        nw, facs.p, c->o2, DC.p, static_cast<long long>(n) * kB,
+        c->check_launch(gpk::launch_deriv_columns_block(c->family, sxp, xp, sqp, N, c->d, pivp + s0, bb,
+                                                        nw, facs.p, c->o2, DC.p, static_cast<long long>(N) * kB,
                                                         ds),
                         1, "deriv_columns_block");
         if (s0 > 0) {
           // Lp[c][q] = L[piv_q, c], dLp_w[c][q] = dL_w[piv_q, c]   (s0 x bb, column-major)
-          c->check_launch(gpk::launch_gather_pivot_rows(c->L.p, n, 0, 1, dpiv.p + s0, s0, bb, Lp.p, ds), 1,
+          c->check_launch(gpk::launch_gather_pivot_rows(c->L.p, N, 0, 1, pivp + s0, s0, bb, Lp.p, ds), 1,
                           "gather_pivot_rows");
-          c->check_launch(gpk::launch_gather_pivot_rows(c->dL.p, n, wstride, nw, dpiv.p + s0, s0, bb, dLp.p, ds),
+          c->check_launch(gpk::launch_gather_pivot_rows(c->dL.p, N, wstride, nw, pivp + s0, s0, bb, dLp.p, ds),
                           1, "gather_pivot_rows");
           const double m1 = -1.0, one = 1.0;
           // DC_w -= dL_w[:, :s0] Lp ;  DC_w -= L[:, :s0] dLp_w
-          CB(cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, bb, s0, &m1, c->dL.p, n, wstride, Lp.p,
-                                       s0, 0, &one, DC.p, n, static_cast<long long>(n) * kB, nw));
-          CB(cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, bb, s0, &m1, c->L.p, n, 0, dLp.p, s0,
-                                       static_cast<long long>(s0) * bb, &one, DC.p, n,
-                                       static_cast<long long>(n) * kB, nw));
+          CB(cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, N, bb, s0, &m1, c->dL.p, N, wstride, Lp.p,
+                                       s0, 0, &one, DC.p, N, static_cast<long long>(N) * kB, nw));
+          CB(cublasDgemmStridedBatched(c->blas, CUBLAS_OP_N, CUBLAS_OP_N, N, bb, s0, &m1, c->L.p, N, 0, dLp.p, s0,
+                                       static_cast<long long>(s0) * bb, &one, DC.p, N,
+                                       static_cast<long long>(N) * kB, nw));
           c->launches += 2;
         }
         // in-block recursion: one launch per block (every CTA replays the pivot rows' recursion)
-        c->check_launch(gpk::launch_dl_block(c->L.p, c->dL.p, wstride, nw, s0, bb, dpiv.p + s0, DC.p,
-                                             static_cast<long long>(n) * kB, n, rep.p, ds),
+        c->check_launch(gpk::launch_dl_block(c->L.p, c->dL.p, wstride, nw, s0, bb, pivp + s0, DC.p,
+                                             static_cast<long long>(N) * kB, N, rep.p, ds),
                         2, "dl_block");
       }
       // tr(P^{-1} dP_w) = 2 sum(C o dL_w)  (algebraically equal to preconditioners.hpp:138-145)
       // all nw traces on the device; the host reads them when it needs them (need_trace)
+      if (shard) {  // own rows per rank, rank-ordered sums
+        std::vector<double> tr(nw, 0.0);
+        for (int w = 0; w < nw; ++w) {
+          const std::vector<double> cd = c->col_dots(c->C.p, c->dL.p + static_cast<size_t>(w) * N * k, k, N);
+          for (int q = 0; q < k; ++q) tr[w] += cd[q];
+        }
+        c->h2d(c->w_trace.p, tr.data(), sizeof(double) * nw);
+        c->trace_pending = true;
+        c->have_dl = true;
+        return;
+      }
       const int nrb = gpk::num_chunks(n * k);
       DBuf<double> part;
       part.ensure(static_cast<size_t>(nrb) * nw);
@@ -2476,7 +2620,14 @@ gpk_status gpk_precond_factor(gpk_ctx* ctx, double* L, int64_t ldl) {
   return guard(ctx, [&] {
     require(ctx->pkind == 2, "gpkrylov_cuda: no pivoted-Cholesky preconditioner");
     if (ctx->k == 0) return;
-    CK(cudaMemcpy2DAsync(L, ldl * sizeof(double), ctx->L.p, ctx->n * sizeof(double), ctx->n * sizeof(double), ctx->k,
+    const double* src = ctx->L.p;
+    DBuf<double> full;
+    if (ctx->pshard) {  // every rank's own rows, gathered
+      full.ensure(static_cast<size_t>(ctx->n) * ctx->k);
+      ctx->allgather_cols(ctx->L.p, ctx->ldP, ctx->k, full.p, ctx->n);
+      src = full.p;
+    }
+    CK(cudaMemcpy2DAsync(L, ldl * sizeof(double), src, ctx->n * sizeof(double), ctx->n * sizeof(double), ctx->k,
                          cudaMemcpyDeviceToHost, ctx->st));
     ctx->sync();
   });
@@ -2492,8 +2643,15 @@ gpk_status gpk_precond_deriv_factor(gpk_ctx* ctx, int which, double* dL, int64_t
       for (int c = 0; c < k; ++c) std::fill(dL + c * ldl, dL + c * ldl + n, 0.0);
       return;
     }
-    CK(cudaMemcpy2DAsync(dL, ldl * sizeof(double), ctx->dL.p + static_cast<size_t>(which) * n * k, n * sizeof(double),
-                         n * sizeof(double), k, cudaMemcpyDeviceToHost, ctx->st));
+    const double* src = ctx->dL.p + static_cast<size_t>(which) * ctx->ldP * k;
+    DBuf<double> full;
+    if (ctx->pshard) {  // every rank's own rows, gathered
+      full.ensure(static_cast<size_t>(n) * k);
+      ctx->allgather_cols(src, ctx->ldP, k, full.p, n);
+      src = full.p;
+    }
+    CK(cudaMemcpy2DAsync(dL, ldl * sizeof(double), src, n * sizeof(double), n * sizeof(double), k,
+                         cudaMemcpyDeviceToHost, ctx->st));
     ctx->sync();
   });
 }

@@ -63,10 +63,12 @@ cudaError_t launch_pack_v_tc(const double* V, long long ldv, int t, int n, int n
 cudaError_t launch_fused_kmvm_tc(int family, int dp, const float* X, const float* vhi, const float* vlo, double* out,
                                  const MvmArgs& a, int splits, cudaStream_t st);
 
-// Gram variant (both contractions on tcgen05): squared distances from the expanded
-// form with the cross term in 3xTF32.  Packs X / l - mean, pre-scaled, as tf32 hi/lo
-// 32x32 swizzled tiles (xh, xl: n_pad x 32 floats) and fp32 norms xn (n_pad); mu: d
-// doubles of scratch.  RBF / Matern-3/2 / Matern-5/2, d <= 32.
+// Gram variant (both contractions on tcgen05): squared distances s_ij = n_i + n_j - 2 x~_i.x~_j
+// straight out of a 3xTF32 MMA on augmented coordinates.  Packs x~ = (X / l - mean) pre-scaled
+// as tf32 hi/lo 32x32 swizzled tiles: xh, xl hold 2 n_pad x 32 floats (the B-side image
+// [x~, 1, n] then the A-side image [-2 x~, n, 1]); xn holds n_pad fp32 norms then n_pad / 64
+// per-j-tile maxima; mu: d doubles of scratch.  RBF / Matern-3/2 / Matern-5/2, d <= 30.
+constexpr int kGramMaxDim = 30;  // d + 2 augmented Gram coordinates in <= 32 tf32 columns
 cudaError_t launch_gram_pack(const double* X, long long ldx, int n, int d, int n_pad, const double* ls,
                              double prescale, double* mu, float* xh, float* xl, float* xn, cudaStream_t st);
 // V (t <= 96 columns) -> per-column power-of-two scaled fp16 hi/lo tiles (+ colscale_c =

@@ -114,6 +114,24 @@ int pchol_persistent_grid(int n, size_t smem);
 cudaError_t launch_pchol_persistent(int family, const double* sx, const double* sq, int n, int d, double o2,
                                     double* L, int rank, double diag_tol, double kmax, double* dg, double* cval,
                                     long long* cidx, PivotState* ps, long long* pivots, int grid, cudaStream_t st);
+// row-sharded pivoted Cholesky (gpk_pchol.cu): per-step kernels on the own rows, candidates and
+// the pivot row exchanged by all-gathers between them
+int pchol_shard_grid(int nl);
+cudaError_t launch_pchol_shard_step(int family, const double* sx, const double* sq, int n, int d, double o2,
+                                    double* L, long long ldl, int r0, int nl, int s, const double* lp,
+                                    const PivotState* ps, double* dg, double* cval, long long* cidx, int grid,
+                                    double* send, cudaStream_t st);
+cudaError_t launch_pchol_shard_select(const double* cand, int world, int s, double diag_tol, double kmax,
+                                      PivotState* ps, long long* pivots, const double* L, long long ldl, int r0,
+                                      int nl, int k, double* rowsend, cudaStream_t st);
+cudaError_t launch_pchol_shard_rowtake(const double* recv, int world, int k, const int* rr0, const int* rrows,
+                                       const PivotState* ps, double* lp, cudaStream_t st);
+cudaError_t launch_pchol_pivot_rows(int phase, const double* src, double* dst, long long ldl, int r0, int nl, int k,
+                                    const long long* piv, int world, const int* rr0, const int* rrows,
+                                    cudaStream_t st);
+cudaError_t launch_gather_ext_rows(const double* src, long long lds, int cols, int r0, int nl, const long long* piv,
+                                   int k, double* dst, long long ne, cudaStream_t st);
+cudaError_t launch_iota_ll(long long* out, int k, long long base, cudaStream_t st);
 cudaError_t launch_deriv_columns_block(int family, const double* sx, const double* x, const double* sq, int n, int d,
                                        const long long* piv, int bb, int nw, const double* facs, double o2,
                                        double* DC, long long dcw_stride, cudaStream_t st);

@@ -83,6 +83,26 @@ GPK_DEV float kval32_scaled(float s) {
     return fmaf(rr, fmaf(rr, C / 3.0f, C), C) * e;
   }
 }
+// kval32_scaled for two entries at once: the FP32 polynomial / scaling steps as paired
+// FFMA2 / FMUL2 (one instruction per two entries), the sqrt / ex2 on the SFU per entry.
+template <int FAM, int LOG2C>
+GPK_DEV float2 kval32x2_scaled(float2 s) {
+  constexpr float C = static_cast<float>(1 << LOG2C);
+  if constexpr (FAM == kRBF) {
+    const float2 a = __fadd2_rn(make_float2(static_cast<float>(LOG2C), static_cast<float>(LOG2C)),
+                                make_float2(-s.x, -s.y));
+    return make_float2(ex2_approx(a.x), ex2_approx(a.y));
+  } else {
+    const float2 r = make_float2(sqrt_approx(s.x), sqrt_approx(s.y));
+    const float2 e = make_float2(ex2_approx(-r.x), ex2_approx(-r.y));
+    if constexpr (FAM == kMatern12) return __fmul2_rn(make_float2(C, C), e);
+    if constexpr (FAM == kMatern32)
+      return __fmul2_rn(__ffma2_rn(r, make_float2(C * kLn2, C * kLn2), make_float2(C, C)), e);
+    const float2 rr = __fmul2_rn(r, make_float2(kLn2, kLn2));  // Matern52
+    const float2 q = __ffma2_rn(rr, make_float2(C / 3.0f, C / 3.0f), make_float2(C, C));
+    return __fmul2_rn(__ffma2_rn(rr, q, make_float2(C, C)), e);
+  }
+}
 // shape_ds (kernels.hpp:115-134) in pre-scaled units.
 template <int FAM>
 GPK_DEV float kds32(float s) {

@@ -29,9 +29,14 @@ __global__ void gram_mean_kernel(const double* __restrict__ X, long long ldx, in
   if (threadIdx.x == 0) mu[k] = red[0] / n / ls[k];
 }
 
-// one thread per (row, coordinate slot): x~ = (X/l - mu) sqrt(prescale), split into
-// tf32 hi / lo at the swizzled position of the tile image; padded rows and
-// coordinates are zero.  Norms: fp32 sum of squares of the fp32 coordinates.
+// one thread per row: x~ = (X/l - mu) sqrt(prescale), n = |x~|^2 (fp32), and the two
+// AUGMENTED coordinate images of the Gram MMA, split into tf32 hi / lo at the swizzled
+// positions of the tile image (padded rows / coordinates zero):
+//   B side (the j-tiles, xh / xl):              [ x~ (d) , 1 , n ]
+//   A side (the row operand, xh / xl + 32 n_pad): [ -2 x~ (d), n , 1 ]
+// so that A_i . B_j = n_i + n_j - 2 x~_i . x~_j = s_ij comes out of the tensor cores directly
+// (the -2 is exact in the split; n and 1 split into hi + lo like every coordinate).  xn[i] = n;
+// xn[n_pad + jt] = max over j-tile jt of n (the per-tile bound of the cancellation guard).
 __global__ void gram_pack_kernel(const double* __restrict__ X, long long ldx, int n, int d, int n_pad,
                                  const double* __restrict__ ls, const double* __restrict__ mu, double pre,
                                  float* __restrict__ xh, float* __restrict__ xl, float* __restrict__ xn) {
@@ -39,25 +44,52 @@ __global__ void gram_pack_kernel(const double* __restrict__ X, long long ldx, in
   if (i >= n_pad) return;
   const long long tile = i >> 5;
   const int r = i & 31;
+  const bool real = i < n;
   float nrm = 0.0f;
-  for (int k = 0; k < 32; ++k) {
-    float v = 0.0f;
-    if (i < n && k < d) v = static_cast<float>((X[k * ldx + i] / ls[k] - mu[k]) * pre);
-    const float hi = tc::to_tf32(v);
-    const float lo = tc::to_tf32(v - hi);
-    const long long off = tile * 1024 + ((r >> 3) * 256 + (r & 7) * 32 + ((((k >> 2) ^ (r & 7))) << 2) + (k & 3));
-    xh[off] = hi;
-    xl[off] = lo;
+  for (int k = 0; k < d; ++k) {
+    const float v = real ? static_cast<float>((X[k * ldx + i] / ls[k] - mu[k]) * pre) : 0.0f;
     nrm = fmaf(v, v, nrm);
+  }
+  const long long aoff = static_cast<long long>(n_pad) * 32;
+  for (int k = 0; k < 32; ++k) {
+    float vb = 0.0f, va = 0.0f;
+    if (real) {
+      if (k < d) {
+        vb = static_cast<float>((X[k * ldx + i] / ls[k] - mu[k]) * pre);
+        va = -2.0f * vb;
+      } else if (k == d) {
+        vb = 1.0f;
+        va = nrm;
+      } else if (k == d + 1) {
+        vb = nrm;
+        va = 1.0f;
+      }
+    }
+    const long long off = tile * 1024 + ((r >> 3) * 256 + (r & 7) * 32 + ((((k >> 2) ^ (r & 7))) << 2) + (k & 3));
+    const float bh = tc::to_tf32(vb), ah = tc::to_tf32(va);
+    xh[off] = bh;
+    xl[off] = tc::to_tf32(vb - bh);
+    xh[aoff + off] = ah;
+    xl[aoff + off] = tc::to_tf32(va - ah);
   }
   xn[i] = nrm;
 }
 
+__global__ void gram_tilemax_kernel(const float* __restrict__ xn, int n_pad, float* __restrict__ tmax) {
+  const int jt = blockIdx.x * blockDim.x + threadIdx.x;
+  if (jt * 64 >= n_pad) return;
+  float m = 0.0f;
+  for (int j = 0; j < 64; ++j) m = fmaxf(m, xn[jt * 64 + j]);
+  tmax[jt] = m;
+}
+
 cudaError_t launch_gram_pack(const double* X, long long ldx, int n, int d, int n_pad, const double* ls,
                              double prescale, double* mu, float* xh, float* xl, float* xn, cudaStream_t st) {
-  if (d < 1 || d > 32) return cudaErrorInvalidValue;
+  if (d < 1 || d > kGramMaxDim) return cudaErrorInvalidValue;
   gram_mean_kernel<<<d, 256, 0, st>>>(X, ldx, n, ls, mu);
   gram_pack_kernel<<<(n_pad + 127) / 128, 128, 0, st>>>(X, ldx, n, d, n_pad, ls, mu, sqrt(prescale), xh, xl, xn);
+  const int nt = n_pad / 64;
+  gram_tilemax_kernel<<<(nt + 127) / 128, 128, 0, st>>>(xn, n_pad, xn + n_pad);
   return cudaGetLastError();
 }
 
@@ -141,8 +173,8 @@ cudaError_t launch_fused_kmvm_tcg(int family, int d, int direct_dp, const float*
                                   const double* colscale, double* out, const MvmArgs& a, int splits,
                                   cudaStream_t st) {
   const int npad = tcg_npad(a.t);
-  if (npad < 0 || d < 1 || d > 32) return cudaErrorInvalidValue;
-  const int ks = (d + 7) / 8;
+  if (npad < 0 || d < 1 || d > 32 || (direct_dp == 0 && d > kGramMaxDim)) return cudaErrorInvalidValue;
+  const int ks = (d + 2 + 7) / 8;  // Gram mode: the augmented coordinates [x~, 1, n] / [-2 x~, n, 1]
   const int units = (a.row_end - a.row_begin + tcg::BM - 1) / tcg::BM * splits;
   dim3 g(a.ctas > 0 ? std::min(units, a.ctas) : units);  // persistent grid, or one CTA per unit
   const int nc8 = npad / 8;

@@ -113,6 +113,19 @@ GPK_DEV uint32_t elect_one() {
   return pred;
 }
 GPK_DEV uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+// fp16 hi / lo split of two entries: hi = f16(e) (packed, x in the low half), lo = f16(e - hi)
+// with e - hi as ONE mixed-precision add per entry (FHADD: f32 = -f16 + f32) instead of
+// unpacking hi to f32 first -- 4 instructions per 2 entries instead of 5.
+GPK_DEV uint32_t split_f16x2(float2 e, uint32_t& lo) {
+  uint32_t hb;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hb) : "f"(e.y), "f"(e.x));
+  unsigned short hx = static_cast<unsigned short>(hb & 0xffffu), hy = static_cast<unsigned short>(hb >> 16);
+  float lx, ly;
+  asm("{\n\t.reg .f16 n;\n\tneg.f16 n, %1;\n\tadd.rn.f32.f16 %0, n, %2;\n\t}" : "=f"(lx) : "h"(hx), "f"(e.x));
+  asm("{\n\t.reg .f16 n;\n\tneg.f16 n, %1;\n\tadd.rn.f32.f16 %0, n, %2;\n\t}" : "=f"(ly) : "h"(hy), "f"(e.y));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(ly), "f"(lx));
+  return hb;
+}
 
 // DPD > 0: direct-difference mode (no Gram MMA): s_ij from the fp32 rows of X32 staged in
 // shared memory (DPD = the padded coordinate count, <= 8) -- the low-dimensional / Matern-1/2
@@ -131,6 +144,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int HC = (NC8 + RPT - 1) / RPT;
   constexpr uint32_t TMEM_COLS = 512;
 
+  // Gram mode: the A-side augmented image (row operand) follows the B-side one; the per-j-tile
+  // norm maxima follow the norms (gram_pack_kernel)
+  const float* XAh = Xh + static_cast<long long>(a.n_pad) * 32;
+  const float* XAl = Xl + static_cast<long long>(a.n_pad) * 32;
+  const float* Xtm = Xn + a.n_pad;
   extern __shared__ unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -344,8 +362,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int u = 0; u < 8; ++u) {
         const int k = q * 8 + u;
         const long long off = rb + ((((k >> 2) ^ (row & 7))) << 2) + (k & 3);
-        h8[u] = __float_as_uint(Xh[off]);
-        l8[u] = __float_as_uint(Xl[off]);
+        h8[u] = __float_as_uint(XAh[off]);
+        l8[u] = __float_as_uint(XAl[off]);
       }
       tmem_st8(tmem_base + tlane + T_AX + q * 8, h8);
       tmem_st8(tmem_base + tlane + T_AX + 32 + q * 8, l8);
@@ -367,7 +385,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     }  // new row block
-    const float2 ni2 = make_float2(ni, ni);
     auto drain = [&](unsigned g) {
       const int buf = g & 1;
       mbar_wait_sleep(&acc_full[buf], (g >> 1) & 1);
@@ -393,8 +410,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       if constexpr (!DIRECT) mbar_wait_sleep(&g_full[gb], (it >> 1) & 1);
       if (threadIdx.x == 64) GPK_TRACE(2, it);
       tc::tc_fence_after();
-      mbar_wait_sleep(&xv_full[s], (it / SG) & 1);  // |x_j|^2 of this stage visible to the generic proxy
+      // direct mode reads the staged rows; Gram mode reads shared memory only in the (rare)
+      // guard path and waits there (the stage is complete: its Gram MMA consumed it)
+      if constexpr (DIRECT) mbar_wait_sleep(&xv_full[s], (it / SG) & 1);
       mbar_wait_sleep(&a_empty[as], ((it / AS) & 1) ^ 1);
+      // guard threshold of this tile: kGuard (|x_i|^2 + max_j |x_j|^2) bounds every pair's own
+      // kGuard (|x_i|^2 + |x_j|^2), so a warp whose 8 entries all exceed it has no near pair
+      const float gthr = DIRECT ? 0.0f : kGuard * (ni + __ldg(Xtm + jt0 + lt));
       // the thread's 16 Gram values in one TMEM load and the Gram buffer released right away
       // (measured: -2% at NC8 = 7; with NC8 > 8 the extra live registers cost 6%, so there the
       // two halves load separately)
@@ -441,58 +463,58 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lane == 0) tc::mbar_arrive(&g_empty[gb]);
           }
         }
-        const float* nsj = Ns + s * BK + q * JPT + hf8 * 8;
-        float2 gmin = make_float2(1.0f, 1.0f);  // min over entries of s - kGuard (|x_i|^2 + |x_j|^2)
+        // s_ij straight from the augmented Gram MMA (n_i + n_j - 2 x~_i . x~_j)
 #pragma unroll
-        for (int p4 = 0; p4 < 2; ++p4) {
-          const float4 n4 = reinterpret_cast<const float4*>(nsj)[p4];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int u = p4 * 4 + 2 * h;
-            const float2 nn = __fadd2_rn(h ? make_float2(n4.z, n4.w) : make_float2(n4.x, n4.y), ni2);
-            const float2 g2 = make_float2(__uint_as_float(gv[u]), __uint_as_float(gv[u + 1]));
-            const float2 t2 = __ffma2_rn(make_float2(-2.0f, -2.0f), g2, nn);
-            const float2 m2 = __ffma2_rn(make_float2(-kGuard, -kGuard), nn, t2);
-            gmin = make_float2(fminf(gmin.x, m2.x), fminf(gmin.y, m2.y));
-            sv[u] = fmaxf(t2.x, 0.0f);
-            sv[u + 1] = fmaxf(t2.y, 0.0f);
-          }
-        }
-        // Cancellation guard: s <= (|x_i|^2 + |x_j|^2) / 16 (near pairs, incl. the
-        // diagonal) is recomputed from fp32 direct differences of the un-centred
-        // coordinates, so the expanded form only serves pairs whose relative error in s
-        // stays at the fp32 level.  Rare for the spread-out data auto mode selects.
-        if (__any_sync(0xffffffffu, fminf(gmin.x, gmin.y) <= 0.0f)) {
-          // the whole warp evaluates the 8 direct distances (no divergence), from shared memory
-          const float4* xi4 = reinterpret_cast<const float4*>(XIs + r * a.dp);
-          const float4* xj4 = reinterpret_cast<const float4*>(XJs + s * (XJ_TILE / 4) + (q * JPT + hf8 * 8) * a.dp);
-          const int d4 = a.dp >> 2;
+        for (int u = 0; u < 8; ++u) sv[u] = __uint_as_float(gv[u]);
+        const float smin = fminf(fminf(fminf(sv[0], sv[1]), fminf(sv[2], sv[3])),
+                                 fminf(fminf(sv[4], sv[5]), fminf(sv[6], sv[7])));
+        // Cancellation guard: s <= kGuard (|x_i|^2 + |x_j|^2) (near pairs, incl. the diagonal,
+        // where the expanded form may even go negative) is recomputed from fp32 direct
+        // differences of the un-centred coordinates, so the expanded form only serves pairs whose
+        // relative error in s stays at the fp32 level.  Every entry that is not a near pair
+        // exceeds kGuard (|x_i|^2 + |x_j|^2) >= 0, hence is positive: no clamp anywhere.
+        if (__any_sync(0xffffffffu, smin <= gthr)) {
+          // some entry is within the tile bound: the exact per-entry test first (cheap), the
+          // direct recompute only when an entry really is a near pair
+          mbar_wait_sleep(&xv_full[s], (it / SG) & 1);  // the stage's norms and rows, generic proxy
+          const float* nsj = Ns + s * BK + q * JPT + hf8 * 8;
+          const float4 n0 = reinterpret_cast<const float4*>(nsj)[0], n1 = reinterpret_cast<const float4*>(nsj)[1];
+          const float nj[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+          bool near[8];
+          bool anyn = false;
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            float acc = 0.0f;
+            near[u] = sv[u] <= kGuard * (nj[u] + ni);
+            anyn = anyn || near[u];
+          }
+          if (__any_sync(0xffffffffu, anyn)) {
+            // the whole warp evaluates the 8 direct distances (no divergence), from shared memory
+            const float4* xi4 = reinterpret_cast<const float4*>(XIs + r * a.dp);
+            const float4* xj4 =
+                reinterpret_cast<const float4*>(XJs + s * (XJ_TILE / 4) + (q * JPT + hf8 * 8) * a.dp);
+            const int d4 = a.dp >> 2;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              float acc = 0.0f;
 #pragma unroll 1
-            for (int k = 0; k < d4; ++k) {
-              const float4 p = xi4[k], qv = xj4[u * d4 + k];
-              const float d0 = p.x - qv.x, d1 = p.y - qv.y, d2 = p.z - qv.z, d3 = p.w - qv.w;
-              acc = fmaf(d0, d0, acc);
-              acc = fmaf(d1, d1, acc);
-              acc = fmaf(d2, d2, acc);
-              acc = fmaf(d3, d3, acc);
+              for (int k = 0; k < d4; ++k) {
+                const float4 p = xi4[k], qv = xj4[u * d4 + k];
+                const float d0 = p.x - qv.x, d1 = p.y - qv.y, d2 = p.z - qv.z, d3 = p.w - qv.w;
+                acc = fmaf(d0, d0, acc);
+                acc = fmaf(d1, d1, acc);
+                acc = fmaf(d2, d2, acc);
+                acc = fmaf(d3, d3, acc);
+              }
+              if (near[u]) sv[u] = acc;
             }
-            if (sv[u] <= kGuard * (nsj[u] + ni)) sv[u] = acc;
           }
         }
         }  // Gram mode
         uint32_t eh[4], el[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          const float2 e2 = make_float2(kval32_scaled<FAM, kEntryLog2>(sv[2 * p]),
-                                        kval32_scaled<FAM, kEntryLog2>(sv[2 * p + 1]));
-          const __half2 h2 = __float22half2_rn(e2);
-          const float2 hf = __half22float2(h2);
-          const __half2 l2 = __float22half2_rn(__fadd2_rn(e2, make_float2(-hf.x, -hf.y)));
-          eh[p] = h2_bits(h2);
-          el[p] = h2_bits(l2);
+          const float2 e2 = kval32x2_scaled<FAM, kEntryLog2>(make_float2(sv[2 * p], sv[2 * p + 1]));
+          eh[p] = split_f16x2(e2, el[p]);
         }
         tmem_st4(tmem_base + tlane + T_AT + as * 64 + q * 8 + hf8 * 4, eh);
         tmem_st4(tmem_base + tlane + T_AT + as * 64 + 32 + q * 8 + hf8 * 4, el);

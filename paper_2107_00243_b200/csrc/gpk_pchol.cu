@@ -303,4 +303,229 @@ cudaError_t launch_dl_block(const double* L, double* dL, long long wstride, int 
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Row-sharded pivoted Cholesky (world > 1): every rank owns the rows
+// [r0, r0 + nl) of L (local leading dimension ldl) and of the diagonal.  Per step, all
+// stream-ordered (no host round trip; a fired stopping rule turns later steps into no-ops):
+//   pchol_shard_step : column s on the own rows -- exactly pchol_persistent_kernel's per-row
+//                      arithmetic, so the rows and the diagonal are bitwise the unsharded
+//                      ones -- and per-CTA (max, lowest index) candidates
+//   pchol_shard_best : the rank's candidate (max, lowest GLOBAL index)
+//   [all-gather of the world's candidates]
+//   pchol_shard_select: the global pivot (max, lowest index over ranks in rank order =
+//                      index order: the reference's strict '>' scan, preconditioners.hpp:
+//                      247-249) and the stopping rules (:250-253)
+//   pchol_shard_rowpack: the owner of the new pivot p sends L[p, 0..s]
+//   [all-gather]  pchol_shard_rowtake: every rank takes the owner's row as the next L[p, :s]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPT) pchol_shard_step_kernel(int f, const double* __restrict__ sx,
+                                                               const double* __restrict__ sq, int n, int d,
+                                                               double o2, double* __restrict__ L, long long ldl,
+                                                               int r0, int nl, int s, const double* __restrict__ lpg,
+                                                               const PivotState* __restrict__ ps,
+                                                               double* __restrict__ dg, double* __restrict__ cval,
+                                                               long long* __restrict__ cidx) {
+  extern __shared__ double lp[];
+  __shared__ double xp[32];
+  __shared__ double sv[kPT / 32];
+  __shared__ long long si[kPT / 32];
+  if (ps->stopped) return;
+  const long long p = ps->p;
+  const double root = sqrt(ps->dp);  // preconditioners.hpp:256
+  for (int c = threadIdx.x; c < s; c += kPT) lp[c] = lpg[c];
+  for (int k = threadIdx.x; k < d; k += kPT) xp[k] = sx[static_cast<long long>(k) * n + p];
+  __syncthreads();
+  const double sqp = sq[p];
+  double best = -DBL_MAX;
+  long long bi = LLONG_MAX;
+  for (int j = blockIdx.x * kPT + threadIdx.x; j < nl; j += gridDim.x * kPT) {
+    const long long i = r0 + j;
+    double g = 0.0;
+    for (int k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(sx[static_cast<long long>(k) * n + i], xp[k]));
+    double sd = __dsub_rn(__dadd_rn(sq[i], sqp), __dmul_rn(2.0, g));
+    sd = sd > 0.0 ? sd : 0.0;
+    const double col = __dmul_rn(o2, ref_shape(f, sd));
+    double h = 0.0;
+    int c = 0;
+    for (; c + 8 <= s; c += 8) {
+      double v8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v8[u] = L[static_cast<long long>(c + u) * ldl + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) h = __dadd_rn(h, __dmul_rn(v8[u], lp[c + u]));
+    }
+    for (; c < s; ++c) h = __dadd_rn(h, __dmul_rn(L[static_cast<long long>(c) * ldl + j], lp[c]));
+    const double v = __ddiv_rn(__dsub_rn(col, h), root);
+    L[static_cast<long long>(s) * ldl + j] = v;
+    const double dn = __dsub_rn(dg[j], __dmul_rn(v, v));
+    dg[j] = dn;
+    better(best, bi, dn, i);
+  }
+  block_best(best, bi, sv, si);
+  if (threadIdx.x == 0) {
+    cval[blockIdx.x] = best;
+    cidx[blockIdx.x] = bi;
+  }
+}
+
+// the rank's candidate over the G CTA candidates -> send = {value, index as double bits}
+__global__ void __launch_bounds__(kPT) pchol_shard_best_kernel(const double* __restrict__ cval,
+                                                               const long long* __restrict__ cidx, int G,
+                                                               const PivotState* __restrict__ ps,
+                                                               double* __restrict__ send) {
+  __shared__ double sv[kPT / 32];
+  __shared__ long long si[kPT / 32];
+  if (ps->stopped) return;
+  double bv = -DBL_MAX;
+  long long bi = LLONG_MAX;
+  for (int b = threadIdx.x; b < G; b += kPT) better(bv, bi, cval[b], cidx[b]);
+  block_best(bv, bi, sv, si);
+  if (threadIdx.x == 0) {
+    send[0] = bv;
+    send[1] = __longlong_as_double(bi);
+  }
+}
+
+// global pivot over the world's candidates (rank order), stopping rules, pivot record
+__global__ void pchol_shard_select_kernel(const double* __restrict__ cand, int world, int s, double diag_tol,
+                                          double kmax, PivotState* __restrict__ ps, long long* __restrict__ pivots) {
+  if (threadIdx.x != 0 || ps->stopped) return;
+  double nv = -DBL_MAX;
+  long long ni = LLONG_MAX;
+  for (int r = 0; r < world; ++r) better(nv, ni, cand[2 * r], __double_as_longlong(cand[2 * r + 1]));
+  const bool negative = nv < -1e-10 * kmax;      // :250-252
+  const bool stop = negative || nv <= diag_tol;  // :253
+  pivots[s] = ps->p;
+  ps->dp = nv;
+  ps->p = ni;
+  ps->done = s + 1;
+  ps->stopped = stop ? 1 : 0;
+  ps->negative = negative ? 1 : 0;
+}
+
+// the owner of the (new) pivot packs L[p, 0..s] (k doubles, zero beyond s and on other ranks)
+__global__ void pchol_shard_rowpack_kernel(const double* __restrict__ L, long long ldl, int r0, int nl, int s, int k,
+                                           const PivotState* __restrict__ ps, double* __restrict__ send) {
+  const long long p = ps->p;
+  const bool mine = !ps->stopped && p >= r0 && p < r0 + nl;
+  for (int c = threadIdx.x; c < k; c += blockDim.x)
+    send[c] = (mine && c <= s) ? L[static_cast<long long>(c) * ldl + (p - r0)] : 0.0;
+}
+
+// every rank takes the owner's row: lp[c] = recv[owner][c]
+__global__ void pchol_shard_rowtake_kernel(const double* __restrict__ recv, int world, int k,
+                                           const int* __restrict__ rr0, const int* __restrict__ rrows,
+                                           const PivotState* __restrict__ ps, double* __restrict__ lp) {
+  if (ps->stopped) return;
+  const long long p = ps->p;
+  int owner = 0;
+  for (int r = 0; r < world; ++r)
+    if (p >= rr0[r] && p < rr0[r] + rrows[r]) owner = r;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) lp[c] = recv[static_cast<long long>(owner) * k + c];
+}
+
+// rows of pivots owned by this rank -> send[q][c] (k x k, zero for other ranks' pivots)
+__global__ void pchol_pivot_rows_pack_kernel(const double* __restrict__ L, long long ldl, int r0, int nl, int k,
+                                             const long long* __restrict__ piv, double* __restrict__ send) {
+  const int q = blockIdx.x;
+  const long long p = piv[q];
+  const bool mine = p >= r0 && p < r0 + nl;
+  for (int c = threadIdx.x; c < k; c += blockDim.x)
+    send[static_cast<long long>(q) * k + c] = mine ? L[static_cast<long long>(c) * ldl + (p - r0)] : 0.0;
+}
+
+// L[nl + q, c] = the owner's row of pivot q (the extended rows of the sharded factor)
+__global__ void pchol_pivot_rows_take_kernel(const double* __restrict__ recv, int world, int k,
+                                             const int* __restrict__ rr0, const int* __restrict__ rrows,
+                                             const long long* __restrict__ piv, double* __restrict__ L,
+                                             long long ldl, int nl) {
+  const int q = blockIdx.x;
+  const long long p = piv[q];
+  int owner = 0;
+  for (int r = 0; r < world; ++r)
+    if (p >= rr0[r] && p < rr0[r] + rrows[r]) owner = r;
+  const double* src = recv + (static_cast<long long>(owner) * k + q) * k;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) L[static_cast<long long>(c) * ldl + nl + q] = src[c];
+}
+
+int pchol_shard_grid(int nl) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int need = (nl + kPT - 1) / kPT;
+  return need < 4 * sms ? (need > 0 ? need : 1) : 4 * sms;
+}
+
+cudaError_t launch_pchol_shard_step(int family, const double* sx, const double* sq, int n, int d, double o2,
+                                    double* L, long long ldl, int r0, int nl, int s, const double* lp,
+                                    const PivotState* ps, double* dg, double* cval, long long* cidx, int grid,
+                                    double* send, cudaStream_t st) {
+  const size_t smem = sizeof(double) * static_cast<size_t>(s > 0 ? s : 1);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(pchol_shard_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  pchol_shard_step_kernel<<<grid, kPT, smem, st>>>(family, sx, sq, n, d, o2, L, ldl, r0, nl, s, lp, ps, dg, cval,
+                                                   cidx);
+  pchol_shard_best_kernel<<<1, kPT, 0, st>>>(cval, cidx, grid, ps, send);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pchol_shard_select(const double* cand, int world, int s, double diag_tol, double kmax,
+                                      PivotState* ps, long long* pivots, const double* L, long long ldl, int r0,
+                                      int nl, int k, double* rowsend, cudaStream_t st) {
+  pchol_shard_select_kernel<<<1, 32, 0, st>>>(cand, world, s, diag_tol, kmax, ps, pivots);
+  pchol_shard_rowpack_kernel<<<1, 256, 0, st>>>(L, ldl, r0, nl, s, k, ps, rowsend);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pchol_shard_rowtake(const double* recv, int world, int k, const int* rr0, const int* rrows,
+                                       const PivotState* ps, double* lp, cudaStream_t st) {
+  pchol_shard_rowtake_kernel<<<1, 256, 0, st>>>(recv, world, k, rr0, rrows, ps, lp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pchol_pivot_rows(int phase, const double* src, double* dst, long long ldl, int r0, int nl, int k,
+                                    const long long* piv, int world, const int* rr0, const int* rrows,
+                                    cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  if (phase == 0)
+    pchol_pivot_rows_pack_kernel<<<k, 128, 0, st>>>(src, ldl, r0, nl, k, piv, dst);
+  else
+    pchol_pivot_rows_take_kernel<<<k, 128, 0, st>>>(src, world, k, rr0, rrows, piv, dst, ldl, nl);
+  return cudaGetLastError();
+}
+
+// extended coordinate rows for the sharded derivative factors: rows [0, nl) = global rows
+// r0 .. r0 + nl - 1, rows [nl, nl + k) = the pivots (column-major, leading dimension ne)
+__global__ void gather_ext_rows_kernel(const double* __restrict__ src, long long lds, int cols, int r0, int nl,
+                                       const long long* __restrict__ piv, int k, double* __restrict__ dst,
+                                       long long ne) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= nl + k || c >= cols) return;
+  const long long g = i < nl ? r0 + i : piv[i - nl];
+  dst[c * ne + i] = src[c * lds + g];
+}
+
+cudaError_t launch_gather_ext_rows(const double* src, long long lds, int cols, int r0, int nl, const long long* piv,
+                                   int k, double* dst, long long ne, cudaStream_t st) {
+  if (cols <= 0) return cudaSuccess;
+  dim3 g(static_cast<unsigned>((nl + k + 255) / 256), cols);
+  gather_ext_rows_kernel<<<g, 256, 0, st>>>(src, lds, cols, r0, nl, piv, k, dst, ne);
+  return cudaGetLastError();
+}
+
+// piv_ext[q] = nl + q
+__global__ void iota_ll_kernel(long long* __restrict__ out, int k, long long base) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < k) out[q] = base + q;
+}
+cudaError_t launch_iota_ll(long long* out, int k, long long base, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  iota_ll_kernel<<<(k + 255) / 256, 256, 0, st>>>(out, k, base);
+  return cudaGetLastError();
+}
+
 }  // namespace gpk

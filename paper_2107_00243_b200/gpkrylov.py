@@ -549,13 +549,14 @@ def make_probes(n: int, count: int, seed: int) -> ProbeBatch:
 @dataclass
 class MllConfig:
     """gp_likelihood.hpp:26-32 (+ backward: 'fused' bilinear derivative pass, 'faithful' per-RHS
-    solves, or 'auto' = fused when every forward solve converged, else faithful)."""
+    solves, 'auto' = fused when every forward solve converged, else faithful, or
+    'fused_per_probe' = fused + per-probe backward gammas from (d+1) derivative MVMs)."""
     solver: CgConfig = field(default_factory=CgConfig)
     share_probes: bool = True
     backward: str = "auto"
 
     def c(self, with_gradient):
-        modes = {"fused": 0, "faithful": 1, "auto": 2}
+        modes = {"fused": 0, "faithful": 1, "auto": 2, "fused_per_probe": 3}
         if self.backward not in modes:
             raise InputError(f"MllConfig: unknown backward mode {self.backward!r}")
         return capi.gpk_mll_cfg(self.solver.c(), int(self.share_probes), int(with_gradient), modes[self.backward])

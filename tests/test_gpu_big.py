@@ -53,7 +53,8 @@ def c2_case(rank):
 
 @pytest.mark.parametrize("rank", [0, 100, 500])
 @pytest.mark.parametrize("precision,backward", [("tf32x3", "fused"), ("fp64", "faithful"), ("fp64", "fused"),
-                                                ("tf32x3", "faithful")])
+                                                ("tf32x3", "faithful"), ("tf32x3", "fused_per_probe"),
+                                                ("tf32x3", "auto")])
 def test_c2_evaluate_mll_matches_oracle(rank, precision, backward):
     g, w, x, y = c2_case(rank)
     op = operator(w, x)
@@ -77,10 +78,13 @@ def test_c2_evaluate_mll_matches_oracle(rank, precision, backward):
                                atol=1e-4 * np.abs(g["forward_gammas"]).max())
     assert abs(np.mean(r.forward_cg_iterations) - np.mean(g["forward_cg_iterations"])) <= 0.1 * np.mean(
         g["forward_cg_iterations"])
-    if backward == "faithful":
-        # per-probe backward gammas of the reference-faithful mode (trace_estimation.hpp:190-224)
+    assert r.backward_mode_used == ("faithful" if backward == "faithful" else "fused")
+    if backward in ("faithful", "fused_per_probe"):
+        # per-probe backward gammas (trace_estimation.hpp:190-224): the faithful mode's own
+        # solves, or s_i' dK_w z_i from the converged probe solves (no backward solves)
         bg = np.array(g["backward_gammas"])
         np.testing.assert_allclose(r.backward_gammas, bg, rtol=1e-3, atol=1e-4 * np.abs(bg).max())
+    if backward == "faithful":
         assert abs(r.total_cg_iterations - g["total_cg_iterations"]) <= 0.1 * g["total_cg_iterations"]
 
 

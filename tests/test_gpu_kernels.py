@@ -52,7 +52,7 @@ def test_mvm_fp32_matches_oracle(orc, fam, n, d, t, precision):
 
 @pytest.mark.parametrize("fam", ["rbf", "matern32", "matern52"])
 @pytest.mark.parametrize("n,d,t", [(1000, 3, 9), (2051, 9, 51), (700, 18, 65), (300, 32, 130), (129, 1, 1),
-                                   (4100, 11, 8)])
+                                   (4100, 11, 8), (640, 30, 51), (5000, 18, 51)])
 @pytest.mark.parametrize("variant", ["direct", "gram"])
 def test_mvm_tc_variants_match_oracle(orc, fam, n, d, t, variant):
     # both kernel-entry strategies of the tensor-core MVM: fp32 direct differences, and
@@ -63,7 +63,8 @@ def test_mvm_tc_variants_match_oracle(orc, fam, n, d, t, variant):
     want = orc.kernel_apply(orc.FAMILIES[fam], x, p, v)
     op = op_for(orc, fam, x, p).set_mvm_variant(variant)
     got = op.apply(v, precision="tf32x3")
-    assert op.mvm_variant()[0] == variant
+    # the Gram MMA runs on d + 2 augmented coordinates (<= 32): d > 30 falls back to direct
+    assert op.mvm_variant()[0] == (variant if d <= 30 else "direct")
     assert rel(got, want) < 3e-6
     for c in range(t):
         assert rel(got[:, c], want[:, c]) < 1e-5
@@ -204,3 +205,28 @@ def test_woodbury_solve_and_logdet(orc):
     p0 = gk.pivoted_cholesky(op, 0)
     assert np.allclose(p0.solve(v[:, 0]), v[:, 0] / 0.02, rtol=1e-15)
     assert p0.logdet() == pytest.approx(n * math.log(0.02), rel=1e-14)
+
+
+@pytest.mark.parametrize("variant,fam,d", [("gram", "matern32", 18), ("gram", "rbf", 9), ("direct", "matern52", 3)])
+def test_tcg_persistent_multi_unit_ctas_bitwise(orc, monkeypatch, variant, fam, d):
+    """The persistent tcgen05 MVM grid runs contiguous (row block, split) units per CTA.  Capping
+    the grid (test hook GPK_TCG_CTAS) forces many units per CTA -- row-block changes (the CTA
+    barrier, the new TMEM row operand) and same-row split changes (flipped mbarrier phases, the
+    unit-indexed split slots, the accumulator reset) -- and must give bitwise the full grid's
+    rows, which match the oracle (these paths only ran at the C2 bench shape)."""
+    n, t = 9000, 51  # 71 row blocks x several 64-tile splits
+    x = orc.random_matrix(n, d, 77)
+    p = orc.Params(d, 1.0, 0.9 * math.sqrt(d), 0.01)
+    v = orc.random_matrix(n, t, 78)
+    full = op_for(orc, fam, x, p).set_mvm_variant(variant)
+    want_gpu = full.apply(v, precision="tf32x3")
+    assert full.mvm_variant()[0] == variant
+    for cap in (7, 29):
+        monkeypatch.setenv("GPK_TCG_CTAS", str(cap))
+        capped = op_for(orc, fam, x, p).set_mvm_variant(variant)
+        got = capped.apply(v, precision="tf32x3")
+        assert np.array_equal(got, want_gpu), cap
+    monkeypatch.delenv("GPK_TCG_CTAS")
+    rows = np.arange(0, n, 37)
+    want = orc.kernel_apply_rows(orc.FAMILIES[fam], x, p, rows, v)
+    assert rel(want_gpu[rows], want) < 3e-6

@@ -13,6 +13,10 @@ from paper_2107_00243_b200.gpkrylov import RankGroup
 pytestmark = pytest.mark.gpu
 
 
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
 def run_ranks(world, fn):
     group = RankGroup(world)
     out, errs = [None] * world, []
@@ -109,3 +113,42 @@ def test_sharded_identity_and_mbcg(orc):
         for c in range(4):
             assert abs(res[c].iterations_used - ref[c].iterations_used) <= max(1, ref[c].iterations_used // 10)
             np.testing.assert_allclose(res[c].solution[r0:r1], ref[c].solution[r0:r1], rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("fam,rank", [("matern32", 40), ("rbf", 64)])
+def test_sharded_preconditioner_matches_single_rank(orc, world, fam, rank):
+    """Row-sharded preconditioner build: each rank factors only its own rows --
+    per step a (max, lowest global index) all-gather and the pivot row from its owner -- so the
+    pivot sequence, the remaining diagonal and every row of L are BITWISE the single-rank ones
+    (the per-row arithmetic is the persistent kernel's); the Woodbury inner matrix and the
+    traces are rank-ordered sums (1e-12), the derivative factors are each rank's rows of the
+    same recursion on [own rows + pivot rows] (1e-10 against the oracle)."""
+    n, d = 1300, 3
+    x = orc.random_matrix(n, d, 601)
+    hp = gk.Hyperparameters.from_raw(d, 1.1, 0.7, 0.03)
+    op1 = gk.KernelOperator(gk.KernelSpec(fam), x, hp)
+    pc1, rem1 = gk.pivoted_cholesky(op1, rank, want_remaining=True)
+    pc1 = gk.pivoted_cholesky_with_derivatives(op1, rank)
+    L1 = pc1.factor()
+
+    def fn(group, r):
+        op = gk.KernelOperator(gk.KernelSpec(fam), x, hp, shard=(group, r))
+        pc, rem = gk.pivoted_cholesky(op, rank, want_remaining=True)
+        piv = pc.pivots()
+        pcd = gk.pivoted_cholesky_with_derivatives(op, rank)
+        return piv, rem, pcd.factor(), [pcd.deriv_factor(w) for w in range(d + 1)], \
+            [pcd.trace_inv_deriv(w) for w in range(d + 2)], pcd.logdet()
+
+    res = run_ranks(world, fn)
+    want = orc.pivoted_cholesky(rank, family=orc.FAMILIES[fam], x=x, p=orc.Params(d, 1.1, 0.7, 0.03))
+    dls = orc.deriv_factors(orc.FAMILIES[fam], x, orc.Params(d, 1.1, 0.7, 0.03), want["L"], want["pivots"])
+    for piv, rem, L, dL, tr, ld in res:
+        assert piv == pc1.pivots() == list(want["pivots"])
+        assert np.array_equal(rem, rem1)
+        assert np.array_equal(L, L1)
+        for w in range(d + 1):
+            assert rel(dL[w], dls[w]) < 1e-10
+        for w in range(d + 2):
+            assert tr[w] == pytest.approx(pc1.trace_inv_deriv(w), rel=1e-11)
+        assert ld == pytest.approx(pc1.logdet(), rel=1e-13)
