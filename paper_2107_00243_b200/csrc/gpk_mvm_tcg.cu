@@ -52,18 +52,19 @@ __global__ void gram_pack_kernel(const double* __restrict__ X, long long ldx, in
   }
   const long long aoff = static_cast<long long>(n_pad) * 32;
   for (int k = 0; k < 32; ++k) {
+    // padded rows keep their 1 entries (with x~ = 0, n = 0): s(real i, padded j) = |x_i|^2 and
+    // s(padded i, real j) = |x_j|^2 as in the non-augmented form, never "near pairs" -- an
+    // all-zero image would make every entry of a padded row block a guard-path entry
     float vb = 0.0f, va = 0.0f;
-    if (real) {
-      if (k < d) {
-        vb = static_cast<float>((X[k * ldx + i] / ls[k] - mu[k]) * pre);
-        va = -2.0f * vb;
-      } else if (k == d) {
-        vb = 1.0f;
-        va = nrm;
-      } else if (k == d + 1) {
-        vb = nrm;
-        va = 1.0f;
-      }
+    if (k < d) {
+      vb = real ? static_cast<float>((X[k * ldx + i] / ls[k] - mu[k]) * pre) : 0.0f;
+      va = -2.0f * vb;
+    } else if (k == d) {
+      vb = 1.0f;
+      va = nrm;
+    } else if (k == d + 1) {
+      vb = nrm;
+      va = 1.0f;
     }
     const long long off = tile * 1024 + ((r >> 3) * 256 + (r & 7) * 32 + ((((k >> 2) ^ (r & 7))) << 2) + (k & 3));
     const float bh = tc::to_tf32(vb), ah = tc::to_tf32(va);

@@ -416,7 +416,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait_sleep(&a_empty[as], ((it / AS) & 1) ^ 1);
       // guard threshold of this tile: kGuard (|x_i|^2 + max_j |x_j|^2) bounds every pair's own
       // kGuard (|x_i|^2 + |x_j|^2), so a warp whose 8 entries all exceed it has no near pair
+#ifdef GPK_TCG_EXACT_GUARD  // experiment: every group takes the exact per-entry test
+      const float gthr = 3.0e38f;
+#else
       const float gthr = DIRECT ? 0.0f : kGuard * (ni + __ldg(Xtm + jt0 + lt));
+#endif
       // the thread's 16 Gram values in one TMEM load and the Gram buffer released right away
       // (measured: -2% at NC8 = 7; with NC8 > 8 the extra live registers cost 6%, so there the
       // two halves load separately)
