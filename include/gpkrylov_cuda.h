@@ -189,6 +189,9 @@ gpk_status gpk_evaluate_mll_device(gpk_ctx* ctx, const double* dy, const double*
 
 /* ---- probes (trace_estimation.hpp:27-36, common.hpp:93-98) --------------- */
 gpk_status gpk_make_probes(int64_t n, int count, uint64_t seed, double* out /* n x count col-major */);
+/* The same stream generated on the device (bitwise the host one), into HBM on the context's
+ * stream: the n x count block of an optimizer step (optimizer.hpp:452) never crosses PCIe. */
+gpk_status gpk_make_probes_device(gpk_ctx* ctx, int64_t n, int count, uint64_t seed, double* d_out);
 uint64_t gpk_mix_seed(uint64_t seed, uint64_t salt);
 
 /* ---- callers of the hot path ------------------------------ */

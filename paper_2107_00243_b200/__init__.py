@@ -8,7 +8,7 @@ kernels behind the C-ABI in include/gpkrylov_cuda.h (libgpkrylov_cuda.so);
 from .gpkrylov import (  # noqa: F401
     CgConfig, CgResult, CudaError, DiagPlusLowRank, Hyperparameters, IdentityPreconditioner, InputError,
     KernelOperator, KernelSpec, MllConfig, MllEvaluation, NumericalError, ProbeBatch, SolverError, SymTridiagonal,
-    batched_pcg, evaluate_mll, evaluate_mll_device, make_probes, mix_seed, mll_estimate, mll_gradient, pcg_solve,
+    batched_pcg, evaluate_mll, evaluate_mll_device, make_probes, make_probes_device, mix_seed, mll_estimate, mll_gradient, pcg_solve,
     pivoted_cholesky, pivoted_cholesky_deriv_factors, pivoted_cholesky_with_derivatives,
 )
 from .gpkrylov import (  # noqa: F401  SURVEY §8(f): the callers of the hot path

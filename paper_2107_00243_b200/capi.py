@@ -98,6 +98,7 @@ SIGNATURES = {
     "gpk_evaluate_mll_device": (C.c_int, [_V, _V, _V, C.c_int64, C.c_int, C.c_uint64, C.POINTER(gpk_mll_cfg),
                                           C.POINTER(gpk_mll_result)]),
     "gpk_make_probes": (C.c_int, [C.c_int64, C.c_int, C.c_uint64, _D]),
+    "gpk_make_probes_device": (C.c_int, [_V, C.c_int64, C.c_int, C.c_uint64, C.c_void_p]),
     "gpk_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "gpk_set_mvm_variant": (C.c_int, [_V, C.c_int]),
     "gpk_get_mvm_variant": (C.c_int, [_V, _I, _D]),

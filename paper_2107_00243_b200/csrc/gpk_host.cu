@@ -2943,6 +2943,15 @@ gpk_status gpk_make_probes(int64_t n, int count, uint64_t seed, double* out) {
   return guard(nullptr, [&] { make_probes_impl(n, count, seed, out); });
 }
 
+gpk_status gpk_make_probes_device(gpk_ctx* ctx, int64_t n, int count, uint64_t seed, double* d_out) {
+  return guard(ctx, [&] {
+    require(ctx != nullptr && d_out != nullptr, "make_probes: null context or output");
+    require(n >= 1, "make_probes: n must be >= 1");
+    require(count >= 1, "make_probes: need at least one probe");
+    ctx->check_launch(gpk::launch_make_probes(n, count, seed, d_out, ctx->st), 1, "make_probes");
+  });
+}
+
 uint64_t gpk_mix_seed(uint64_t seed, uint64_t salt) { return mix_seed_impl(seed, salt); }
 
 }  // extern "C"

@@ -43,6 +43,8 @@ cudaError_t launch_fused_kmvm(bool fp64, int family, int dp, int mode, const voi
 cudaError_t launch_fused_kmvm_f64g(int family, int dp, const double* X, const double* sq, int n, const double* V,
                                    long long ldv, int tc, double* out, long long ldo, double scale, int row_begin,
                                    int row_end, cudaStream_t st);
+// gpk_probes.cu: n x count Rademacher probes +-1/sqrt(n) from one mt19937_64(seed) stream, column-major
+cudaError_t launch_make_probes(long long n, int count, unsigned long long seed, double* out, cudaStream_t st);
 cudaError_t launch_reduce_splits(const double* part, int splits, long long split_stride, int t, int n,
                                  long long ldpart, double* out, long long ldo, cudaStream_t st);
 

@@ -34,8 +34,9 @@
 //   warp 1     : TMEM allocator + MMA issuer (converged warp, elected lane):
 //                G = A_x X_j^T (M=128, N=64, 3 x KS tf32 instructions) issued one
 //                tile AHEAD of Acc += K_tile V_j (M=128, N=NPAD, 4 x 3 f16 instructions)
-//   warps 2..17: 16 producer warps (TMEM lane group = warp % 4, 16-column slice of
-//                the j-tile = (warp - 2) / 4): Gram -> distance -> kernel shape ->
+//   warps 2, 3  : idle (register donors: setmaxnreg gives the producers 112 registers)
+//   warps 4..19: 16 producer warps (TMEM lane group = warp % 4, 16-column slice of
+//                the j-tile = (warp - 4) / 4): Gram -> distance -> kernel shape ->
 //                fp16 hi/lo -> TMEM; fp64 drain of their accumulator lanes.
 #pragma once
 #include <cuda_fp16.h>
@@ -50,7 +51,11 @@ constexpr int BK = 64;                    // j-tile
 constexpr int NPW = 16;                   // producer warps
 constexpr int RPT = 4;                    // producer warps per TMEM lane group
 constexpr int JPT = BK / RPT;             // entries per producer thread per tile (16)
-constexpr int THREADS = (2 + NPW) * 32;   // 576
+constexpr int THREADS = (4 + NPW) * 32;   // 640: warpgroup 0 = TMA issuer, MMA issuer, two idle register donors
+// setmaxnreg: the 128 x (96 - 32) registers warpgroup 0 releases = the 512 x (112 - 96) the producers acquire
+// (setmaxnreg.inc draws on the CTA's own released registers only)
+constexpr int REGS_ISSUE = 32, REGS_PROD = 112;
+constexpr int kConv = 4;                   // accumulation groups summed in fp32 (RN) per fp64 add
 constexpr int SG = 4;                     // X_j / V_j stages
 constexpr int AS = 2;                     // kernel-tile stages (TMEM)
 constexpr int MAX_NPAD = 96;
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   auto u_jt0 = [&](int u) { return (u - (u / S) * S) * per; };
   auto u_nt = [&](int u) { return min(u_jt0(u) + per, ntiles) - u_jt0(u); };
   auto u_newrow = [&](int u) { return u == u0 || u_rb(u) != u_rb(u - 1); };
-  auto row_barrier = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(THREADS) : "memory"); };
+  auto row_barrier = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(THREADS - 64) : "memory"); };  // all but the idle warps
   const int F = a.flush > 0 ? a.flush : 1;
   if (threadIdx.x == 0) GPK_TRACE(0, 0);
 
@@ -229,6 +234,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS_ISSUE));
   if (warp == 0) {
     // ---------------- TMA producer (converged warp, elected lane) ----------------
     const uint32_t xjb = static_cast<uint32_t>(BK * a.dp * 4);
@@ -335,16 +342,27 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       }
     }
+  }
   } else {
     // ---------------- producer / epilogue warps ----------------
-    const int pw = warp - 2;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS_PROD));
+    const int pw = warp - 4;
     const int lg = warp & 3;   // TMEM lane group
     const int q = pw >> 2;     // 16-column slice of the j-tile, and column-chunk subset of the drain
     const int r = lg * 32 + lane;
     const uint32_t tlane = static_cast<uint32_t>(lg * 32) << 16;
+    // fp32 TMEM groups are summed in fp32 registers (round to nearest) kConv at a time before the
+    // fp64 add: the F2F.F64.F32 conversions share the XU pipe with the MUFUs of the entries
+    constexpr bool TWO_LEVEL = HC <= 2;
     double acc64[HC * 8];
+    float acc32[TWO_LEVEL ? HC * 8 : 1];
+    int n32 = 0;
 #pragma unroll
     for (int e = 0; e < HC * 8; ++e) acc64[e] = 0.0;
+    if constexpr (TWO_LEVEL) {
+#pragma unroll
+      for (int e = 0; e < HC * 8; ++e) acc32[e] = 0.0f;
+    }
     float xi[DIRECT ? DPD : 1];
     unsigned it = 0, gce = 0, rl = 0;
     int row = 0;
@@ -385,6 +403,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     }  // new row block
+    auto flush32 = [&]() {
+      if constexpr (TWO_LEVEL) {
+#pragma unroll
+        for (int e = 0; e < HC * 8; ++e) {
+          acc64[e] += static_cast<double>(acc32[e]);
+          acc32[e] = 0.0f;
+        }
+        n32 = 0;
+      }
+    };
     auto drain = [&](unsigned g) {
       const int buf = g & 1;
       mbar_wait_sleep(&acc_full[buf], (g >> 1) & 1);
@@ -397,12 +425,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::tmem_ld8(tmem_base + tlane + T_ACC + buf * NPAD + c8 * 8, v);
           tc::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc64[h * 8 + e] += static_cast<double>(__uint_as_float(v[e]));
+          for (int e = 0; e < 8; ++e) {
+            if constexpr (TWO_LEVEL) acc32[h * 8 + e] += __uint_as_float(v[e]);
+            else acc64[h * 8 + e] += static_cast<double>(__uint_as_float(v[e]));
+          }
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&acc_empty[buf]);
+      if constexpr (TWO_LEVEL) {
+        if (++n32 == kConv) flush32();
+      }
     };
     for (int lt = 0; lt < nt; ++lt, ++it) {
       const int s = it % SG, as = it % AS, gb = it & 1;
@@ -424,7 +458,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // the thread's 16 Gram values in one TMEM load and the Gram buffer released right away
       // (measured: -2% at NC8 = 7; with NC8 > 8 the extra live registers cost 6%, so there the
       // two halves load separately)
-      constexpr bool G16 = !DIRECT && NC8 <= 8;
+      constexpr bool G16 = !DIRECT;  // (with 112 registers per producer thread the single load also pays for NC8 > 8)
       uint32_t gv16[G16 ? 16 : 8];
       if constexpr (G16) {
         tmem_ld16(tmem_base + tlane + T_GRAM + gb * BK + q * JPT, gv16);
@@ -531,6 +565,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lt % F == 0 && lt > 0) drain(gce++);
     }
     drain(gce++);
+    flush32();
     if (threadIdx.x == 64) GPK_TRACE(0, 2);
     if (row < a.row_end) {
       double* o = out + static_cast<long long>(u - u_rb(u) * S) * a.split_stride;

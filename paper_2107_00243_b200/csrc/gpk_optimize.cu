@@ -96,7 +96,7 @@ class Driver {
       r.gradient = grad.data();
       gpk_mll_cfg c = mc_;
       c.with_gradient = 1;
-      s = gpk_evaluate_mll(tr_, y_, probes_.data(), n_, l_, probe_seed_, &c, &r);
+      s = gpk_evaluate_mll_device(tr_, dy_.p, dprobes_.p, n_, l_, probe_seed_, &c, &r);
       if (s == GPK_OK) {
         cg_iters_ += r.total_cg_iterations;
         const Vec cg = collapse(grad);
@@ -117,21 +117,19 @@ class Driver {
   }
 
   // ---- begin_step hook (:448-453): preconditioner at the step's iterate, fresh probes
-  // The host mt19937_64 probe stream (trace_estimation.hpp:27-36, 0.47 s at n = 2^20, l = 64)
-  // is drawn on a host thread while the device builds the preconditioner.
+  // The mt19937_64 probe stream (trace_estimation.hpp:27-36) is generated on the device
+  // (gpk_probes.cu, bitwise the host stream) behind the preconditioner build on the context's
+  // stream; y was uploaded once.  Nothing of size n crosses PCIe during the optimization.
   void begin_step(int step, const Vec& x) {
     const Vec th = full_theta(x);
     must(set_params(tr_, th), tr_);
     probe_seed_ = gpk_mix_seed(seed_, static_cast<uint64_t>(step));
-    probes_.resize(static_cast<size_t>(n_) * l_);
-    gpk_status probe_rc = GPK_OK;
-    std::thread draw([&] { probe_rc = gpk_make_probes(n_, l_, probe_seed_, probes_.data()); });
-    struct Join {
-      std::thread& t;
-      ~Join() {
-        if (t.joinable()) t.join();
-      }
-    } join{draw};
+    if (dy_.p == nullptr) {
+      dy_.alloc(static_cast<size_t>(n_));
+      if (cudaMemcpy(dy_.p, y_, sizeof(double) * static_cast<size_t>(n_), cudaMemcpyHostToDevice) != cudaSuccess)
+        throw Fatal{GPK_CUDA_ERROR, "optimize: upload of y failed"};
+      dprobes_.alloc(static_cast<size_t>(n_) * l_);
+    }
     if (rank_ < 0) {
       must(gpk_precond_identity(tr_), tr_);
     } else {
@@ -141,8 +139,7 @@ class Driver {
            tr_);
       must(gpk_precond_deriv_factors(tr_), tr_);
     }
-    draw.join();
-    if (probe_rc != GPK_OK) throw Fatal{probe_rc, "make_probes: invalid arguments"};
+    must(gpk_make_probes_device(tr_, n_, l_, probe_seed_, dprobes_.p), tr_);
   }
 
   // ---- validation metric (:455-471): dense mll_exact per point, or the identity-
@@ -156,10 +153,13 @@ class Driver {
       must(gpk_mll_exact(va_, yv_, &v, nullptr), va_);
       return -v / static_cast<double>(nv_);
     }
-    if (vprobes_.empty()) {
+    if (dvprobes_.p == nullptr) {
       vseed_ = gpk_mix_seed(seed_, 0x7a11ULL);
-      vprobes_.resize(static_cast<size_t>(nv_) * l_);
-      must(gpk_make_probes(nv_, l_, vseed_, vprobes_.data()), va_);
+      dyv_.alloc(static_cast<size_t>(nv_));
+      if (cudaMemcpy(dyv_.p, yv_, sizeof(double) * static_cast<size_t>(nv_), cudaMemcpyHostToDevice) != cudaSuccess)
+        throw Fatal{GPK_CUDA_ERROR, "optimize: upload of the validation targets failed"};
+      dvprobes_.alloc(static_cast<size_t>(nv_) * l_);
+      must(gpk_make_probes_device(va_, nv_, l_, vseed_, dvprobes_.p), va_);
     }
     must(gpk_precond_identity(va_), va_);
     gpk_mll_cfg c = mc_;
@@ -167,7 +167,7 @@ class Driver {
     gpk_mll_result r{};
     Vec grad(static_cast<size_t>(d_ + 2), 0.0);
     r.gradient = grad.data();
-    must(gpk_evaluate_mll(va_, yv_, vprobes_.data(), nv_, l_, vseed_, &c, &r), va_);
+    must(gpk_evaluate_mll_device(va_, dyv_.p, dvprobes_.p, nv_, l_, vseed_, &c, &r), va_);
     return -r.value / static_cast<double>(nv_);
   }
 
@@ -431,7 +431,19 @@ class Driver {
   gpk_mll_cfg mc_;
   uint64_t seed_;
   int64_t dense_limit_;
-  Vec probes_, vprobes_;
+  struct DevBuf {  // device allocation owned by the driver
+    double* p = nullptr;
+    void alloc(size_t count) {
+      if (cudaMalloc(reinterpret_cast<void**>(&p), sizeof(double) * count) != cudaSuccess) {
+        p = nullptr;
+        throw Fatal{GPK_CUDA_ERROR, "optimize: device allocation failed"};
+      }
+    }
+    ~DevBuf() {
+      if (p) cudaFree(p);
+    }
+  };
+  DevBuf dy_, dprobes_, dyv_, dvprobes_;
   uint64_t probe_seed_ = 0, vseed_ = 0;
   std::vector<StepRow> steps_;
   std::vector<EvalRow> evals_;

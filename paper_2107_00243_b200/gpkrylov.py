@@ -543,6 +543,23 @@ def make_probes(n: int, count: int, seed: int) -> ProbeBatch:
     return ProbeBatch(z, int(seed), int(count))
 
 
+def make_probes_device(k: "KernelOperator", count: int, seed: int, device=0):
+    """The same stream generated by the device kernel (gpk_probes.cu) on the operator's stream,
+    into a torch cuda tensor of shape (count, n) -- column c of the reference's n x count block is
+    row c (the layout evaluate_mll_device takes); bitwise make_probes."""
+    import torch
+
+    n = k.rows()
+    if count < 1:
+        raise InputError("make_probes: need at least one probe")
+    z = torch.empty((count, n), dtype=torch.float64, device=f"cuda:{device}")
+    k.ctx.check(k.ctx.lib.gpk_make_probes_device(k.ctx.h, int(n), int(count), C.c_uint64(seed),
+                                                 C.c_void_p(z.data_ptr())))
+
+    torch.cuda.synchronize()  # the library stream is not torch's: the caller may read z right away
+    return z
+
+
 # ---------------------------------------------------------------------------
 # gp_likelihood.hpp
 # ---------------------------------------------------------------------------

@@ -1,11 +1,15 @@
-"""Row sharding of the mBCG hot path across ranks (one process per GPU).
+"""TEST MODEL (not product code): numpy / torch.distributed restatement of the row sharding
+that the C++ driver implements (gpk_host.cu shard_of / apply_kernel / psolve / the sharded
+pivoted Cholesky), so that the decomposition can be exercised at world size 2 over gloo on CPU.
 
 Host-side logic of the multi-GPU design, expressed with
 torch.distributed collectives so it runs over NCCL on B200s and over gloo on
 CPU (tests/test_sharding_gloo.py):
 
 * every n-length array (CG state, L, C, dL) is split into contiguous row
-  shards; shard sizes differ by at most one row;
+  shards of whole 128-row blocks (the product's rule, gpk_host.cu shard_of: a fused-MVM
+  row block never straddles ranks; tests/test_gpu_sharded.py checks gpk_shard_rows
+  against shard_range);
 * per CG iteration the direction block is all-gathered (each rank needs all
   columns' values at all rows for its K rows x all-j contraction) and the
   per-column partial dot products are all-reduced;
@@ -24,13 +28,15 @@ import numpy as np
 
 
 def shard_range(n: int, rank: int, world: int):
-    """Contiguous, balanced [start, stop) row range of `rank`."""
+    """[start, stop) row range of `rank`: contiguous runs of 128-row blocks, block counts
+    balanced to within one (gpk_host.cu shard_of, bit for bit)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
-    base, extra = divmod(n, world)
-    start = rank * base + min(rank, extra)
-    stop = start + base + (1 if rank < extra else 0)
-    return start, stop
+    nb = (n + 127) // 128
+    base, extra = divmod(nb, world)
+    b0 = rank * base + min(rank, extra)
+    b1 = b0 + base + (1 if rank < extra else 0)
+    return min(n, b0 * 128), min(n, b1 * 128)
 
 
 def allreduce_sum_fixed(x: np.ndarray, dist) -> np.ndarray:

@@ -230,3 +230,18 @@ def test_tcg_persistent_multi_unit_ctas_bitwise(orc, monkeypatch, variant, fam, 
     rows = np.arange(0, n, 37)
     want = orc.kernel_apply_rows(orc.FAMILIES[fam], x, p, rows, v)
     assert rel(want_gpu[rows], want) < 3e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,count,seed", [(1, 1, 0), (311, 1, 5489), (312, 2, 1), (313, 3, 17), (1000, 7, 2 ** 63 + 11),
+                                           (16384, 50, 0x9E3779B97F4A7C15)])
+def test_device_probes_equal_host_stream(orc, n, count, seed):
+    """gpk_make_probes_device (block-parallel MT19937-64 on the device, gpk_probes.cu) is bitwise
+    the host std::mt19937_64 stream of trace_estimation.hpp:27-36 -- and the oracle's own."""
+    x = orc.random_matrix(max(n, 2), 2, 1)[:n]
+    op = gk.KernelOperator(gk.KernelSpec("rbf"), x, gk.Hyperparameters.from_raw(2, 1.0, 1.0, 0.1))
+    z = gk.make_probes_device(op, count, seed).cpu().numpy()  # (count, n)
+    host = gk.make_probes(n, count, seed).probes
+    assert z.shape == (count, n)
+    assert np.array_equal(z.T, host)
+    assert np.array_equal(host, orc.make_probes(n, count, seed))

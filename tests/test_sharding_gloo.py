@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2107_00243_b200 import sharding
+import sharding_model as sharding
 
 
 def _free_port():
@@ -40,13 +40,17 @@ def run(fn, world=2):
 
 
 def test_shard_ranges_partition_and_balance():
-    for n in (1, 7, 16384, 1048576):
+    # the product's rule (gpk_host.cu shard_of): contiguous runs of whole 128-row blocks, block
+    # counts balanced to within one -- a fused-MVM row block never straddles two ranks
+    for n in (1, 7, 1100, 16384, 45730, 1048576):
         for world in (1, 2, 3, 8):
             rs = [sharding.shard_range(n, r, world) for r in range(world)]
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
-            sizes = [b - a for a, b in rs]
-            assert max(sizes) - min(sizes) <= 1
+            assert all(a % 128 == 0 or a == n for a, _ in rs)
+            blocks = [(b - a + 127) // 128 for a, b in rs]
+            assert max(blocks) - min(blocks) <= 1
+    assert [sharding.shard_range(1100, r, 2) for r in range(2)] == [(0, 640), (640, 1100)]
 
 
 def _reduce_fn(rank, world, dist):
