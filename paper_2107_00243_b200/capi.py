@@ -153,6 +153,24 @@ class _Stubbed:
 _lib = None
 
 
+def _preload_nccl():
+    """The library links libnccl.so.2.  When PyTorch is installed its wheel bundles a (newer) NCCL
+    under the same soname; whichever copy is loaded first serves both, and torch cannot import on
+    top of an older system copy.  Load torch's copy first (if there is one) so that the import
+    order of torch and this package does not matter."""
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for base in (spec.submodule_search_locations if spec else []):
+            so = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(so):
+                C.CDLL(so, mode=C.RTLD_GLOBAL)
+                return
+    except Exception:
+        pass  # the system libnccl.so.2 on the loader path is used
+
+
 def lib():
     """Load the sm_100a library (raises if it was not built; never falls back)."""
     global _lib
@@ -160,6 +178,7 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ExtensionMissing(
                 f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        _preload_nccl()
         handle = C.CDLL(LIB_PATH)
         missing = []
         for name, (res, args) in SIGNATURES.items():

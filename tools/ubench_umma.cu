@@ -24,7 +24,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 }
 
-template <int KIND, int N, bool A_TMEM>
+template <int KIND, int N, bool A_TMEM, int NACC = 1>
 __global__ void __launch_bounds__(128, 1) k(long long* out, int reps) {
   extern __shared__ unsigned char raw[];
   const uint32_t base = (smem_u32(raw) + 1023u) & ~1023u;
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(128, 1) k(long long* out, int reps) {
     const uint64_t bdesc = desc_sw128(base), adesc = desc_sw128(base + 32768);
     long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
-      const uint32_t d = tm + 256, a = tm + (r & 7) * 8;
+      const uint32_t d = tm + 256 + (r % NACC) * 64, a = tm + (r & 7) * 8;  // NACC independent accumulator chains
       if constexpr (A_TMEM) {
         if constexpr (KIND == 0)
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d), "r"(a), "l"(bdesc), "r"(idesc), "r"(1u) : "memory");
@@ -73,11 +73,11 @@ __global__ void __launch_bounds__(128, 1) k(long long* out, int reps) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
 }
 
-template <int KIND, int N, bool A_TMEM>
+template <int KIND, int N, bool A_TMEM, int NACC = 1>
 void run(const char* name) {
   long long* d;
   cudaMalloc(&d, 16);
-  auto kk = k<KIND, N, A_TMEM>;
+  auto kk = k<KIND, N, A_TMEM, NACC>;
   cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   for (int reps : {16, 256}) {
     kk<<<1, 128, 100 * 1024>>>(d, reps);
@@ -103,5 +103,11 @@ int main() {
   run<1, 128, true>("tf32 M128 N128 K8  A=TMEM");
   run<1, 64, false>("tf32 M128 N64  K8  A=smem");
   run<0, 16, true>("f16  M128 N16  K16 A=TMEM");
+  // same instruction stream spread over 2 / 4 independent accumulators: is the floor a dependency latency?
+  run<0, 56, true, 2>("f16  N56 A=TMEM, 2 accumulators");
+  run<0, 56, true, 4>("f16  N56 A=TMEM, 4 accumulators");
+  run<1, 64, true, 2>("tf32 N64 A=TMEM, 2 accumulators");
+  run<1, 64, true, 4>("tf32 N64 A=TMEM, 4 accumulators");
+  run<0, 56, false, 4>("f16  N56 A=smem, 4 accumulators");
   return 0;
 }
