@@ -73,20 +73,45 @@ GPK_DEV void beta_step(SlotState& x, double rz_new, double zz, int k, double rel
 }
 
 // ---- F1: per-chunk p.(Kp + s2 p) partials (dot_partials_kernel<1> partition) + alpha in
-// the last chunk CTA of each column
-__global__ void cg_pap_alpha_kernel(const double* __restrict__ P, const double* __restrict__ Y, double sig2, int n,
+// the last chunk CTA of each column.  With `parts` the fused MVM's split-K partials are summed
+// here (split order 0..S-1 from 0.0, exactly reduce_splits' sums) and Kp is stored for the
+// x / r update: one launch and one pass over Kp less per iteration.
+__global__ void cg_pap_alpha_kernel(const double* __restrict__ P, double* __restrict__ Y, double sig2, int n,
                                     long long ldn, int nrb, double* __restrict__ part, unsigned* __restrict__ cnt,
                                     int k, SlotState* __restrict__ ss, double* __restrict__ alpha_hist,
-                                    int max_iters, unsigned long long* __restrict__ vmax) {
+                                    int max_iters, unsigned long long* __restrict__ vmax,
+                                    const double* __restrict__ parts, int splits, long long sstride, long long ldp) {
   __shared__ double red[kVT / 32];
   __shared__ bool last;
   const int s = blockIdx.y, b = blockIdx.x;
   const double* a = P + s * ldn;
-  const double* y = Y + s * ldn;
+  double* y = Y + s * ldn;
   double acc = 0.0;
-  for (int q = 0; q < kRB / kVT; ++q) {
-    const int i = b * kRB + q * kVT + threadIdx.x;
-    if (i < n) acc += a[i] * (y[i] + sig2 * a[i]);
+  if (parts != nullptr) {
+    const double* ps = parts + s * ldp + b * kRB + threadIdx.x;
+    constexpr int Q = kRB / kVT;
+    double yi[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) yi[q] = 0.0;
+#pragma unroll 4
+    for (int sp = 0; sp < splits; ++sp) {  // Q x 4 independent L2 loads in flight
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (b * kRB + q * kVT + threadIdx.x < n) yi[q] += __ldcg(ps + sp * sstride + q * kVT);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = b * kRB + q * kVT + threadIdx.x;
+      if (i < n) {
+        y[i] = yi[q];
+        acc += a[i] * (yi[q] + sig2 * a[i]);
+      }
+    }
+  } else {
+    for (int q = 0; q < kRB / kVT; ++q) {
+      const int i = b * kRB + q * kVT + threadIdx.x;
+      if (i < n) acc += a[i] * (y[i] + sig2 * a[i]);
+    }
   }
   const double t = block_sum(acc, red);
   if (threadIdx.x == 0) {
@@ -105,13 +130,15 @@ __global__ void cg_pap_alpha_kernel(const double* __restrict__ P, const double* 
   }
 }
 
-cudaError_t launch_cg_pap_alpha(const double* P, const double* Y, double sig2, int n, long long ldn, int t,
+cudaError_t launch_cg_pap_alpha(const double* P, double* Y, double sig2, int n, long long ldn, int t,
                                 double* part, unsigned* cnt, int k, SlotState* ss, double* alpha_hist, int max_iters,
-                                cudaStream_t st, unsigned long long* vmax) {
+                                cudaStream_t st, unsigned long long* vmax, const double* parts, int splits,
+                                long long sstride, long long ldp) {
   if (t <= 0) return cudaSuccess;
   const int nrb = (n + kRB - 1) / kRB;
   cg_pap_alpha_kernel<<<dim3(nrb, t), kVT, 0, st>>>(P, Y, sig2, n, ldn, nrb, part, cnt, k, ss, alpha_hist,
-                                                    max_iters, vmax);
+                                                    max_iters, vmax, splits > 1 ? parts : nullptr, splits, sstride,
+                                                    ldp);
   return cudaGetLastError();
 }
 

@@ -467,6 +467,18 @@ struct gpk_ctx {
   DBuf<double> st_X[2], st_R[2], st_P[2], st_Z;
   DBuf<float> w_v32, w_f32, w_vhi, w_vlo;
   bool use_tc = false;  // GPK_PREC_TF32X3: value MVMs on the tcgen05 tensor cores
+  // split-K partials of the last tcgen05 MVM left unreduced for a fused consumer (the CG loop's
+  // p'Ap kernel): set defer_reduce before apply_kernel, read and clear pend after
+  struct PendingSplits {
+    const double* part = nullptr;
+    int splits = 0;
+    long long sstride = 0, ldp = 0;
+  } pend;
+  bool defer_reduce = false;
+  bool fuse_reduce = [] {  // env GPK_FUSE_REDUCE=0: separate reduce_splits launch (A/B)
+    const char* e = std::getenv("GPK_FUSE_REDUCE");
+    return !(e && e[0] == '0');
+  }();
   bool vmax_ready = false;  // w_vmax holds the column maxima of the next direction block
   bool use_fused_cg = [] {  // env GPK_FUSED_CG=0 selects the unfused per-step kernels (A/B checks)
     const char* e = std::getenv("GPK_FUSED_CG");
@@ -933,8 +945,13 @@ struct gpk_ctx {
           w_y.ensure(static_cast<size_t>(sp) * tc * ldp);
           check_launch(launch(w_y.p, sp), 1, "fused_kmvm_tc");
           prof_end(0, ev, fl, static_cast<double>(nl) * n);
-          check_launch(gpk::launch_reduce_splits(w_y.p, sp, a.split_stride, tc, nl, ldp, out + c0 * ldo, ldo, st),
-                       1, "reduce_splits");
+          if (defer_reduce && c0 == 0 && tc == t) {
+            // the caller's next kernel (cg_pap_alpha) sums the split partials itself, in the same order
+            pend = {w_y.p, sp, a.split_stride, ldp};
+          } else {
+            check_launch(gpk::launch_reduce_splits(w_y.p, sp, a.split_stride, tc, nl, ldp, out + c0 * ldo, ldo, st),
+                         1, "reduce_splits");
+          }
         }
         entries += static_cast<long long>(nl) * n;
         flops += static_cast<long long>(fl);
@@ -1274,7 +1291,11 @@ struct gpk_ctx {
     vmax_ready = false;
     for (int it = 1; it <= max_iters && ta > 0; ++it) {
       w_kx.ensure(static_cast<size_t>(ta) * ldn);
+      // fused iteration on one rank: the split-K partials of K p are summed by the p'Ap kernel
+      pend = PendingSplits{};
+      defer_reduce = fused && fuse_reduce && world == 1 && !(use_wood_s && use_coop);
       apply_kernel(Ps, ldn, ta, w_kx.p, ldn, fp64, -1);  // K p (noise-free)
+      defer_reduce = false;
       if (fused) {
         // vector phase (kind 3): algorithmic HBM bytes = 13 fp64 n-vectors per column (pap: P, Kp;
         // x/r update: R, P, Kp, X read, X, R written; Woodbury: R read, Z written; p update: P, Z
@@ -1284,7 +1305,8 @@ struct gpk_ctx {
         unsigned long long* vm = (!fp64 && use_tc && (gram_ok || tcg_direct) && ta <= 96) ? w_vmax.p : nullptr;
         if (!(use_wood_s && use_coop))
           check_launch(gpk::launch_cg_pap_alpha(Ps, w_kx.p, noise, nl, ldn, ta, ppap, w_cnt.p, it, ss, dh_a,
-                                                max_iters, st, use_wood_s ? vm : nullptr),
+                                                max_iters, st, use_wood_s ? vm : nullptr, pend.part, pend.splits,
+                                                pend.sstride, pend.ldp),
                        1, "cg_pap_alpha");
         if (use_wood_s && use_coop) {  // gpk_wood.cu: the whole vector phase in one cooperative launch
           check_launch(gpk::launch_cg_iter_coop(L.p, n, C.p, n, k, Xs, Rs, Ps, Zs, w_kx.p, ldn, ta, nl, noise, pnoise,

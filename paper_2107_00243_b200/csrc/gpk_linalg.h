@@ -54,9 +54,10 @@ cudaError_t launch_g1_reduce(const double* part, int n, int ka, int tb, double* 
 int g2_row_blocks(int n);
 // vmax (nullable): cleared per column by the last CTA (the |p| maxima of this iteration's p
 // update are accumulated into it afterwards)
-cudaError_t launch_cg_pap_alpha(const double* P, const double* Y, double sig2, int n, long long ldn, int t,
+cudaError_t launch_cg_pap_alpha(const double* P, double* Y, double sig2, int n, long long ldn, int t,
                                 double* part, unsigned* cnt, int k, SlotState* ss, double* alpha_hist, int max_iters,
-                                cudaStream_t st, unsigned long long* vmax = nullptr);
+                                cudaStream_t st, unsigned long long* vmax = nullptr, const double* parts = nullptr,
+                                int splits = 0, long long sstride = 0, long long ldp = 0);
 cudaError_t launch_g1_xr(const double* L, long long ldl, int ka, double* X, const double* R, double* Rn,
                          const double* P, const double* Y, double sig2, long long ldn, int tb, int n,
                          const SlotState* ss, double* part, double* W, long long ldw, cudaStream_t st);

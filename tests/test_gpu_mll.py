@@ -318,11 +318,37 @@ def test_c1_auto_backward_follows_convergence(precision):
     if precision == "fp64":
         np.testing.assert_allclose(auto.gradient, g["gradient"], rtol=2e-4)
     else:
-        # a reduced-precision operator perturbs the truncated Krylov iterates themselves: the
-        # truncated gradient then moves by the order of the truncation error (measured 1.1-3.3x)
+        # a reduced-precision operator perturbs the truncated Krylov iterates themselves (kappa ~ 4e4,
+        # nothing converged): the truncated gradient then moves by the order of the truncation error --
+        # measured 1.1-3.3x of it with the round-1 accumulation order, 1.0-4.6x with round 2's fp32
+        # second-level sums; at most 1.8e-4 relative in either case
         ref = np.array(g["gradient"])
         trunc = np.abs(ref - np.array(json.load(open(os.path.join(GOLD, "c1_converged_oracle.json")))["gradient"]))
-        assert np.all(np.abs(auto.gradient - ref) <= 4.0 * trunc + 1e-4 * np.abs(ref))
+        assert np.all(np.abs(auto.gradient - ref) <= 8.0 * trunc + 1e-4 * np.abs(ref))
+        np.testing.assert_allclose(auto.gradient, ref, rtol=1e-3)
     # converged solves: 'auto' is the fused pass
     _, conv = _c1_eval(1000, precision, "auto")
     assert conv.unconverged_columns == 0 and conv.backward_mode_used == "fused"
+
+
+def test_fused_split_reduction_is_bitwise_the_separate_launch(orc, monkeypatch):
+    """The CG loop's p'Ap kernel sums the fused MVM's split-K partials itself (same split order
+    from 0.0 as reduce_splits): every iterate, hence the whole evaluation, is bitwise the one with
+    the separate reduction launch (GPK_FUSE_REDUCE=0)."""
+    n, d, l = 3000, 9, 6
+    x = orc.random_matrix(n, d, 91)
+    y = np.sin(x[:, 0]) + 0.1 * orc.random_matrix(n, 1, 92)[:, 0]
+    hp = gk.Hyperparameters.from_raw(d, 1.0, 1.5, 0.05)
+    z = gk.make_probes(n, l, gk.mix_seed(3, 1))
+    cfg = gk.MllConfig(gk.CgConfig(200, 1e-6, False, "tf32x3", 2), True, "fused")
+    got = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("GPK_FUSE_REDUCE", flag)
+        op = gk.KernelOperator(gk.KernelSpec("matern32"), x, hp)  # the switch is read per context
+        pc = gk.pivoted_cholesky_with_derivatives(op, 20)
+        got.append(gk.evaluate_mll(y, op, pc, z, cfg))
+    a, b = got
+    assert a.value == b.value and a.logdet == b.logdet
+    assert np.array_equal(a.gradient, b.gradient)
+    assert np.array_equal(a.forward_cg_iterations, b.forward_cg_iterations)
+    assert b.gpu_launches - a.gpu_launches >= a.solve_iterations  # one launch less per iteration
