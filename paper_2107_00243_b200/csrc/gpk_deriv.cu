@@ -144,33 +144,93 @@ __global__ void __launch_bounds__(kDThreads, 1)
 
     // W tile (4 x 4 per thread) = S[a, :] . Z[b, :]
     T w[4][4];
+    if constexpr (sizeof(T) == 4) {
+      // fp32: paired FFMA2 (two b columns per instruction): half the issue slots of the rank-l product
+      float2 w2[4][2];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) w[r][c] = T(0);
+      for (int r = 0; r < 4; ++r) w2[r][0] = w2[r][1] = make_float2(0.0f, 0.0f);
 #pragma unroll 5
-    for (int i = 0; i < l; ++i) {  // unrolled: the shared loads of later i are in flight early
-      T sa[4], zb[4];
-      if constexpr (sizeof(T) == 4) {  // one 128-bit shared load per operand quad
+      for (int i = 0; i < l; ++i) {  // unrolled: the shared loads of later i are in flight early
         const float4 va = *reinterpret_cast<const float4*>(Ss + i * kDA + ta * 4);
         const float4 vb = *reinterpret_cast<const float4*>(Zs + i * kDB + tb * 4);
-        sa[0] = va.x, sa[1] = va.y, sa[2] = va.z, sa[3] = va.w;
-        zb[0] = vb.x, zb[1] = vb.y, zb[2] = vb.z, zb[3] = vb.w;
-      } else {
+        const float sa[4] = {va.x, va.y, va.z, va.w};
+        const float2 z01 = make_float2(vb.x, vb.y), z23 = make_float2(vb.z, vb.w);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float2 s2 = make_float2(sa[r], sa[r]);
+          w2[r][0] = __ffma2_rn(s2, z01, w2[r][0]);
+          w2[r][1] = __ffma2_rn(s2, z23, w2[r][1]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        w[r][0] = w2[r][0].x;
+        w[r][1] = w2[r][0].y;
+        w[r][2] = w2[r][1].x;
+        w[r][3] = w2[r][1].y;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[r][c] = T(0);
+#pragma unroll 5
+      for (int i = 0; i < l; ++i) {
+        T sa[4], zb[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) sa[r] = Ss[i * kDA + ta * 4 + r];
 #pragma unroll
         for (int c = 0; c < 4; ++c) zb[c] = Zs[i * kDB + tb * 4 + c];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) w[r][c] = fma(sa[r], zb[c], w[r][c]);
       }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) w[r][c] = fma(sa[r], zb[c], w[r][c]);
     }
 
     T acc[NA];
 #pragma unroll
     for (int q = 0; q < NA; ++q) acc[q] = T(0);
+    if constexpr (sizeof(T) == 4 && DP % 2 == 0) {
+      // fp32: the d coordinate differences, their squares and the d lengthscale sums as paired
+      // FADD2 / FFMA2 / FMUL2 over two coordinates (same products and sums per coordinate as below)
+      float2 acc2[DP / 2];
+#pragma unroll
+      for (int k = 0; k < DP / 2; ++k) acc2[k] = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int bl = tb * 4 + c;
+        float2 xb2[DP / 2];
+#pragma unroll
+        for (int k = 0; k < DP / 2; ++k) xb2[k] = *reinterpret_cast<const float2*>(Xb + bl * DP + 2 * k);
+        const float ub = Ub[bl];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int al = ta * 4 + r;
+          float2 df[DP / 2];
+          float2 s2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int k = 0; k < DP / 2; ++k) {
+            const float2 xa2 = *reinterpret_cast<const float2*>(Xa + al * DP + 2 * k);
+            df[k] = __fadd2_rn(xa2, make_float2(-xb2[k].x, -xb2[k].y));
+            s2 = __ffma2_rn(df[k], df[k], s2);
+          }
+          float e, ds;
+          shape_pair<float, FAM>(s2.x + s2.y, e, ds);
+          const float q = fmaf(-cmix, w[r][c], Ua[al] * ub);  // u_a u_b - (n/l) W_ab
+          acc[0] = fmaf(e, q, acc[0]);
+          const float g = ds * q;
+          const float2 g2 = make_float2(g, g);
+#pragma unroll
+          for (int k = 0; k < DP / 2; ++k) acc2[k] = __ffma2_rn(__fmul2_rn(g2, df[k]), df[k], acc2[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < DP / 2; ++k) {
+        acc[1 + 2 * k] = acc2[k].x;
+        acc[2 + 2 * k] = acc2[k].y;
+      }
+    } else {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int bl = tb * 4 + c;
@@ -197,6 +257,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
 #pragma unroll
         for (int k = 0; k < DP; ++k) acc[1 + k] = fma(g, dd[k], acc[1 + k]);
       }
+    }
     }
 #pragma unroll
     for (int q = 0; q < NA; ++q) acc64[q] += static_cast<double>(acc[q]);
