@@ -544,6 +544,10 @@ struct gpk_ctx {
       return 0;
     return sms;
   }();
+  int tcg_unit_order = [] {  // env GPK_TCG_ORDER=0/1 forces the unit order (A/B); default: by operand footprint
+    const char* e = std::getenv("GPK_TCG_ORDER");
+    return e ? std::atoi(e) : -1;
+  }();
   // TEST HOOK (env GPK_TCG_CTAS=c): cap the persistent MVM grid at c CTAs without changing the
   // unit decomposition (splits_for_tcg keeps the SM count), so every CTA runs several units --
   // row-block changes and same-row split changes -- with results bitwise those of the full grid
@@ -916,6 +920,12 @@ struct gpk_ctx {
           a.jtiles_per_split = per64;
           a.ctas = (tcg_grid_cap > 0 && tcg_ctas > 0) ? std::min(tcg_ctas, tcg_grid_cap) : tcg_ctas;
           a.flush = tc_flush;  // 64-wide tiles: 128 entries per fp32 TMEM accumulation at the default 2
+          {
+            // operands of one full j sweep (fp16 V hi / lo, X images or rows, norms): beyond about half
+            // the 126 MB L2 the CTAs run the units strided so that they share every j-tile in time
+            const double foot = static_cast<double>(n_pad) * (4.0 * npad + (gram_ok ? 260.0 : 0.0) + 4.0 * dp);
+            a.unit_order = (tcg_unit_order >= 0 ? tcg_unit_order : (foot > 64e6 ? 1 : 0)) && a.ctas > 0 && sp > 1;
+          }
         } else {
           const int npad = gpk::tc_npad(tc);
           w_vhi.ensure(static_cast<size_t>(n_pad) * npad);

@@ -22,6 +22,7 @@ struct MvmArgs {
   int row_end;               // one past the last output row; outputs are stored at row - row_begin
   int dp;                    // padded coordinate count of the packed fp32 rows (Gram guard path)
   int ctas;                  // tcg MVM: persistent grid size (0: one CTA per (row block, split) unit)
+  int unit_order;            // tcg MVM, persistent grid: 0 = contiguous units per CTA, 1 = strided (all CTAs in one split)
 };
 
 // Packed-operand geometry for a given column count.

@@ -194,12 +194,23 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int S = (ntiles + per - 1) / per;
   const int nrb = (a.row_end - a.row_begin + BM - 1) / BM;
   const long long U = static_cast<long long>(nrb) * S;
+  // Unit order (a.unit_order).  0: u = rb * S + sp, CTA b runs the CONTIGUOUS units [b U / G, (b+1) U / G) --
+  // consecutive splits of one row block keep the pipeline and the row operand (small n: the operands
+  // are L2-resident anyway).  1: u = sp * nrb + rb, CTA b runs the STRIDED units b, b + G, b + 2 G, ... --
+  // at any time all CTAs sweep the SAME j-range (split), each for its own row block, nearly in lock
+  // step, so a j-tile is fetched from HBM once per time slot instead of once per CTA (n = 2^20: the
+  // operands are 630 MB, 5x the L2; contiguous order measured 3.99 TB of DRAM reads per launch at an
+  // L2 hit rate of 15%, profiles/r2_mvm_c5_ncu.txt).
+  const bool strided = a.unit_order == 1;
   const int u0 = static_cast<int>(blockIdx.x * U / gridDim.x);
   const int u1 = static_cast<int>((blockIdx.x + 1) * U / gridDim.x);
-  auto u_rb = [&](int u) { return u / S; };
-  auto u_jt0 = [&](int u) { return (u - (u / S) * S) * per; };
+  const int nu = strided ? (U > blockIdx.x ? static_cast<int>((U - 1 - blockIdx.x) / gridDim.x) + 1 : 0) : u1 - u0;
+  auto uid = [&](int w) { return strided ? w * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x) : u0 + w; };
+  auto u_rb = [&](int u) { return strided ? u % nrb : u / S; };
+  auto u_sp = [&](int u) { return strided ? u / nrb : u - (u / S) * S; };
+  auto u_jt0 = [&](int u) { return u_sp(u) * per; };
   auto u_nt = [&](int u) { return min(u_jt0(u) + per, ntiles) - u_jt0(u); };
-  auto u_newrow = [&](int u) { return u == u0 || u_rb(u) != u_rb(u - 1); };
+  auto w_newrow = [&](int w) { return w == 0 || u_rb(uid(w)) != u_rb(uid(w - 1)); };
   auto row_barrier = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(THREADS - 64) : "memory"); };  // all but the idle warps
   const int F = a.flush > 0 ? a.flush : 1;
   if (threadIdx.x == 0) GPK_TRACE(0, 0);
@@ -240,10 +251,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- TMA producer (converged warp, elected lane) ----------------
     const uint32_t xjb = static_cast<uint32_t>(BK * a.dp * 4);
     unsigned it = 0;  // unsigned: stage / phase arithmetic without sign fix-ups
-    for (int u = u0; u < u1; ++u) {
+    for (int w = 0; w < nu; ++w) {
+    const int u = uid(w);
     const int jt0 = u_jt0(u), nt = u_nt(u);
-    if (u_newrow(u)) {
-      if (u != u0) row_barrier();
+    if (w_newrow(w)) {
+      if (w != 0) row_barrier();
       const int row0 = a.row_begin + u_rb(u) * BM;
       if (elect_one()) {
         mbar_arrive_expect_tx(xi_full, BM * a.dp * 4);
@@ -301,15 +313,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) GPK_TRACE(7, k);
       };
       unsigned it = 0, gc = 0, rl = 0;
-      for (int u = u0; u < u1; ++u) {
+      for (int w = 0; w < nu; ++w) {
+      const int u = uid(w);
       const int nt = u_nt(u);
-      if (u_newrow(u)) {
-        if (u != u0) row_barrier();
+      if (w_newrow(w)) {
+        if (w != 0) row_barrier();
         if constexpr (!DIRECT) mbar_wait_sleep(ax_ready, rl & 1);
         ++rl;
         gram(it);
       }
-      const bool next_same_row = u + 1 < u1 && !u_newrow(u + 1);
+      const bool next_same_row = w + 1 < nu && !w_newrow(w + 1);
       for (int lt = 0; lt < nt; ++lt, ++it) {
         // the next Gram tile overlaps this tile's kernel-shape evaluation (not across a row change)
         if (lt + 1 < nt || next_same_row) gram(it + 1);
@@ -351,9 +364,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = pw >> 2;     // 16-column slice of the j-tile, and column-chunk subset of the drain
     const int r = lg * 32 + lane;
     const uint32_t tlane = static_cast<uint32_t>(lg * 32) << 16;
+    // (every NC8: 112 registers hold 24 fp32 + 24 fp64 sums without spilling)
     // fp32 TMEM groups are summed in fp32 registers (round to nearest) kConv at a time before the
     // fp64 add: the F2F.F64.F32 conversions share the XU pipe with the MUFUs of the entries
-    constexpr bool TWO_LEVEL = HC <= 2;
+    constexpr bool TWO_LEVEL = true;
     double acc64[HC * 8];
     float acc32[TWO_LEVEL ? HC * 8 : 1];
     int n32 = 0;
@@ -367,10 +381,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     unsigned it = 0, gce = 0, rl = 0;
     int row = 0;
     float ni = 0.0f;
-    for (int u = u0; u < u1; ++u) {
+    for (int w = 0; w < nu; ++w) {
+    const int u = uid(w);
     const int jt0 = u_jt0(u), nt = u_nt(u);
-    if (u_newrow(u)) {
-    if (u != u0) row_barrier();
+    if (w_newrow(w)) {
+    if (w != 0) row_barrier();
     row = a.row_begin + u_rb(u) * BM + r;
     ni = DIRECT ? 0.0f : Xn[row];
     if constexpr (!DIRECT) {  // this row's centred coordinates (tf32 hi / lo, columns q*8 .. q*8+7) -> A_x in TMEM
@@ -568,7 +583,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     flush32();
     if (threadIdx.x == 64) GPK_TRACE(0, 2);
     if (row < a.row_end) {
-      double* o = out + static_cast<long long>(u - u_rb(u) * S) * a.split_stride;
+      double* o = out + static_cast<long long>(u_sp(u)) * a.split_stride;
 #pragma unroll
       for (int h = 0; h < HC; ++h) {
         const int c8 = q + h * RPT;

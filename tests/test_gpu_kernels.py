@@ -226,7 +226,19 @@ def test_tcg_persistent_multi_unit_ctas_bitwise(orc, monkeypatch, variant, fam, 
         capped = op_for(orc, fam, x, p).set_mvm_variant(variant)
         got = capped.apply(v, precision="tf32x3")
         assert np.array_equal(got, want_gpu), cap
-    monkeypatch.delenv("GPK_TCG_CTAS")
+    # strided unit order (what large n uses so that all CTAs share a j-range in the L2): the same
+    # (row block, split) units with the same split slots, handed out b, b + G, b + 2 G, ... -- every
+    # unit then starts a new row block -- bitwise the contiguous order
+    for cap in (7, 29, 0):
+        if cap:
+            monkeypatch.setenv("GPK_TCG_CTAS", str(cap))
+        else:
+            monkeypatch.delenv("GPK_TCG_CTAS")
+        monkeypatch.setenv("GPK_TCG_ORDER", "1")
+        strided = op_for(orc, fam, x, p).set_mvm_variant(variant)
+        got = strided.apply(v, precision="tf32x3")
+        assert np.array_equal(got, want_gpu), ("strided", cap)
+    monkeypatch.delenv("GPK_TCG_ORDER")
     rows = np.arange(0, n, 37)
     want = orc.kernel_apply_rows(orc.FAMILIES[fam], x, p, rows, v)
     assert rel(want_gpu[rows], want) < 3e-6
