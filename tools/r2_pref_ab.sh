@@ -1,8 +1,8 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
 timeout 60 python tools/prof_mvm.py 2048 9 51 matern32 tf32x3 3 || { echo HANG; exit 1; }
-for w in C2 C3 C5; do
-  echo "== $w prefetch"; timeout 200 python tools/prof_mvm.py $w tf32x3 10 || { echo HANG; exit 1; }
-  echo "== $w no prefetch"; GPK_LIB_PATH=paper_2107_00243_b200/lib_exp/libgpk_nopref.so timeout 200 python tools/prof_mvm.py $w tf32x3 10 2>&1 | grep -v Warn
+for w in C2 C3 C4 C5; do
+  echo "== $w 16-entry block"; timeout 200 python tools/prof_mvm.py $w tf32x3 10 || { echo HANG; exit 1; }
+  echo "== $w previous (two blocks of 8)"; GPK_LIB_PATH=paper_2107_00243_b200/lib_exp/libgpk_prev.so timeout 200 python tools/prof_mvm.py $w tf32x3 10 2>&1 | grep -v Warn
 done
 timeout 600 python -m pytest tests/test_gpu_kernels.py -m gpu -x -q -k "mvm or tcg" 2>&1 | tail -3
