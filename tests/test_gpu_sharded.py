@@ -68,6 +68,27 @@ def test_sharded_mvm_rows_bitwise(orc, world):
             assert np.array_equal(res[p], ref[p][r0:r1]), p
 
 
+def test_sharded_mvm_rows_bitwise_strided_units(orc, monkeypatch):
+    """The strided unit order of the persistent tcgen05 MVM (what n = 2^20 uses) on a shard: a rank's
+    rows are still bitwise the unsharded rows (d = 9: the Gram variant; the grid capped so that every
+    CTA runs several strided units of the rank's own row blocks)."""
+    n, d, t = 5000, 9, 20
+    x = orc.random_matrix(n, d, 601)
+    hp = gk.Hyperparameters.from_raw(d, 1.0, 2.5, 0.05)
+    v = orc.random_matrix(n, t, 602)
+    ref = gk.KernelOperator(gk.KernelSpec("matern32"), x, hp).apply(v, precision="tf32x3")
+    monkeypatch.setenv("GPK_TCG_ORDER", "1")
+    monkeypatch.setenv("GPK_TCG_CTAS", "11")
+
+    def fn(group, r):
+        op = gk.KernelOperator(gk.KernelSpec("matern32"), x, hp, shard=(group, r))
+        r0, r1 = op.shard_rows()
+        return r0, r1, op.apply(v, precision="tf32x3")[r0:r1]
+
+    for r0, r1, got in run_ranks(2, fn):
+        assert np.array_equal(got, ref[r0:r1])
+
+
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("precision,backward", [("fp64", "faithful"), ("fp64", "fused"), ("tf32x3", "fused")])
 def test_sharded_evaluate_matches_single_rank(orc, world, precision, backward):
