@@ -558,7 +558,7 @@ def main():
     gram = tc and r["mvm_variant"] == "gram"
     t_cols = w.probes + 1
     npad = 8 * ((t_cols + 7) // 8)
-    ks = (w.d + 7) // 8
+    ks = (w.d + 2 + 7) // 8  # Gram k-steps over the augmented coordinates [x~, 1, n]
     common = {"flops_per_launch": mvm["flops"] / max(mvm["launches"], 1),
               "avg_launch_ms": mvm["ms"] / max(mvm["launches"], 1),
               "launches_per_step": mvm["launches"] / max(args.steps, 1),
@@ -588,6 +588,15 @@ def main():
             sfu_peak = 148 * 16 * mhz * 1e6 / mufu
             roofline["sfu_bound"] = {"mufu_per_entry": mufu, "peak_entries_per_s": sfu_peak,
                                      "entries_per_s": entries_per_s, "frac": entries_per_s / sfu_peak}
+            # the tensor pipe's instruction floor: every tcgen05.mma with M = 128, N <= 96 costs ~51 cycles
+            # (tools/ubench_umma.cu, profiles/r2_mvm_pipeline_experiments.txt); per 128 x 64 tile the kernel
+            # issues 12 contraction MMAs (4 k-steps x {hi hi, hi lo, lo hi}) + 3 KS Gram MMAs
+            mmas = 12 + 3 * ks
+            floor_entries = 148 * mhz * 1e6 * (128 * 64) / (mmas * 51.0)
+            roofline["tensor_pipe_floor"] = {"mma_per_tile": mmas, "cycles_per_mma": 51.0,
+                                             "peak_entries_per_s": floor_entries,
+                                             "frac": entries_per_s / floor_entries,
+                                             "source": "measured instruction cost (ubench_umma), not a vendor peak"}
     else:
         fp32_peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
         roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
