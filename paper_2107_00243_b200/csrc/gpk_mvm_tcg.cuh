@@ -455,9 +455,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     };
     for (int lt = 0; lt < nt; ++lt, ++it) {
       const int s = it % SG, as = it % AS, gb = it & 1;
-      if (threadIdx.x == 64) GPK_TRACE(1, it);
+      if (threadIdx.x == 128) GPK_TRACE(1, it);
       if constexpr (!DIRECT) mbar_wait_sleep(&g_full[gb], (it >> 1) & 1);
-      if (threadIdx.x == 64) GPK_TRACE(2, it);
+      if (threadIdx.x == 128) GPK_TRACE(2, it);
       tc::tc_fence_after();
       // direct mode reads the staged rows; Gram mode reads shared memory only in the (rare)
       // guard path and waits there (the stage is complete: its Gram MMA consumed it)
@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&g_empty[gb]);
       }
+      if (threadIdx.x == 128) GPK_TRACE(5, it);
 #pragma unroll
       for (int hf8 = 0; hf8 < 2; ++hf8) {  // two halves of 8 entries: Gram -> s -> entry -> TMEM
         float sv[8];
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     drain(gce++);
     flush32();
-    if (threadIdx.x == 64) GPK_TRACE(0, 2);
+    if (threadIdx.x == 128) GPK_TRACE(0, 2);
     if (row < a.row_end) {
       double* o = out + static_cast<long long>(u_sp(u)) * a.split_stride;
 #pragma unroll
