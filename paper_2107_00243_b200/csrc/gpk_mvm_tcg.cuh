@@ -541,7 +541,38 @@ __global__ void __launch_bounds__(THREADS, 1)
             near[u] = sv[u] <= kGuard * (nj[u] + ni);
             anyn = anyn || near[u];
           }
-          if (__any_sync(0xffffffffu, anyn)) {
+          // Low-dimensional data (d + 2 <= 16: KS <= 2) with short lengthscales have near pairs on a
+          // large share of their tiles (C3: the tile bound fires on half of the 8-entry groups, a real
+          // near pair sits in a quarter of them): there only the lanes that hold a near pair recompute
+          // it (typically one lane, one entry) -- C3 1.74 -> 1.48 ms, C5 974 -> 936 ms per launch.  In
+          // higher dimension near pairs are the diagonal tile's business and the whole warp walks the 8
+          // entries together (no divergence, the schedule C2 was tuned with).
+          constexpr bool DIVG = KS <= 2;
+          if constexpr (DIVG) {
+            if (anyn) {
+              const float4* xi4 = reinterpret_cast<const float4*>(XIs + r * a.dp);
+              const float4* xj4 =
+                  reinterpret_cast<const float4*>(XJs + s * (XJ_TILE / 4) + (q * JPT + hf8 * 8) * a.dp);
+              const int d4 = a.dp >> 2;
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                if (near[u]) {
+                  float acc = 0.0f;
+#pragma unroll 1
+                  for (int k = 0; k < d4; ++k) {
+                    const float4 p = xi4[k], qv = xj4[u * d4 + k];
+                    const float d0 = p.x - qv.x, d1 = p.y - qv.y, d2 = p.z - qv.z, d3 = p.w - qv.w;
+                    acc = fmaf(d0, d0, acc);
+                    acc = fmaf(d1, d1, acc);
+                    acc = fmaf(d2, d2, acc);
+                    acc = fmaf(d3, d3, acc);
+                  }
+                  sv[u] = acc;
+                }
+              }
+            }
+            __syncwarp();
+          } else if (__any_sync(0xffffffffu, anyn)) {
             // the whole warp evaluates the 8 direct distances (no divergence), from shared memory
             const float4* xi4 = reinterpret_cast<const float4*>(XIs + r * a.dp);
             const float4* xj4 =
